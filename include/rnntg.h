@@ -1,0 +1,192 @@
+/*
+ * rnntg — B200 (sm_100a) one-symbol-per-frame transducer decoding.
+ *
+ * Plain C ABI over the CUDA library paper_2211_00484_b200/librnntg.so.
+ * No torch types, no C++ types: pointers, sizes and POD parameter structs.
+ *
+ * Each entry point replaces one public function of the reference C++ library
+ * (rnnt-kit, /root/reference/proj/include/rnnt):
+ *
+ *   rnntg_model_create          <- init_model / ToyTransducer weights
+ *                                  (model.hpp:61-90, 129-169; weights in
+ *                                  param_views naming, model.hpp:75-82)
+ *   rnntg_greedy_search_batch   <- greedy_search_batch   (search.hpp:107-167)
+ *   rnntg_beam_search_batch     <- beam_search, S = 1    (search.hpp:206-277),
+ *                                  batched over utterances like the CLI's
+ *                                  parallel_for (tools/rnnt_main.cpp:274-287)
+ *   rnntg_graph_create          <- Fsa / make_fsa        (fsa.hpp:54-111)
+ *   rnntg_fsa_beam_search       <- fsa_beam_search       (fsa_search.hpp:326-387)
+ *                                  + lattice_to_best_seq(kMax) (394-409)
+ *                                  + best_path(...).score (fsa.hpp:345-376)
+ *
+ * The reference takes acoustic features and runs its toy encoder inside the
+ * search; the north-star boundary takes encoder frames (the encoder is the
+ * caller's).  include/rnnt_gpu.hpp restores the exact
+ * reference signatures on top of this ABI by running the reference encoder
+ * on the host first.
+ *
+ * Errors: every call returns an rnntg_status; rnntg_last_error() gives the
+ * message of the calling thread's last failure.  INVALID_ARGUMENT is the
+ * reference's ValidationError; INTERNAL is its std::logic_error.
+ *
+ * Threading: a model handle owns one CUDA device, one CUDA stream and its
+ * scratch memory; calls on a handle are serialised, different handles may be
+ * used from different threads.  Graph handles are read-only once created and
+ * may be shared by the decode calls of the handle they were created on.
+ */
+#ifndef RNNTG_H_
+#define RNNTG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RNNTG_OK = 0,
+  RNNTG_INVALID_ARGUMENT = 1, /* reference ValidationError */
+  RNNTG_INTERNAL = 2,         /* reference std::logic_error */
+  RNNTG_CUDA_ERROR = 3,
+  RNNTG_UNSUPPORTED = 4       /* valid for the reference, beyond a device cap */
+} rnntg_status;
+
+/* Where the frame / result buffers of a decode call live. */
+typedef enum {
+  RNNTG_MEM_HOST = 0,   /* host memory: H2D and D2H copies inside the call */
+  RNNTG_MEM_DEVICE = 1  /* device memory on the model's GPU */
+} rnntg_mem;
+
+typedef enum { RNNTG_MERGE_MAX = 0, RNNTG_MERGE_LOG_ADD = 1 } rnntg_merge_op;
+
+/* Joiner arithmetic.  EXACT reproduces the reference's fp32 logits bit for
+ * bit (sequential non-fused fp32 on CUDA cores + a glibc-2.39 tanhf port).
+ * BF16 runs the output projection on tcgen05 tensor cores with bf16 operands
+ * and fp32 accumulation; it is the separately reported fast variant and is
+ * NOT token-exact. */
+typedef enum { RNNTG_JOINER_EXACT = 0, RNNTG_JOINER_BF16 = 1 } rnntg_joiner_mode;
+
+typedef struct rnntg_model_s* rnntg_model_t;
+typedef struct rnntg_graph_s* rnntg_graph_t;
+
+/* Stateless-transducer weights, fp32 row-major host arrays in the
+ * reference's param_views naming (model.hpp:75-82).  context_size must be 2. */
+typedef struct {
+  int32_t vocab_size;   /* V, blank = 0 */
+  int32_t enc_dim;      /* D */
+  int32_t emb_dim;      /* E */
+  int32_t joiner_dim;   /* J (<= 512, as model.hpp:287-288) */
+  int32_t context_size; /* must be 2 */
+  const float* emb;     /* [V][E]   */
+  const float* ctx_w;   /* [E][2E]  */
+  const float* ctx_b;   /* [E]      */
+  const float* j_we;    /* [J][D]   */
+  const float* j_wd;    /* [J][E]   */
+  const float* j_b;     /* [J]      */
+  const float* out_w;   /* [V][J]   */
+  const float* out_b;   /* [V]      */
+} rnntg_model_desc;
+
+/* SearchParams (search.hpp:44-50) restricted to max_symbols = 1. */
+typedef struct {
+  int32_t beam_size;         /* >= 1 */
+  int32_t max_symbols;       /* must be 1 (one symbol per frame) */
+  int32_t merge_op;          /* rnntg_merge_op */
+  int32_t length_norm;       /* 0/1 */
+  int32_t max_total_symbols; /* 0 = uncapped */
+} rnntg_beam_params;
+
+/* FsaSearchParams (fsa_search.hpp:33-37). */
+typedef struct {
+  double beam;          /* >= 0 */
+  int32_t max_states;   /* >= 1 */
+  int32_t max_contexts; /* >= 1 */
+} rnntg_fsa_params;
+
+/* Per-call counters (device-side, for the roofline and occupancy report). */
+typedef struct {
+  int64_t stream_frames;  /* sum over streams of frames decoded */
+  int64_t joiner_rows;    /* joiner rows evaluated (distinct contexts) */
+  int64_t arcs_expanded;  /* FSA: graph arcs expanded */
+  int64_t lattice_arcs;   /* FSA: lattice arcs kept */
+  int64_t tie_breaks;     /* exact-score ties resolved by the tie rules */
+  int64_t kernel_launches;/* CUDA kernels launched by the call */
+  float gpu_ms;           /* device time of the call (CUDA events) */
+  float decode_ms;        /* device time of the persistent decode kernel */
+} rnntg_stats;
+
+const char* rnntg_last_error(void);
+const char* rnntg_version(void);
+
+rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
+                                rnntg_model_t* out);
+rnntg_status rnntg_model_destroy(rnntg_model_t model);
+/* Use `stream` (a cudaStream_t) for all work of this handle; NULL = the
+ * handle's own stream. */
+rnntg_status rnntg_set_stream(rnntg_model_t model, void* stream);
+rnntg_status rnntg_set_joiner_mode(rnntg_model_t model, int32_t mode);
+rnntg_status rnntg_get_stats(rnntg_model_t model, rnntg_stats* out);
+
+/*
+ * Frames: `enc` is [frame_splits[B]][enc_dim] fp32, stream i owning rows
+ * frame_splits[i] .. frame_splits[i+1]-1 (a ragged batch, like the
+ * reference's std::vector<Mat<float>>).  frame_splits is always host memory.
+ *
+ * Results: ragged token lists.  out_splits[B+1] (host memory) receives the
+ * prefix sums; out_tokens must hold frame_splits[B] int32 (S = 1 bounds each
+ * stream by its frame count); out_scores (may be NULL) receives one fp64
+ * score per stream.  `mem` says where enc / out_tokens / out_scores live.
+ */
+rnntg_status rnntg_greedy_search_batch(rnntg_model_t model, const float* enc,
+                                       const int32_t* frame_splits, int32_t B,
+                                       int32_t max_symbols, int32_t mem,
+                                       int32_t* out_splits,
+                                       int32_t* out_tokens);
+
+rnntg_status rnntg_beam_search_batch(rnntg_model_t model, const float* enc,
+                                     const int32_t* frame_splits, int32_t B,
+                                     const rnntg_beam_params* params,
+                                     int32_t mem, int32_t* out_splits,
+                                     int32_t* out_tokens, double* out_scores);
+
+/* Decoding graph: CSR arcs grouped by source state (arcs of state s are
+ * arc_splits[s] .. arc_splits[s+1]-1, in the order best-path tie rules see
+ * them), natural-log fp64 weights.  Labels must be in [1, V) (graphs are
+ * epsilon-free, fsa_search.hpp:103-111).  Host memory. */
+rnntg_status rnntg_graph_create(rnntg_model_t model, int32_t num_states,
+                                const int32_t* arc_splits, int32_t num_arcs,
+                                const int32_t* dst, const int32_t* label,
+                                const double* weight, rnntg_graph_t* out);
+rnntg_status rnntg_graph_destroy(rnntg_graph_t graph);
+
+/* One shared graph for all streams (the CLI decodes every utterance with the
+ * same graph, rnnt_main.cpp:297).  out_scores = best_path score per stream,
+ * -inf when the lattice has no complete path. */
+rnntg_status rnntg_fsa_beam_search(rnntg_model_t model, const float* enc,
+                                   const int32_t* frame_splits, int32_t B,
+                                   rnntg_graph_t graph,
+                                   const rnntg_fsa_params* params, int32_t mem,
+                                   int32_t* out_splits, int32_t* out_tokens,
+                                   double* out_scores);
+
+/* Kernel-level entry points (bit-exactness tests of the joiner pieces).
+ * All pointers are host memory. */
+rnntg_status rnntg_debug_decoder_projection(rnntg_model_t model,
+                                            const int32_t* contexts, int32_t n,
+                                            float* pd_out);
+rnntg_status rnntg_debug_joiner_logits(rnntg_model_t model, const float* enc,
+                                       const int32_t* contexts, int32_t n,
+                                       float* logits_out);
+/* tanhf port over x[i], i < n (exhaustive sweep support): writes a 64-bit
+ * FNV-style hash of the output bits of every 2^24-input chunk starting at
+ * chunk `first_chunk` into hashes[0..num_chunks). */
+rnntg_status rnntg_debug_tanhf_chunk_hashes(int32_t device, int32_t first_chunk,
+                                            int32_t num_chunks,
+                                            uint64_t* hashes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RNNTG_H_ */

@@ -1,0 +1,367 @@
+"""ctypes mirror of the reference decoder API over librnntg.so.
+
+Reference (rnnt-kit) -> here:
+  greedy_search_batch(m, batch, 1)         search.hpp:107-167  -> Decoder.greedy_search_batch
+  beam_search(m, f, SearchParams)          search.hpp:206-277  -> Decoder.beam_search / beam_search_batch
+  fsa_beam_search + lattice_to_best_seq    fsa_search.hpp:326-426 -> Decoder.fsa_beam_search
+  Fsa (CSR arcs)                           fsa.hpp:54-80       -> Graph
+
+Inputs are encoder frames (the reference runs its toy encoder inside each
+search; the north-star boundary starts at the encoder output).  Errors map to
+the reference's exception types: ValidationError (bad arguments) and
+LogicError (internal inconsistency).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import build as _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = _build.LIB
+
+PARAM_NAMES = ("emb", "ctx_w", "ctx_b", "j_we", "j_wd", "j_b", "out_w", "out_b")
+
+OK, INVALID_ARGUMENT, INTERNAL, CUDA_ERROR, UNSUPPORTED = range(5)
+MEM_HOST, MEM_DEVICE = 0, 1
+MERGE_MAX, MERGE_LOG_ADD = 0, 1
+
+
+class RnntgError(RuntimeError):
+    """CUDA or capability error from librnntg."""
+
+
+class ValidationError(RnntgError, ValueError):
+    """The reference's rnnt::ValidationError (common.hpp:38-40)."""
+
+
+class LogicError(RnntgError):
+    """The reference's std::logic_error."""
+
+
+class UnsupportedError(RnntgError):
+    """Valid for the reference, beyond a documented device cap."""
+
+
+class _Desc(C.Structure):
+    _fields_ = [
+        ("vocab_size", C.c_int32),
+        ("enc_dim", C.c_int32),
+        ("emb_dim", C.c_int32),
+        ("joiner_dim", C.c_int32),
+        ("context_size", C.c_int32),
+    ] + [(n, C.POINTER(C.c_float)) for n in PARAM_NAMES]
+
+
+class _BeamParams(C.Structure):
+    _fields_ = [
+        ("beam_size", C.c_int32),
+        ("max_symbols", C.c_int32),
+        ("merge_op", C.c_int32),
+        ("length_norm", C.c_int32),
+        ("max_total_symbols", C.c_int32),
+    ]
+
+
+class _FsaParams(C.Structure):
+    _fields_ = [("beam", C.c_double), ("max_states", C.c_int32), ("max_contexts", C.c_int32)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [
+        ("stream_frames", C.c_int64),
+        ("joiner_rows", C.c_int64),
+        ("arcs_expanded", C.c_int64),
+        ("lattice_arcs", C.c_int64),
+        ("tie_breaks", C.c_int64),
+        ("kernel_launches", C.c_int64),
+        ("gpu_ms", C.c_float),
+        ("decode_ms", C.c_float),
+    ]
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(lib_path):
+        # Build in-tree (nvcc cross-compiles without a GPU); never fall back.
+        _build.build()
+    lib = C.CDLL(lib_path)
+    vp, i32, i32p, f32p, f64p = C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p, C.c_void_p
+    lib.rnntg_last_error.restype = C.c_char_p
+    lib.rnntg_version.restype = C.c_char_p
+    lib.rnntg_model_create.argtypes = [C.POINTER(_Desc), i32, C.POINTER(vp)]
+    lib.rnntg_model_destroy.argtypes = [vp]
+    lib.rnntg_set_stream.argtypes = [vp, vp]
+    lib.rnntg_set_joiner_mode.argtypes = [vp, i32]
+    lib.rnntg_get_stats.argtypes = [vp, C.POINTER(_Stats)]
+    lib.rnntg_greedy_search_batch.argtypes = [vp, f32p, i32p, i32, i32, i32, i32p, vp]
+    lib.rnntg_beam_search_batch.argtypes = [vp, f32p, i32p, i32, C.POINTER(_BeamParams), i32, i32p, vp, f64p]
+    lib.rnntg_graph_create.argtypes = [vp, i32, i32p, i32, i32p, i32p, f64p, C.POINTER(vp)]
+    lib.rnntg_graph_destroy.argtypes = [vp]
+    lib.rnntg_fsa_beam_search.argtypes = [vp, f32p, i32p, i32, vp, C.POINTER(_FsaParams), i32, i32p, vp, f64p]
+    lib.rnntg_debug_decoder_projection.argtypes = [vp, i32p, i32, f32p]
+    lib.rnntg_debug_joiner_logits.argtypes = [vp, f32p, i32p, i32, f32p]
+    lib.rnntg_debug_tanhf_chunk_hashes.argtypes = [i32, i32, i32, C.POINTER(C.c_uint64)]
+    for f in (
+        "rnntg_model_create",
+        "rnntg_model_destroy",
+        "rnntg_set_stream",
+        "rnntg_set_joiner_mode",
+        "rnntg_get_stats",
+        "rnntg_greedy_search_batch",
+        "rnntg_beam_search_batch",
+        "rnntg_graph_create",
+        "rnntg_graph_destroy",
+        "rnntg_fsa_beam_search",
+        "rnntg_debug_decoder_projection",
+        "rnntg_debug_joiner_logits",
+        "rnntg_debug_tanhf_chunk_hashes",
+    ):
+        getattr(lib, f).restype = C.c_int
+    _lib = lib
+    return lib
+
+
+def _check(rc):
+    if rc == OK:
+        return
+    msg = _load().rnntg_last_error().decode()
+    raise {INVALID_ARGUMENT: ValidationError, INTERNAL: LogicError, UNSUPPORTED: UnsupportedError}.get(
+        rc, RnntgError
+    )(msg)
+
+
+def _ptr(a):
+    return C.c_void_p(a.ctypes.data)
+
+
+def _i32p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+@dataclass
+class ModelWeights:
+    """Stateless-transducer weights in param_views naming (model.hpp:75-82)."""
+
+    V: int
+    D: int
+    E: int
+    J: int
+    p: dict
+
+    @staticmethod
+    def from_dict(p: dict) -> "ModelWeights":
+        V, E = p["emb"].shape
+        J, D = p["j_we"].shape
+        return ModelWeights(V, D, E, J, {n: np.ascontiguousarray(p[n], np.float32) for n in PARAM_NAMES})
+
+
+@dataclass
+class BeamParams:
+    """SearchParams (search.hpp:44-50) at max_symbols = 1."""
+
+    beam_size: int = 4
+    max_symbols: int = 1
+    merge_op: int = MERGE_MAX
+    length_norm: bool = False
+    max_total_symbols: int = 0
+
+
+@dataclass
+class FsaParams:
+    """FsaSearchParams (fsa_search.hpp:33-37)."""
+
+    beam: float = 20.0
+    max_states: int = 64
+    max_contexts: int = 8
+
+
+def _frames(enc, frame_splits):
+    """(pointer, mem kind, keepalive) for host numpy / torch tensors."""
+    splits = np.ascontiguousarray(frame_splits, np.int32)
+    if hasattr(enc, "data_ptr"):  # torch tensor
+        if enc.dtype.__str__() != "torch.float32" or not enc.is_contiguous():
+            raise ValidationError("enc must be a contiguous float32 tensor")
+        mem = MEM_DEVICE if enc.is_cuda else MEM_HOST
+        return C.c_void_p(enc.data_ptr()), mem, splits, enc
+    a = np.ascontiguousarray(enc, np.float32)
+    return _ptr(a), MEM_HOST, splits, a
+
+
+def _ragged(splits, flat):
+    return [flat[splits[i] : splits[i + 1]].tolist() for i in range(len(splits) - 1)]
+
+
+class Graph:
+    """Device copy of a CSR decoding graph (fsa.hpp:54-80)."""
+
+    def __init__(self, decoder: "Decoder", num_states, arc_splits, dst, label, weight):
+        lib = _load()
+        self._lib = lib
+        self.num_states = int(num_states)
+        arc_splits = np.ascontiguousarray(arc_splits, np.int32)
+        dst = np.ascontiguousarray(dst, np.int32)
+        label = np.ascontiguousarray(label, np.int32)
+        weight = np.ascontiguousarray(weight, np.float64)
+        self.num_arcs = int(dst.shape[0])
+        h = C.c_void_p()
+        _check(
+            lib.rnntg_graph_create(
+                decoder.h,
+                self.num_states,
+                _i32p(arc_splits),
+                self.num_arcs,
+                _i32p(dst),
+                _i32p(label),
+                _ptr(weight),
+                C.byref(h),
+            )
+        )
+        self.h = h
+
+    @staticmethod
+    def trivial(decoder: "Decoder") -> "Graph":
+        """trivial_graph (fsa.hpp:266-273): one state, self-loops 1..V-1, score 0."""
+        V = decoder.V
+        return Graph(
+            decoder,
+            1,
+            np.array([0, V - 1], np.int32),
+            np.zeros(V - 1, np.int32),
+            np.arange(1, V, dtype=np.int32),
+            np.zeros(V - 1, np.float64),
+        )
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.rnntg_graph_destroy(self.h)
+            self.h = None
+
+
+class Decoder:
+    """A model resident on one GPU (rnntg_model_t)."""
+
+    def __init__(self, weights: ModelWeights, device: int = 0):
+        lib = _load()
+        self._lib = lib
+        self.w = weights
+        self.V, self.D, self.E, self.J = weights.V, weights.D, weights.E, weights.J
+        arrs = [np.ascontiguousarray(weights.p[n], np.float32) for n in PARAM_NAMES]
+        desc = _Desc(
+            weights.V,
+            weights.D,
+            weights.E,
+            weights.J,
+            2,
+            *[a.ctypes.data_as(C.POINTER(C.c_float)) for a in arrs],
+        )
+        h = C.c_void_p()
+        _check(lib.rnntg_model_create(C.byref(desc), device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.rnntg_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def set_stream(self, stream_handle: int | None):
+        _check(self._lib.rnntg_set_stream(self.h, C.c_void_p(stream_handle or 0)))
+
+    def stats(self) -> dict:
+        s = _Stats()
+        _check(self._lib.rnntg_get_stats(self.h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in _Stats._fields_}
+
+    # ---- searches ----
+    def greedy_search_batch(self, enc, frame_splits, max_symbols=1, out_tokens=None):
+        p, mem, splits, keep = _frames(enc, frame_splits)
+        B = len(splits) - 1
+        osp = np.zeros(B + 1, np.int32)
+        if mem == MEM_DEVICE:
+            tok, tokp = out_tokens, C.c_void_p(out_tokens.data_ptr())
+        else:
+            tok = np.zeros(max(1, int(splits[-1])), np.int32)
+            tokp = _ptr(tok)
+        _check(self._lib.rnntg_greedy_search_batch(self.h, p, _i32p(splits), B, max_symbols, mem, _i32p(osp), tokp))
+        if mem == MEM_DEVICE:
+            return osp, tok
+        return _ragged(osp, tok)
+
+    def beam_search_batch(self, enc, frame_splits, params: BeamParams = BeamParams(), out_tokens=None, out_scores=None):
+        p, mem, splits, keep = _frames(enc, frame_splits)
+        B = len(splits) - 1
+        osp = np.zeros(B + 1, np.int32)
+        bp = _BeamParams(
+            params.beam_size, params.max_symbols, params.merge_op, int(params.length_norm), params.max_total_symbols
+        )
+        if mem == MEM_DEVICE:
+            tokp, scp = C.c_void_p(out_tokens.data_ptr()), C.c_void_p(out_scores.data_ptr())
+        else:
+            tok = np.zeros(max(1, int(splits[-1])), np.int32)
+            sc = np.zeros(max(1, B), np.float64)
+            tokp, scp = _ptr(tok), _ptr(sc)
+        _check(self._lib.rnntg_beam_search_batch(self.h, p, _i32p(splits), B, C.byref(bp), mem, _i32p(osp), tokp, scp))
+        if mem == MEM_DEVICE:
+            return osp, out_tokens, out_scores
+        return _ragged(osp, tok), sc[:B].copy()
+
+    def beam_search(self, enc_one, params: BeamParams = BeamParams()):
+        """Per-utterance form of the reference's beam_search (returns ys)."""
+        enc_one = np.ascontiguousarray(enc_one, np.float32)
+        ys, _ = self.beam_search_batch(enc_one, [0, enc_one.shape[0]], params)
+        return ys[0]
+
+    def fsa_beam_search(self, enc, frame_splits, graph: Graph, params: FsaParams = FsaParams()):
+        p, mem, splits, keep = _frames(enc, frame_splits)
+        B = len(splits) - 1
+        osp = np.zeros(B + 1, np.int32)
+        tok = np.zeros(max(1, int(splits[-1])), np.int32)
+        sc = np.zeros(max(1, B), np.float64)
+        fp = _FsaParams(float(params.beam), int(params.max_states), int(params.max_contexts))
+        _check(
+            self._lib.rnntg_fsa_beam_search(
+                self.h, p, _i32p(splits), B, graph.h, C.byref(fp), mem, _i32p(osp), _ptr(tok), _ptr(sc)
+            )
+        )
+        return _ragged(osp, tok), sc[:B].copy()
+
+    # ---- kernel-level parity ----
+    def decoder_projection(self, ctxs):
+        ctxs = np.ascontiguousarray(ctxs, np.int32)
+        out = np.zeros((len(ctxs), self.J), np.float32)
+        _check(self._lib.rnntg_debug_decoder_projection(self.h, _i32p(ctxs), len(ctxs), _ptr(out)))
+        return out
+
+    def joiner_logits(self, enc_rows, ctxs):
+        enc_rows = np.ascontiguousarray(enc_rows, np.float32)
+        ctxs = np.ascontiguousarray(ctxs, np.int32)
+        out = np.zeros((len(ctxs), self.V), np.float32)
+        _check(self._lib.rnntg_debug_joiner_logits(self.h, _ptr(enc_rows), _i32p(ctxs), len(ctxs), _ptr(out)))
+        return out
+
+
+def tanhf_chunk_hashes(first_chunk=0, num_chunks=256, device=0):
+    out = (C.c_uint64 * num_chunks)()
+    _check(_load().rnntg_debug_tanhf_chunk_hashes(device, first_chunk, num_chunks, out))
+    return [int(x) for x in out]
+
+
+def exported_symbols():
+    """Names declared in include/rnntg.h (for the ABI export test)."""
+    import re
+
+    hdr = open(os.path.join(_HERE, "..", "include", "rnntg.h")).read()
+    return sorted(set(re.findall(r"\b(rnntg_[a-z_0-9]+)\s*\(", hdr)))

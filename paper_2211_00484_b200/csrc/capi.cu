@@ -1,0 +1,548 @@
+// C ABI of librnntg.so (include/rnntg.h): argument validation mirroring the
+// reference's checks, device model construction, and the decode drivers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace rnntg {
+
+static thread_local std::string g_error;
+void set_error(const std::string& msg) { g_error = msg; }
+
+}  // namespace rnntg
+
+using rnntg::Scratch;
+using rnntg::set_error;
+
+struct rnntg_model_s {
+  int device = 0;
+  rnntg::DeviceModel d;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int num_sms = 1;
+  int joiner_mode = RNNTG_JOINER_EXACT;
+  Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  rnntg_stats stats{};
+  std::mutex mu;
+  std::vector<void*> owned;  // device weight buffers
+};
+
+struct rnntg_graph_s {
+  rnntg_model_t model = nullptr;
+  int32_t num_states = 0, num_arcs = 0;
+  int32_t* splits = nullptr;  // device [S+1]
+  void* arcs = nullptr;       // device 16-byte records {dst, label, weight}
+};
+
+namespace {
+
+int32_t round_up(int32_t x, int32_t m) { return (x + m - 1) / m * m; }
+
+rnntg_status invalid(const std::string& msg) {
+  set_error(msg);
+  return RNNTG_INVALID_ARGUMENT;
+}
+
+template <typename T>
+rnntg_status upload(rnntg_model_t h, T** dst, const std::vector<T>& src) {
+  RNNTG_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(dst), sizeof(T) * std::max<size_t>(1, src.size())));
+  h->owned.push_back(*dst);
+  RNNTG_CUDA_TRY(cudaMemcpy(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice));
+  return RNNTG_OK;
+}
+
+// k-major transpose with zero-padded columns: out[k][n] = w[n][k].
+std::vector<float> transpose_pad(const float* w, int32_t N, int32_t K, int32_t ldo) {
+  std::vector<float> out(static_cast<size_t>(K) * ldo, 0.0f);
+  for (int32_t n = 0; n < N; ++n)
+    for (int32_t k = 0; k < K; ++k) out[static_cast<size_t>(k) * ldo + n] = w[static_cast<size_t>(n) * K + k];
+  return out;
+}
+
+// Validates the frame layout (one Mat per stream in the reference).
+rnntg_status check_frames(const float* enc, const int32_t* fs, int32_t B) {
+  if (B < 0) return invalid("batch size must be >= 0");
+  if (B > 0 && fs == nullptr) return invalid("frame_splits is null");
+  if (B > 0 && fs[0] != 0) return invalid("frame_splits[0] must be 0");
+  for (int32_t i = 0; i < B; ++i)
+    if (fs[i + 1] < fs[i]) return invalid("frame_splits must be non-decreasing");
+  if (B > 0 && fs[B] > 0 && enc == nullptr) return invalid("enc is null");
+  return RNNTG_OK;
+}
+
+// Common front half of a decode call: frames on the device, pe = j_we . enc.
+rnntg_status prepare(rnntg_model_t h, const float* enc, const int32_t* fs,
+                     int32_t B, int32_t mem, const float** d_enc) {
+  const int64_t total = B > 0 ? fs[B] : 0;
+  const int32_t D = h->d.D, J = h->d.J;
+  RNNTG_CUDA_TRY(h->splits.ensure(sizeof(int32_t) * (B + 1)));
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(h->splits.ptr, fs, sizeof(int32_t) * (B + 1),
+                                 cudaMemcpyHostToDevice, h->stream));
+  if (mem == RNNTG_MEM_HOST) {
+    RNNTG_CUDA_TRY(h->enc.ensure(sizeof(float) * std::max<int64_t>(1, total) * D));
+    if (total > 0)
+      RNNTG_CUDA_TRY(cudaMemcpyAsync(h->enc.ptr, enc, sizeof(float) * total * D,
+                                     cudaMemcpyHostToDevice, h->stream));
+    *d_enc = h->enc.as<float>();
+  } else {
+    *d_enc = enc;
+  }
+  RNNTG_CUDA_TRY(h->pe.ensure(sizeof(float) * std::max<int64_t>(1, total) * J));
+  RNNTG_CUDA_TRY(h->tok.ensure(sizeof(int32_t) * std::max<int64_t>(1, total)));
+  RNNTG_CUDA_TRY(h->len.ensure(sizeof(int32_t) * std::max(1, B)));
+  RNNTG_CUDA_TRY(h->score.ensure(sizeof(double) * std::max(1, B)));
+  RNNTG_CUDA_TRY(h->counters.ensure(sizeof(unsigned long long) * 8));
+  RNNTG_CUDA_TRY(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long) * 8, h->stream));
+  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
+  if (total > 0)
+    RNNTG_CUDA_TRY(rnntg::launch_gemm_exact(*d_enc, D, h->d.j_wet, h->d.Jp, nullptr,
+                                            h->pe.as<float>(), J, total, J, D, false,
+                                            nullptr, 0, 0, h->stream));
+  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+  return RNNTG_OK;
+}
+
+__global__ void compact_tokens_kernel(const int32_t* __restrict__ slot_tokens,
+                                      const int32_t* __restrict__ fs,
+                                      const int32_t* __restrict__ out_splits,
+                                      int32_t B, int32_t* __restrict__ out) {
+  const int s = blockIdx.x;
+  if (s >= B) return;
+  const int32_t n = out_splits[s + 1] - out_splits[s];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[out_splits[s] + i] = slot_tokens[fs[s] + i];
+}
+
+// Common back half: lengths -> out_splits, tokens compacted to the ragged
+// layout, scores, stats.
+rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
+                    int32_t* out_splits, int32_t* out_tokens, double* out_scores,
+                    int64_t launches) {
+  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[2], h->stream));
+  const int64_t total = B > 0 ? fs[B] : 0;
+  std::vector<int32_t> lens(std::max(1, B));
+  if (B > 0)
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(lens.data(), h->len.ptr, sizeof(int32_t) * B,
+                                   cudaMemcpyDeviceToHost, h->stream));
+  unsigned long long cnt[8];
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(cnt, h->counters.ptr, sizeof(cnt), cudaMemcpyDeviceToHost, h->stream));
+  RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  out_splits[0] = 0;
+  for (int32_t i = 0; i < B; ++i) out_splits[i + 1] = out_splits[i] + lens[i];
+  if (mem == RNNTG_MEM_HOST) {
+    if (total > 0) {
+      std::vector<int32_t> slots(total);
+      RNNTG_CUDA_TRY(cudaMemcpyAsync(slots.data(), h->tok.ptr, sizeof(int32_t) * total,
+                                     cudaMemcpyDeviceToHost, h->stream));
+      if (out_scores)
+        RNNTG_CUDA_TRY(cudaMemcpyAsync(out_scores, h->score.ptr, sizeof(double) * B,
+                                       cudaMemcpyDeviceToHost, h->stream));
+      RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+      for (int32_t i = 0; i < B; ++i)
+        std::memcpy(out_tokens + out_splits[i], slots.data() + fs[i], sizeof(int32_t) * lens[i]);
+    } else if (out_scores && B > 0) {
+      RNNTG_CUDA_TRY(cudaMemcpy(out_scores, h->score.ptr, sizeof(double) * B, cudaMemcpyDeviceToHost));
+    }
+  } else {
+    RNNTG_CUDA_TRY(h->out_splits.ensure(sizeof(int32_t) * (B + 1)));
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(h->out_splits.ptr, out_splits, sizeof(int32_t) * (B + 1),
+                                   cudaMemcpyHostToDevice, h->stream));
+    if (B > 0 && total > 0) {
+      compact_tokens_kernel<<<B, 128, 0, h->stream>>>(h->tok.as<int32_t>(), h->splits.as<int32_t>(),
+                                                      h->out_splits.as<int32_t>(), B, out_tokens);
+      RNNTG_CUDA_TRY(cudaGetLastError());
+      ++launches;
+    }
+    if (out_scores && B > 0)
+      RNNTG_CUDA_TRY(cudaMemcpyAsync(out_scores, h->score.ptr, sizeof(double) * B,
+                                     cudaMemcpyDeviceToDevice, h->stream));
+    RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  float ms_all = 0, ms_dec = 0;
+  cudaEventElapsedTime(&ms_all, h->ev[0], h->ev[2]);
+  cudaEventElapsedTime(&ms_dec, h->ev[1], h->ev[2]);
+  h->stats.stream_frames = static_cast<int64_t>(cnt[0]);
+  h->stats.joiner_rows = static_cast<int64_t>(cnt[1]);
+  h->stats.arcs_expanded = static_cast<int64_t>(cnt[2]);
+  h->stats.lattice_arcs = static_cast<int64_t>(cnt[3]);
+  h->stats.tie_breaks = static_cast<int64_t>(cnt[4]);
+  h->stats.kernel_launches = launches;
+  h->stats.gpu_ms = ms_all;
+  h->stats.decode_ms = ms_dec;
+  return RNNTG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rnntg_last_error(void) { return rnntg::g_error.c_str(); }
+const char* rnntg_version(void) { return "rnntg 0.1 (sm_100a)"; }
+
+rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
+                                rnntg_model_t* out) {
+  if (!desc || !out) return invalid("null argument");
+  *out = nullptr;
+  // check_config (model.hpp:174-182).
+  if (desc->vocab_size < 2) return invalid("vocab_size must be >= 2 (blank plus one token)");
+  if (desc->context_size != 2) return invalid("context_size must be 2");
+  if (desc->enc_dim < 1 || desc->emb_dim < 1 || desc->joiner_dim < 1)
+    return invalid("model dims must be >= 1");
+  if (desc->joiner_dim > rnntg::kMaxJoiner) return invalid("joiner_dim too large");
+  if (desc->vocab_size > rnntg::kMaxVocab) {
+    set_error("vocab_size > 512 is beyond this build's joiner row cap");
+    return RNNTG_UNSUPPORTED;
+  }
+  const float* ptrs[] = {desc->emb, desc->ctx_w, desc->ctx_b, desc->j_we,
+                         desc->j_wd, desc->j_b, desc->out_w, desc->out_b};
+  for (const float* p : ptrs)
+    if (!p) return invalid("model weight pointer is null");
+  const int32_t V = desc->vocab_size, D = desc->enc_dim, E = desc->emb_dim, J = desc->joiner_dim;
+  const double table_bytes = static_cast<double>(V) * V * J * 4.0;
+  if (table_bytes > 64.0 * (1ull << 30)) {
+    set_error("decoder context table exceeds 64 GiB");
+    return RNNTG_UNSUPPORTED;
+  }
+
+  RNNTG_CUDA_TRY(cudaSetDevice(device));
+  auto* h = new rnntg_model_s();
+  h->device = device;
+  auto fail = [&](rnntg_status st) {
+    rnntg_model_destroy(h);
+    return st;
+  };
+  if (cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    set_error("cudaStreamCreate failed");
+    delete h;
+    return RNNTG_CUDA_ERROR;
+  }
+  h->stream = h->own_stream;
+  for (auto& e : h->ev) cudaEventCreate(&e);
+  h->num_sms = rnntg::decode_num_sms(device);
+  rnntg::DeviceModel& d = h->d;
+  d.V = V;
+  d.D = D;
+  d.E = E;
+  d.J = J;
+  d.Vp = round_up(V, 256);
+  d.Ep = round_up(E, 128);
+  d.Jp = round_up(J, 128);
+  rnntg_status st;
+  if ((st = upload(h, &d.emb, std::vector<float>(desc->emb, desc->emb + static_cast<size_t>(V) * E))) ||
+      (st = upload(h, &d.ctx_wt, transpose_pad(desc->ctx_w, E, 2 * E, d.Ep))) ||
+      (st = upload(h, &d.ctx_b, std::vector<float>(desc->ctx_b, desc->ctx_b + E))) ||
+      (st = upload(h, &d.j_wet, transpose_pad(desc->j_we, J, D, d.Jp))) ||
+      (st = upload(h, &d.j_wdt, transpose_pad(desc->j_wd, J, E, d.Jp))) ||
+      (st = upload(h, &d.j_b, std::vector<float>(desc->j_b, desc->j_b + J))) ||
+      (st = upload(h, &d.out_wt, transpose_pad(desc->out_w, V, J, d.Vp))))
+    return fail(st);
+  {
+    std::vector<float> ob(d.Vp, 0.0f);
+    std::copy(desc->out_b, desc->out_b + V, ob.begin());
+    if ((st = upload(h, &d.out_b, ob))) return fail(st);
+  }
+  // K0: the decoder-side joiner projection of every packed context,
+  // pd[c] = j_wd . tanh(ctx_b + ctx_w . [emb[c/V]; emb[c%V]]), chunked.
+  const int64_t C = static_cast<int64_t>(V) * V;
+  if (cudaMalloc(reinterpret_cast<void**>(&d.pd_table), sizeof(float) * C * J) != cudaSuccess) {
+    set_error("cannot allocate the decoder context table");
+    return fail(RNNTG_CUDA_ERROR);
+  }
+  h->owned.push_back(d.pd_table);
+  const int64_t chunk = 32768;
+  float* dec = nullptr;
+  if (cudaMalloc(reinterpret_cast<void**>(&dec), sizeof(float) * chunk * E) != cudaSuccess) {
+    set_error("cannot allocate decoder scratch");
+    return fail(RNNTG_CUDA_ERROR);
+  }
+  for (int64_t c0 = 0; c0 < C; c0 += chunk) {
+    const int64_t n = std::min(chunk, C - c0);
+    cudaError_t e = rnntg::launch_gemm_exact(nullptr, 0, d.ctx_wt, d.Ep, d.ctx_b, dec, E, n, E,
+                                             2 * E, true, d.emb, V, c0, h->stream);
+    if (e == cudaSuccess)
+      e = rnntg::launch_gemm_exact(dec, E, d.j_wdt, d.Jp, nullptr, d.pd_table + c0 * J, J, n, J, E,
+                                   false, nullptr, 0, 0, h->stream);
+    if (e != cudaSuccess) {
+      cudaFree(dec);
+      set_error(std::string("decoder table: ") + cudaGetErrorString(e));
+      return fail(RNNTG_CUDA_ERROR);
+    }
+  }
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  cudaFree(dec);
+  if (e != cudaSuccess) {
+    set_error(std::string("decoder table: ") + cudaGetErrorString(e));
+    return fail(RNNTG_CUDA_ERROR);
+  }
+  *out = h;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_model_destroy(rnntg_model_t h) {
+  if (!h) return RNNTG_OK;
+  cudaSetDevice(h->device);
+  if (h->own_stream) cudaStreamSynchronize(h->own_stream);
+  for (void* p : h->owned) cudaFree(p);
+  for (Scratch* s : {&h->enc, &h->pe, &h->splits, &h->tok, &h->len, &h->score, &h->bp,
+                     &h->counters, &h->ctx, &h->out_tok, &h->out_splits, &h->logits})
+    s->release();
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_set_stream(rnntg_model_t h, void* stream) {
+  if (!h) return invalid("null model");
+  std::lock_guard<std::mutex> lk(h->mu);
+  h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own_stream;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_set_joiner_mode(rnntg_model_t h, int32_t mode) {
+  if (!h) return invalid("null model");
+  if (mode != RNNTG_JOINER_EXACT) {
+    set_error("bf16 tcgen05 joiner is not built in this version");
+    return RNNTG_UNSUPPORTED;
+  }
+  h->joiner_mode = mode;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_get_stats(rnntg_model_t h, rnntg_stats* out) {
+  if (!h || !out) return invalid("null argument");
+  *out = h->stats;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_greedy_search_batch(rnntg_model_t h, const float* enc,
+                                       const int32_t* fs, int32_t B,
+                                       int32_t max_symbols, int32_t mem,
+                                       int32_t* out_splits, int32_t* out_tokens) {
+  if (!h) return invalid("null model");
+  // search.hpp:110-111.
+  if (max_symbols != 1) return invalid("greedy_search_batch supports max_symbols = 1 only");
+  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
+  rnntg_status st = check_frames(enc, fs, B);
+  if (st) return st;
+  if (!out_splits) return invalid("out_splits is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  const float* d_enc = nullptr;
+  if ((st = prepare(h, enc, fs, B, mem, &d_enc))) return st;
+  int64_t launches = fs[B] > 0 ? 1 : 0;
+  if (B > 0) {
+    rnntg::DecodeArgs a{};
+    a.m = &h->d;
+    a.pe = h->pe.as<float>();
+    a.frame_splits = h->splits.as<int32_t>();
+    a.B = B;
+    a.streams_per_cta = std::min(32, std::max(1, (B + h->num_sms - 1) / h->num_sms));
+    a.tokens = h->tok.as<int32_t>();
+    a.lengths = h->len.as<int32_t>();
+    a.scores = h->score.as<double>();
+    a.counters = h->counters.as<unsigned long long>();
+    RNNTG_CUDA_TRY(cudaMemsetAsync(h->score.ptr, 0, sizeof(double) * B, h->stream));
+    RNNTG_CUDA_TRY(rnntg::launch_decode_greedy(a, h->stream));
+    ++launches;
+  }
+  return finish(h, fs, B, mem, out_splits, out_tokens, nullptr, launches);
+}
+
+rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
+                                     const int32_t* fs, int32_t B,
+                                     const rnntg_beam_params* p, int32_t mem,
+                                     int32_t* out_splits, int32_t* out_tokens,
+                                     double* out_scores) {
+  if (!h || !p) return invalid("null argument");
+  // beam_search validation, search.hpp:210-212.
+  if (p->max_symbols < 1) return invalid("max_symbols must be >= 1");
+  if (p->beam_size < 1) return invalid("beam_size must be >= 1");
+  if (p->max_symbols != 1) {
+    set_error("only one symbol per frame (max_symbols = 1) is implemented");
+    return RNNTG_UNSUPPORTED;
+  }
+  if (p->beam_size > rnntg::kMaxBeam) {
+    set_error("beam_size > 8 is beyond this build's per-stream hypothesis cap");
+    return RNNTG_UNSUPPORTED;
+  }
+  if (p->merge_op != RNNTG_MERGE_MAX && p->merge_op != RNNTG_MERGE_LOG_ADD) return invalid("bad merge_op");
+  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
+  rnntg_status st = check_frames(enc, fs, B);
+  if (st) return st;
+  if (!out_splits) return invalid("out_splits is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  const float* d_enc = nullptr;
+  if ((st = prepare(h, enc, fs, B, mem, &d_enc))) return st;
+  int64_t launches = fs[B] > 0 ? 1 : 0;
+  if (B > 0) {
+    const int64_t total = fs[B];
+    RNNTG_CUDA_TRY(h->bp.ensure(sizeof(uint32_t) * (total + B) * rnntg::kMaxBeam));
+    rnntg::DecodeArgs a{};
+    a.m = &h->d;
+    a.pe = h->pe.as<float>();
+    a.frame_splits = h->splits.as<int32_t>();
+    a.B = B;
+    const int gmax = std::max(1, 32 / p->beam_size);
+    a.streams_per_cta = std::min(gmax, std::max(1, (B + h->num_sms - 1) / h->num_sms));
+    a.tokens = h->tok.as<int32_t>();
+    a.lengths = h->len.as<int32_t>();
+    a.scores = h->score.as<double>();
+    a.counters = h->counters.as<unsigned long long>();
+    a.beam_size = p->beam_size;
+    a.merge_op = p->merge_op;
+    a.length_norm = p->length_norm;
+    a.max_total = p->max_total_symbols;
+    a.backptr = h->bp.as<uint32_t>();
+    RNNTG_CUDA_TRY(rnntg::launch_decode_beam(a, h->stream));
+    ++launches;
+  }
+  return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+}
+
+rnntg_status rnntg_graph_create(rnntg_model_t h, int32_t num_states,
+                                const int32_t* arc_splits, int32_t num_arcs,
+                                const int32_t* dst, const int32_t* label,
+                                const double* weight, rnntg_graph_t* out) {
+  if (!h || !out) return invalid("null argument");
+  *out = nullptr;
+  if (num_states < 1) return invalid("fsa must have at least one state");
+  if (num_arcs < 0 || !arc_splits) return invalid("bad arc list");
+  if (arc_splits[0] != 0 || arc_splits[num_states] != num_arcs)
+    return invalid("arc_splits must start at 0 and end at num_arcs");
+  for (int32_t s = 0; s < num_states; ++s)
+    if (arc_splits[s + 1] < arc_splits[s]) return invalid("arc_splits must be non-decreasing");
+  for (int32_t a = 0; a < num_arcs; ++a) {
+    if (dst[a] < 0 || dst[a] >= num_states) return invalid("arc references state out of range");
+    // init_streams, fsa_search.hpp:103-111.
+    if (label[a] == 0) return invalid("decoding graph contains a blank/epsilon (label 0) arc");
+    if (label[a] < 0 || label[a] >= h->d.V)
+      return invalid("decoding graph label " + std::to_string(label[a]) + " outside model vocabulary");
+    if (!std::isfinite(weight[a])) return invalid("arc score must be finite");
+  }
+  std::lock_guard<std::mutex> lk(h->mu);
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  auto* g = new rnntg_graph_s();
+  g->model = h;
+  g->num_states = num_states;
+  g->num_arcs = num_arcs;
+  struct ArcRec {
+    int32_t dst, label;
+    double w;
+  };
+  std::vector<ArcRec> rec(std::max(1, num_arcs));
+  for (int32_t a = 0; a < num_arcs; ++a) rec[a] = {dst[a], label[a], weight[a]};
+  if (cudaMalloc(&g->arcs, sizeof(ArcRec) * rec.size()) != cudaSuccess ||
+      cudaMalloc(reinterpret_cast<void**>(&g->splits), sizeof(int32_t) * (num_states + 1)) != cudaSuccess) {
+    rnntg_graph_destroy(g);
+    set_error("cannot allocate the device graph");
+    return RNNTG_CUDA_ERROR;
+  }
+  cudaMemcpy(g->arcs, rec.data(), sizeof(ArcRec) * rec.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(g->splits, arc_splits, sizeof(int32_t) * (num_states + 1), cudaMemcpyHostToDevice);
+  *out = g;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_graph_destroy(rnntg_graph_t g) {
+  if (!g) return RNNTG_OK;
+  if (g->arcs) cudaFree(g->arcs);
+  if (g->splits) cudaFree(g->splits);
+  delete g;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
+                                   const int32_t* fs, int32_t B,
+                                   rnntg_graph_t graph,
+                                   const rnntg_fsa_params* p, int32_t mem,
+                                   int32_t* out_splits, int32_t* out_tokens,
+                                   double* out_scores) {
+  if (!h || !p || !graph) return invalid("null argument");
+  // check_fsa_search_params, fsa_search.hpp:83-90.
+  if (!(p->beam >= 0.0)) return invalid("fsa search beam must be >= 0");
+  if (p->max_states < 1) return invalid("max_states must be >= 1");
+  if (p->max_contexts < 1) return invalid("max_contexts must be >= 1");
+  (void)enc;
+  (void)fs;
+  (void)B;
+  (void)mem;
+  (void)out_splits;
+  (void)out_tokens;
+  (void)out_scores;
+  set_error("fsa_beam_search device path not built yet");
+  return RNNTG_UNSUPPORTED;
+}
+
+rnntg_status rnntg_debug_decoder_projection(rnntg_model_t h, const int32_t* ctxs,
+                                            int32_t n, float* pd_out) {
+  if (!h || (n > 0 && (!ctxs || !pd_out))) return invalid("null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  const int32_t J = h->d.J;
+  for (int32_t i = 0; i < n; ++i) {
+    if (ctxs[i] < 0 || ctxs[i] >= h->d.V * h->d.V) return invalid("packed context out of range");
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(pd_out + static_cast<size_t>(i) * J,
+                                   h->d.pd_table + static_cast<size_t>(ctxs[i]) * J,
+                                   sizeof(float) * J, cudaMemcpyDeviceToHost, h->stream));
+  }
+  RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_debug_joiner_logits(rnntg_model_t h, const float* enc,
+                                       const int32_t* ctxs, int32_t n,
+                                       float* logits_out) {
+  if (!h || (n > 0 && (!enc || !ctxs || !logits_out))) return invalid("null argument");
+  if (n <= 0) return RNNTG_OK;
+  std::lock_guard<std::mutex> lk(h->mu);
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  for (int32_t i = 0; i < n; ++i)
+    if (ctxs[i] < 0 || ctxs[i] >= h->d.V * h->d.V) return invalid("packed context out of range");
+  const int32_t D = h->d.D, J = h->d.J, V = h->d.V;
+  RNNTG_CUDA_TRY(h->enc.ensure(sizeof(float) * n * D));
+  RNNTG_CUDA_TRY(h->pe.ensure(sizeof(float) * n * J));
+  RNNTG_CUDA_TRY(h->ctx.ensure(sizeof(int32_t) * n));
+  RNNTG_CUDA_TRY(h->logits.ensure(sizeof(float) * n * V));
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(h->enc.ptr, enc, sizeof(float) * n * D, cudaMemcpyHostToDevice, h->stream));
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(h->ctx.ptr, ctxs, sizeof(int32_t) * n, cudaMemcpyHostToDevice, h->stream));
+  RNNTG_CUDA_TRY(rnntg::launch_gemm_exact(h->enc.as<float>(), D, h->d.j_wet, h->d.Jp, nullptr,
+                                          h->pe.as<float>(), J, n, J, D, false, nullptr, 0, 0,
+                                          h->stream));
+  RNNTG_CUDA_TRY(rnntg::launch_joiner_rows_exact(h->d, h->pe.as<float>(), h->ctx.as<int32_t>(), n,
+                                                 h->logits.as<float>(), h->stream));
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(logits_out, h->logits.ptr, sizeof(float) * n * V,
+                                 cudaMemcpyDeviceToHost, h->stream));
+  RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_debug_tanhf_chunk_hashes(int32_t device, int32_t first_chunk,
+                                            int32_t num_chunks, uint64_t* hashes) {
+  if (first_chunk < 0 || num_chunks < 1 || first_chunk + num_chunks > 256 || !hashes)
+    return invalid("chunk range must lie in [0, 256)");
+  RNNTG_CUDA_TRY(cudaSetDevice(device));
+  unsigned long long* d = nullptr;
+  RNNTG_CUDA_TRY(cudaMalloc(&d, sizeof(unsigned long long) * num_chunks));
+  cudaError_t e = rnntg::launch_tanhf_hash(first_chunk, num_chunks, d, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess)
+    e = cudaMemcpy(hashes, d, sizeof(unsigned long long) * num_chunks, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) {
+    set_error(cudaGetErrorString(e));
+    return RNNTG_CUDA_ERROR;
+  }
+  return RNNTG_OK;
+}
+
+}  // extern "C"

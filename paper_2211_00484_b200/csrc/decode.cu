@@ -1,0 +1,853 @@
+// Persistent, stream-stationary decode kernels (greedy / modified beam).
+//
+// One CTA owns a fixed group of G streams for the whole utterance and loops
+// over frames itself: streams are independent (batching transparency,
+// search_test.cpp:169-187, fsa_search_test.cpp:364-393), so no grid-wide
+// synchronisation and no per-frame kernel launch exists.  Per frame the CTA
+//
+//   A. lists its joiner rows: one per distinct (stream, packed context) —
+//      rows are a pure function of (stream, frame, context) (model.hpp:240),
+//      so hypotheses sharing a context share a row, bit-identically;
+//   B. builds h[r] = tanhf((pe + pd[ctx]) + j_b) in shared memory
+//      (joiner_logits_from_proj, model.hpp:284-292; pd from the K0 table);
+//   C. computes logits = out_b + out_w . h with sequential non-fused fp32 on
+//      CUDA cores, out_w streamed from L2 in 32 KB k-chunks by
+//      cp.async.bulk + mbarrier (double buffered, prefetching across frame
+//      boundaries because the chunk sequence is data independent);
+//   D. reduces each row: greedy first-max argmax (search.hpp:59-66); beam
+//      log-softmax normaliser (model.hpp:115-125) and the row's top-B tokens;
+//   E. advances each stream's search state (warp per stream).
+//
+// After the last frame a warp per stream traces the back-pointer lattice
+// (kept in HBM) and writes the token sequence.
+#include <float.h>
+#include <math.h>
+
+#include "exact_math.h"
+#include "internal.cuh"
+
+namespace rnntg {
+namespace {
+
+using rnntg_exact::fadd;
+using rnntg_exact::fmul;
+
+constexpr int kWarps = kDecodeThreads / 32;  // 16
+constexpr int kBK = 16;                      // k rows per out_w chunk
+constexpr int kRowCap = 32;                  // joiner rows per CTA per frame
+constexpr int kHStride = kRowCap + 4;        // padded k-major h tile stride
+
+struct ModelView {
+  int32_t V, J, Vp;
+  const float* __restrict__ out_wt;  // [J][Vp]
+  const float* __restrict__ out_b;   // [Vp]
+  const float* __restrict__ j_b;     // [J]
+  const float* __restrict__ pd;      // [V*V][J]
+};
+
+// ---------------------------------------------------------------------------
+// mbarrier + bulk copy helpers (sm_90+ PTX, SASS UBLKCP / SYNCS).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
+                                         uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// out_w chunk pipeline.  Chunk g (a running sequence number across frames)
+// holds k-rows [(g % nc) * kBK, ...) of out_wt and lives in stage g & 1.
+// ---------------------------------------------------------------------------
+struct WPipe {
+  float* stage[2];
+  uint64_t* bar;  // [2]
+  int32_t nc;     // chunks per frame
+};
+
+__device__ __forceinline__ void wpipe_issue(const WPipe& p, const ModelView& m,
+                                            uint32_t g) {
+  const int32_t c = static_cast<int32_t>(g % static_cast<uint32_t>(p.nc));
+  const int32_t rows = min(kBK, m.J - c * kBK);
+  const uint32_t bytes = static_cast<uint32_t>(rows) * m.Vp * 4u;
+  uint64_t* bar = p.bar + (g & 1u);
+  fence_proxy_async();
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(p.stage[g & 1u], m.out_wt + static_cast<int64_t>(c) * kBK * m.Vp,
+           bytes, bar);
+}
+
+// C. logits[r][n] = out_b[n] + sum_k out_w[n][k] * h[r][k], sequential in k.
+// Hs: k-major h tile [J][kHStride]; Ls (aliasing Hs): row-major [R][Vp].
+// Warp w owns rows 4*(w/NH) .. +3 and columns (w%NH)*256 + {4l..4l+3,
+// 128+4l..128+4l+3}, NH = Vp/256.
+__device__ __forceinline__ void joiner_gemm(const ModelView& m, const WPipe& p,
+                                            uint32_t& g, float* HL, int R) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NH = m.Vp >> 8;
+  const int items = ((R + 3) >> 2) * NH;
+  const bool active = warp < items;
+  const int rg = warp / NH, half = warp % NH;
+  const int col0 = half * 256 + lane * 4, col1 = col0 + 128;
+
+  float acc[4][8];
+  {
+    float4 b0 = make_float4(0, 0, 0, 0), b1 = b0;
+    if (active) {
+      b0 = *reinterpret_cast<const float4*>(m.out_b + col0);
+      b1 = *reinterpret_cast<const float4*>(m.out_b + col1);
+    }
+    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = bv[j];
+  }
+
+  for (int32_t c = 0; c < p.nc; ++c, ++g) {
+    const uint32_t st = g & 1u;
+    mbar_wait(p.bar + st, (g >> 1) & 1u);
+    if (active) {
+      const float* Ws = p.stage[st];
+      const int kk_end = min(kBK, m.J - c * kBK);
+      const float* hp = HL + static_cast<int64_t>(c * kBK) * kHStride + rg * 4;
+#pragma unroll 4
+      for (int kk = 0; kk < kk_end; ++kk) {
+        const float4 h4 = *reinterpret_cast<const float4*>(hp + kk * kHStride);
+        const float4 wa = *reinterpret_cast<const float4*>(Ws + kk * m.Vp + col0);
+        const float4 wb = *reinterpret_cast<const float4*>(Ws + kk * m.Vp + col1);
+        const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
+        const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            acc[i][j] = fadd(acc[i][j], fmul(wv[j], hv[i]));
+      }
+    }
+    __syncthreads();  // every warp is done with this stage
+    if (threadIdx.x == 0) wpipe_issue(p, m, g + 2);
+  }
+  // The last __syncthreads above also retired every read of Hs, so the logits
+  // may overwrite it.
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = rg * 4 + i;
+      if (r < R) {
+        float* lr = HL + static_cast<int64_t>(r) * m.Vp;
+        *reinterpret_cast<float4*>(lr + col0) =
+            make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        *reinterpret_cast<float4*>(lr + col1) =
+            make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// B. h[r][i] = tanhf((pe[r][i] + pd[ctx_r][i]) + j_b[i]) into the k-major tile.
+__device__ __forceinline__ void build_h(const ModelView& m, const float* pe,
+                                        const int64_t* row_pe,
+                                        const int32_t* row_ctx, int R,
+                                        float* HL) {
+  const int J = m.J;
+  const int total = R * J;
+  for (int idx = threadIdx.x; idx < total; idx += kDecodeThreads) {
+    const int r = idx / J, i = idx - r * J;
+    const float a = pe[row_pe[r] * J + i];
+    const float b = m.pd[static_cast<int64_t>(row_ctx[r]) * J + i];
+    HL[i * kHStride + r] = rnntg_exact::tanhf_glibc(fadd(fadd(a, b), m.j_b[i]));
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float warp_max_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Log-softmax normaliser of one logits row (model.hpp:115-125): float max,
+// double sum of exp(double(l) - max), lse = max + log(sum).  The sum is a
+// warp tree instead of the reference's index-order loop; the two differ by a
+// few fp64 ulps (documented in DESIGN.md; scores are checked to 1e-9 rel).
+__device__ __forceinline__ double row_lse(const float* L, int V) {
+  const int lane = threadIdx.x & 31;
+  float mx = -FLT_MAX;
+  for (int k = lane; k < V; k += 32) mx = fmaxf(mx, L[k]);
+  mx = warp_max_f(mx);
+  double s = 0.0;
+  for (int k = lane; k < V; k += 32) s += exp(static_cast<double>(L[k]) - static_cast<double>(mx));
+  s = warp_sum_d(s);
+  return static_cast<double>(mx) + log(s);
+}
+
+// (logit desc, token asc): the order of a hypothesis' extensions, whose
+// scores s + (double(l) - lse) are monotone in the float logit l.
+__device__ __forceinline__ bool tok_before(float la, int ka, float lb, int kb) {
+  return la > lb || (la == lb && ka < kb);
+}
+
+// ---------------------------------------------------------------------------
+// Greedy (search.hpp:107-167, S = 1).
+// ---------------------------------------------------------------------------
+struct GreedySmem {
+  uint64_t bar[2];
+  int64_t row_pe[kRowCap];
+  int32_t row_ctx[kRowCap];
+  int32_t row_stream[kRowCap];
+  int32_t ctx[kRowCap];
+  int32_t len[kRowCap];
+  int32_t nrows;
+};
+
+__global__ void __launch_bounds__(kDecodeThreads, 1)
+    greedy_kernel(ModelView m, const float* __restrict__ pe,
+                  const int32_t* __restrict__ frame_splits, int32_t B,
+                  int32_t G, int32_t* __restrict__ tokens,
+                  int32_t* __restrict__ lengths,
+                  unsigned long long* __restrict__ counters) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* HL = reinterpret_cast<float*>(smem_raw);
+  const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
+  float* W0 = HL + hl_floats;
+  float* W1 = W0 + kBK * m.Vp;
+  GreedySmem& S = *reinterpret_cast<GreedySmem*>(W1 + kBK * m.Vp);
+
+  const int s0 = blockIdx.x * G;
+  const int ns = min(G, B - s0);
+  if (ns <= 0) return;
+  WPipe pipe{{W0, W1}, S.bar, (m.J + kBK - 1) / kBK};
+
+  int32_t tmax = 0;
+  for (int i = 0; i < ns; ++i)
+    tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
+  if (threadIdx.x < ns) {
+    S.ctx[threadIdx.x] = 0;
+    S.len[threadIdx.x] = 0;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    wpipe_issue(pipe, m, 0);
+    wpipe_issue(pipe, m, 1);
+  }
+  uint32_t g = 0;
+  unsigned long long rows_total = 0;
+
+  for (int32_t t = 0; t < tmax; ++t) {
+    if (threadIdx.x == 0) {  // A. one row per live stream
+      int R = 0;
+      for (int i = 0; i < ns; ++i) {
+        const int32_t fs = frame_splits[s0 + i];
+        if (t < frame_splits[s0 + i + 1] - fs) {
+          S.row_pe[R] = fs + t;
+          S.row_ctx[R] = S.ctx[i];
+          S.row_stream[R] = i;
+          ++R;
+        }
+      }
+      S.nrows = R;
+    }
+    __syncthreads();
+    const int R = S.nrows;
+    rows_total += R;
+    build_h(m, pe, S.row_pe, S.row_ctx, R, HL);
+    joiner_gemm(m, pipe, g, HL, R);
+    // D+E. first-max argmax of the raw float logits, append non-blank.
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < R; r += kWarps) {
+      const float* L = HL + static_cast<int64_t>(r) * m.Vp;
+      float bv = -FLT_MAX;
+      int bk = 0x7fffffff;
+      for (int k = lane; k < m.V; k += 32)
+        if (tok_before(L[k], k, bv, bk)) {
+          bv = L[k];
+          bk = k;
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+        if (tok_before(ov, ok, bv, bk)) {
+          bv = ov;
+          bk = ok;
+        }
+      }
+      if (lane == 0 && bk != 0) {
+        const int i = S.row_stream[r];
+        const int32_t len = S.len[i];
+        tokens[frame_splits[s0 + i] + len] = bk;
+        S.len[i] = len + 1;
+        S.ctx[i] = (S.ctx[i] % m.V) * m.V + bk;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < ns) lengths[s0 + threadIdx.x] = S.len[threadIdx.x];
+  // Drain the two prefetched chunks before the CTA's smem is released.
+  if (threadIdx.x == 0) {
+    mbar_wait(&S.bar[g & 1u], (g >> 1) & 1u);
+    mbar_wait(&S.bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);
+    unsigned long long sf = 0;
+    for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
+    atomicAdd(&counters[0], sf);
+    atomicAdd(&counters[1], rows_total);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Modified beam search (beam_search at max_symbols = 1, search.hpp:206-277).
+// ---------------------------------------------------------------------------
+constexpr int kMaxG = kRowCap;  // streams per CTA (beam 1)
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
+}
+// Sequence identity: two independent chained 64-bit hashes of ys plus
+// |ys| and the last token.
+__device__ __forceinline__ uint64_t hash_ext1(uint64_t h, int32_t k) {
+  return mix64(h + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(k + 1));
+}
+__device__ __forceinline__ uint64_t hash_ext2(uint64_t h, int32_t k) {
+  return mix64((h ^ 0xd6e8feb86659fd93ull) * 0x100000001b3ull +
+               static_cast<uint64_t>(k) * 0xff51afd7ed558ccdull);
+}
+
+struct Hyps {  // one stream's beam, sorted best first
+  double score[kMaxBeam];
+  uint64_t h1[kMaxBeam], h2[kMaxBeam], p1[kMaxBeam], p2[kMaxBeam];
+  int32_t ctx[kMaxBeam], len[kMaxBeam], last[kMaxBeam], row[kMaxBeam];
+  int32_t nh;
+};
+
+struct BeamCand {  // stage-1 extension or stage-2 merged entry
+  double score;
+  uint64_t h1, h2, p1, p2;
+  int32_t parent;  // hypothesis slot at layer t
+  int32_t tok;     // 0 = blank continuation (the parent's own ys)
+  int32_t len, ctx, last;
+};
+
+struct BeamSmem {
+  uint64_t bar[2];
+  int64_t row_pe[kRowCap];
+  int32_t row_ctx[kRowCap];
+  double row_lse[kRowCap];
+  float row_l0[kRowCap];
+  float row_tl[kRowCap][kMaxBeam];
+  int32_t row_tk[kRowCap][kMaxBeam];
+  int32_t nrows;
+};
+
+// Walks two equal-length sequences backwards through the back-pointer
+// lattice and returns <0, 0, >0 for lexicographic X<Y, X==Y, X>Y.  Each
+// sequence is (layer tau, slot, pending token or -1).  Only reached on exact
+// score ties (the third key of hyp_better, search.hpp:172-178).
+__device__ int lex_cmp(const uint32_t* __restrict__ bp, int tx, int sx, int px,
+                       int ty, int sy, int py) {
+  int res = 0;
+  while (true) {
+    if (px < 0 && py < 0 && tx == ty && sx == sy) break;  // shared prefix
+    int a = -1, b = -1;
+    if (px >= 0) {
+      a = px;
+      px = -1;
+    } else {
+      while (tx > 0) {
+        const uint32_t e = bp[tx * kMaxBeam + sx];
+        --tx;
+        sx = static_cast<int>(e & 0xffu);
+        const int tok = static_cast<int>(e >> 8);
+        if (tok != 0) {
+          a = tok;
+          break;
+        }
+      }
+    }
+    if (py >= 0) {
+      b = py;
+      py = -1;
+    } else {
+      while (ty > 0) {
+        const uint32_t e = bp[ty * kMaxBeam + sy];
+        --ty;
+        sy = static_cast<int>(e & 0xffu);
+        const int tok = static_cast<int>(e >> 8);
+        if (tok != 0) {
+          b = tok;
+          break;
+        }
+      }
+    }
+    if (a < 0 || b < 0) break;
+    if (a != b) res = a < b ? -1 : 1;
+  }
+  return res;
+}
+
+// hyp_better(a, b) over candidates of one frame (search.hpp:172-178).
+__device__ __forceinline__ bool cand_before(const BeamCand& a, double ka,
+                                            const BeamCand& b, double kb,
+                                            const uint32_t* bp, int layer,
+                                            unsigned long long* ties) {
+  if (ka != kb) return ka > kb;
+  if (a.len != b.len) return a.len < b.len;
+  ++*ties;
+  // Same length.  Extensions of the same parent: smaller token first.
+  if (a.tok != 0 && b.tok != 0 && a.parent == b.parent) return a.tok < b.tok;
+  const int c = lex_cmp(bp, layer, a.parent, a.tok != 0 ? a.tok : -1, layer,
+                        b.parent, b.tok != 0 ? b.tok : -1);
+  return c < 0;
+}
+
+__global__ void __launch_bounds__(kDecodeThreads, 1)
+    beam_kernel(ModelView m, const float* __restrict__ pe,
+                const int32_t* __restrict__ frame_splits, int32_t B, int32_t G,
+                int32_t beam, int32_t merge_log, int32_t length_norm,
+                int32_t max_total, uint32_t* __restrict__ backptr,
+                int32_t* __restrict__ tokens, int32_t* __restrict__ lengths,
+                double* __restrict__ scores,
+                unsigned long long* __restrict__ counters) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* HL = reinterpret_cast<float*>(smem_raw);
+  const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
+  float* W0 = HL + hl_floats;
+  float* W1 = W0 + kBK * m.Vp;
+  BeamSmem& S = *reinterpret_cast<BeamSmem*>(W1 + kBK * m.Vp);
+  Hyps* H = reinterpret_cast<Hyps*>(&S + 1);          // [G]
+  BeamCand* C = reinterpret_cast<BeamCand*>(H + G);   // [G][kMaxBeam*kMaxBeam + kMaxBeam]
+  constexpr int kCandPerStream = kMaxBeam * kMaxBeam + 2 * kMaxBeam;
+
+  const int s0 = blockIdx.x * G;
+  const int ns = min(G, B - s0);
+  if (ns <= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WPipe pipe{{W0, W1}, S.bar, (m.J + kBK - 1) / kBK};
+
+  int32_t tmax = 0;
+  for (int i = 0; i < ns; ++i)
+    tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
+  for (int i = threadIdx.x; i < ns; i += kDecodeThreads) {
+    Hyps& h = H[i];
+    h.nh = 1;
+    h.score[0] = 0.0;
+    h.ctx[0] = 0;
+    h.len[0] = 0;
+    h.last[0] = -1;
+    h.h1[0] = 0x243f6a8885a308d3ull;
+    h.h2[0] = 0x13198a2e03707344ull;
+    h.p1[0] = h.p2[0] = 0;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    wpipe_issue(pipe, m, 0);
+    wpipe_issue(pipe, m, 1);
+  }
+  uint32_t g = 0;
+  unsigned long long rows_total = 0, ties = 0;
+
+  for (int32_t t = 0; t < tmax; ++t) {
+    // A. rows: distinct contexts per live stream (lane = stream, G <= 32).
+    if (warp == 0) {
+      const int i = lane;
+      int cnt = 0;
+      if (i < ns && t < frame_splits[s0 + i + 1] - frame_splits[s0 + i]) {
+        const Hyps& h = H[i];
+        for (int j = 0; j < h.nh; ++j) {
+          bool fresh = true;
+          for (int q = 0; q < j; ++q) fresh = fresh && h.ctx[q] != h.ctx[j];
+          cnt += fresh ? 1 : 0;
+        }
+      }
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (cnt > 0) {
+        Hyps& h = H[i];
+        const int64_t pr = frame_splits[s0 + i] + t;
+        int r = incl - cnt;
+        for (int j = 0; j < h.nh; ++j) {
+          int first = j;
+          for (int q = j - 1; q >= 0; --q)
+            if (h.ctx[q] == h.ctx[j]) first = q;
+          if (first == j) {
+            S.row_pe[r] = pr;
+            S.row_ctx[r] = h.ctx[j];
+            h.row[j] = r++;
+          } else {
+            h.row[j] = h.row[first];
+          }
+        }
+      }
+      if (lane == 31) S.nrows = incl;
+    }
+    __syncthreads();
+    const int R = S.nrows;
+    rows_total += R;
+    build_h(m, pe, S.row_pe, S.row_ctx, R, HL);
+    joiner_gemm(m, pipe, g, HL, R);
+
+    // D. per row: lse, blank logit, top-`beam` tokens k >= 1 by (logit desc,
+    // token asc).  Each lane keeps a sorted local top-kMaxBeam, then `beam`
+    // warp-wide pops.
+    for (int r = warp; r < R; r += kWarps) {
+      const float* L = HL + static_cast<int64_t>(r) * m.Vp;
+      const double lse = row_lse(L, m.V);
+      float tl[kMaxBeam];
+      int tk[kMaxBeam];
+#pragma unroll
+      for (int q = 0; q < kMaxBeam; ++q) {
+        tl[q] = -FLT_MAX;
+        tk[q] = 0x7fffffff;
+      }
+      for (int k = (lane == 0 ? 32 : lane); k < m.V; k += 32) {
+        float cv = L[k];
+        int ck = k;
+        if (!tok_before(cv, ck, tl[kMaxBeam - 1], tk[kMaxBeam - 1])) continue;
+#pragma unroll
+        for (int q = 0; q < kMaxBeam; ++q) {
+          if (tok_before(cv, ck, tl[q], tk[q])) {
+            const float tv = tl[q];
+            const int tkk = tk[q];
+            tl[q] = cv;
+            tk[q] = ck;
+            cv = tv;
+            ck = tkk;
+          }
+        }
+      }
+      for (int q = 0; q < beam; ++q) {
+        float bv = tl[0];
+        int bk = tk[0], bl = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+          const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+          if (tok_before(ov, ok, bv, bk)) {
+            bv = ov;
+            bk = ok;
+            bl = ol;
+          }
+        }
+        if (lane == 0) {
+          S.row_tl[r][q] = bv;
+          S.row_tk[r][q] = bk;
+        }
+        if (lane == bl) {
+#pragma unroll
+          for (int z = 0; z < kMaxBeam - 1; ++z) {
+            tl[z] = tl[z + 1];
+            tk[z] = tk[z + 1];
+          }
+          tl[kMaxBeam - 1] = -FLT_MAX;
+          tk[kMaxBeam - 1] = 0x7fffffff;
+        }
+      }
+      if (lane == 0) {
+        S.row_lse[r] = lse;
+        S.row_l0[r] = L[0];
+      }
+    }
+    __syncthreads();
+
+    // E. beam step, one warp per stream.  Reference order (search.hpp:
+    // 223-259 at S = 1): the extensions are cut to the beam first
+    // (prune_to_beam of next_level), then merged with the blank
+    // continuations by full-sequence equality, then the frame set is cut.
+    for (int i = warp; i < ns; i += kWarps) {
+      const int32_t fs = frame_splits[s0 + i];
+      const int32_t T = frame_splits[s0 + i + 1] - fs;
+      if (t >= T) continue;
+      Hyps& h = H[i];
+      BeamCand* cand = C + static_cast<int64_t>(i) * kCandPerStream;
+      BeamCand* merged = cand + kMaxBeam * kMaxBeam;  // [2 * kMaxBeam]
+      uint32_t* bp = backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam;
+      const int nh = h.nh;
+
+      // Stage 1: every hypothesis' top-`beam` extensions; the global top
+      // `beam` of those is the reference's pruned next_level.
+      const int next = nh * beam;
+      for (int c = lane; c < next; c += 32) {
+        const int j = c / beam, q = c % beam;
+        const int r = h.row[j];
+        const bool may_emit = max_total <= 0 || h.len[j] < max_total;
+        const int k = S.row_tk[r][q];
+        BeamCand& e = cand[c];
+        e.score = (may_emit && k < m.V)
+                      ? h.score[j] + (static_cast<double>(S.row_tl[r][q]) - S.row_lse[r])
+                      : -INFINITY;
+        e.parent = j;
+        e.tok = k;
+        e.len = h.len[j] + 1;
+      }
+      __syncwarp();
+      int rank[2] = {0x7fffffff, 0x7fffffff};
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int c = lane + u * 32;
+        if (c >= next || cand[c].score == -INFINITY) continue;
+        const BeamCand a = cand[c];
+        int rk = 0;
+        for (int d = 0; d < next; ++d) {
+          const BeamCand& b = cand[d];
+          if (d == c || b.score == -INFINITY) continue;
+          if (cand_before(b, b.score, a, a.score, bp, t, &ties)) ++rk;
+        }
+        rank[u] = rk;
+      }
+      BeamCand sel[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (rank[u] < beam) sel[u] = cand[lane + u * 32];
+      int nsel = (rank[0] < beam ? 1 : 0) + (rank[1] < beam ? 1 : 0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nsel += __shfl_xor_sync(0xffffffffu, nsel, o);
+      __syncwarp();
+      // Stage 2 inputs: blank continuations in merged[0..nh), selected
+      // extensions (with their new identities) in cand[0..nsel) by rank.
+      if (lane < nh) {
+        const int r = h.row[lane];
+        BeamCand& b = merged[lane];
+        b.score = h.score[lane] + (static_cast<double>(S.row_l0[r]) - S.row_lse[r]);
+        b.h1 = h.h1[lane];
+        b.h2 = h.h2[lane];
+        b.p1 = h.p1[lane];
+        b.p2 = h.p2[lane];
+        b.parent = lane;
+        b.tok = 0;
+        b.len = h.len[lane];
+        b.ctx = h.ctx[lane];
+        b.last = h.last[lane];
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (rank[u] >= beam) continue;
+        BeamCand e = sel[u];
+        const int gp = e.parent;
+        e.h1 = hash_ext1(h.h1[gp], e.tok);
+        e.h2 = hash_ext2(h.h2[gp], e.tok);
+        e.p1 = h.h1[gp];
+        e.p2 = h.h2[gp];
+        e.ctx = (h.ctx[gp] % m.V) * m.V + e.tok;
+        e.last = e.tok;
+        cand[rank[u]] = e;
+      }
+      __syncwarp();
+      // merge_into (search.hpp:180-187): an extension ys_g+k equals the blank
+      // continuation of hypothesis j iff |ys_j| = |ys_g|+1, last(ys_j) = k
+      // and prefix(ys_j) = ys_g.
+      int nm = nh;
+      if (lane == 0) {
+        for (int q = 0; q < nsel; ++q) {
+          const BeamCand& e = cand[q];
+          int hit = -1;
+          for (int j = 0; j < nh; ++j)
+            if (merged[j].last == e.tok && merged[j].len == e.len &&
+                merged[j].p1 == e.p1 && merged[j].p2 == e.p2) {
+              hit = j;
+              break;
+            }
+          if (hit >= 0) {
+            double& sc = merged[hit].score;
+            if (merge_log) {  // log_add, common.hpp:48-54
+              const double a = sc, b = e.score;
+              if (a == -INFINITY) {
+                sc = b;
+              } else if (b != -INFINITY) {
+                const double hi = a > b ? a : b, lo = a > b ? b : a;
+                sc = hi + log1p(exp(lo - hi));
+              }
+            } else {
+              sc = sc > e.score ? sc : e.score;
+            }
+          } else {
+            merged[nm++] = e;
+          }
+        }
+      }
+      nm = __shfl_sync(0xffffffffu, nm, 0);
+      __syncwarp();
+      // prune_to_beam of the frame set by hyp_better.
+      int myrank = 0x7fffffff;
+      BeamCand mine;
+      if (lane < nm) {
+        mine = merged[lane];
+        int rk = 0;
+        for (int d = 0; d < nm; ++d) {
+          if (d == lane) continue;
+          if (cand_before(merged[d], merged[d].score, mine, mine.score, bp, t, &ties)) ++rk;
+        }
+        myrank = rk;
+      }
+      __syncwarp();
+      if (myrank < beam) {
+        h.score[myrank] = mine.score;
+        h.h1[myrank] = mine.h1;
+        h.h2[myrank] = mine.h2;
+        h.p1[myrank] = mine.p1;
+        h.p2[myrank] = mine.p2;
+        h.ctx[myrank] = mine.ctx;
+        h.len[myrank] = mine.len;
+        h.last[myrank] = mine.last;
+        bp[(t + 1) * kMaxBeam + myrank] =
+            (static_cast<uint32_t>(mine.tok) << 8) | static_cast<uint32_t>(mine.parent);
+      }
+      if (lane == 0) h.nh = min(nm, beam);
+      __syncwarp();
+
+      // Stream finished: the winner by hyp_better on score or length-normed
+      // score (search.hpp:261-276), traced back through the lattice.
+      if (t + 1 == T && lane == 0) {
+        const int nf = h.nh;
+        int best = 0;
+        for (int j = 1; j < nf; ++j) {
+          const double kj = length_norm ? h.score[j] / max(1, h.len[j]) : h.score[j];
+          const double kb =
+              length_norm ? h.score[best] / max(1, h.len[best]) : h.score[best];
+          BeamCand a, b;
+          a.len = h.len[j];
+          a.parent = j;
+          a.tok = 0;
+          b.len = h.len[best];
+          b.parent = best;
+          b.tok = 0;
+          if (cand_before(a, kj, b, kb, bp, T, &ties)) best = j;
+        }
+        scores[s0 + i] = h.score[best];
+        lengths[s0 + i] = h.len[best];
+        int pos = h.len[best];
+        int tau = T, slot = best;
+        while (tau > 0) {
+          const uint32_t e = bp[tau * kMaxBeam + slot];
+          --tau;
+          slot = static_cast<int>(e & 0xffu);
+          const int tok = static_cast<int>(e >> 8);
+          if (tok != 0) tokens[fs + --pos] = tok;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // Zero-frame streams: empty result, score 0.
+  for (int i = threadIdx.x; i < ns; i += kDecodeThreads)
+    if (frame_splits[s0 + i + 1] == frame_splits[s0 + i]) {
+      lengths[s0 + i] = 0;
+      scores[s0 + i] = 0.0;
+    }
+  atomicAdd(&counters[4], ties);
+  if (threadIdx.x == 0) {
+    mbar_wait(&S.bar[g & 1u], (g >> 1) & 1u);
+    mbar_wait(&S.bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);
+    unsigned long long sf = 0;
+    for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
+    atomicAdd(&counters[0], sf);
+    atomicAdd(&counters[1], rows_total);
+  }
+}
+
+size_t smem_common(const ModelView& m) {
+  const size_t hl = static_cast<size_t>(max(m.J * kHStride, kRowCap * m.Vp)) * 4;
+  return hl + static_cast<size_t>(2) * kBK * m.Vp * 4;
+}
+
+ModelView view_of(const DeviceModel& d) {
+  return ModelView{d.V, d.J, d.Vp, d.out_wt, d.out_b, d.j_b, d.pd_table};
+}
+
+}  // namespace
+
+int decode_num_sms(int device) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  return n > 0 ? n : 1;
+}
+
+cudaError_t launch_decode_greedy(const DecodeArgs& a, cudaStream_t s) {
+  const ModelView m = view_of(*a.m);
+  const size_t smem = smem_common(m) + sizeof(GreedySmem);
+  cudaError_t e = cudaFuncSetAttribute(
+      greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int grid = (a.B + a.streams_per_cta - 1) / a.streams_per_cta;
+  greedy_kernel<<<grid, kDecodeThreads, smem, s>>>(
+      m, a.pe, a.frame_splits, a.B, a.streams_per_cta, a.tokens, a.lengths,
+      a.counters);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s) {
+  const ModelView m = view_of(*a.m);
+  const int G = a.streams_per_cta;
+  const size_t smem = smem_common(m) + sizeof(BeamSmem) + sizeof(Hyps) * G +
+                      sizeof(BeamCand) * G * (kMaxBeam * kMaxBeam + 2 * kMaxBeam);
+  cudaError_t e = cudaFuncSetAttribute(
+      beam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int grid = (a.B + G - 1) / G;
+  beam_kernel<<<grid, kDecodeThreads, smem, s>>>(
+      m, a.pe, a.frame_splits, a.B, G, a.beam_size, a.merge_op, a.length_norm,
+      a.max_total, a.backptr, a.tokens, a.lengths, a.scores, a.counters);
+  return cudaGetLastError();
+}
+
+}  // namespace rnntg

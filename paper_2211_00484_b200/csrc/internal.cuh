@@ -1,0 +1,122 @@
+// Internal declarations shared by the rnntg CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/rnntg.h"
+
+namespace rnntg {
+
+constexpr int kMaxVocab = 512;      // joiner output row staged whole in smem
+constexpr int kMaxJoiner = 512;     // reference limit (model.hpp:287-288)
+constexpr int kMaxBeam = 8;         // hypotheses per stream (warp lanes)
+constexpr int kDecodeThreads = 512; // persistent decode CTA
+
+void set_error(const std::string& msg);
+
+#define RNNTG_CUDA_TRY(expr)                                              \
+  do {                                                                    \
+    cudaError_t _e = (expr);                                              \
+    if (_e != cudaSuccess) {                                              \
+      ::rnntg::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+      return RNNTG_CUDA_ERROR;                                            \
+    }                                                                     \
+  } while (0)
+
+// Device copy of the model, laid out for the kernels.
+struct DeviceModel {
+  int32_t V = 0, D = 0, E = 0, J = 0;
+  int32_t Vp = 0;          // V rounded up to a multiple of 128
+  float* emb = nullptr;    // [V][E]
+  float* ctx_wt = nullptr; // [2E][Ep]  (transposed ctx_w, k-major)
+  float* ctx_b = nullptr;  // [E]
+  float* j_wet = nullptr;  // [D][Jp]   (transposed j_we)
+  float* j_wdt = nullptr;  // [E][Jp]   (transposed j_wd)
+  float* j_b = nullptr;    // [J]
+  float* out_wt = nullptr; // [J][Vp]   (transposed out_w, zero-padded)
+  float* out_b = nullptr;  // [Vp]
+  float* pd_table = nullptr; // [V*V][J]: decoder-side joiner projection of
+                             // every packed context (K0)
+  uint16_t* out_w_bf16 = nullptr; // [Vp][J] bf16 (tcgen05 variant)
+  int32_t Ep = 0, Jp = 0;
+};
+
+// Growable device scratch.
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&ptr, need);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(ptr);
+  }
+};
+
+// ---- exact sequential GEMM (gemm_exact.cu) ----
+// Y[m][n] = (bias ? bias[n] : 0) + sum_{k<K} X[m][k] * Wt[k][n], the k sum in
+// index order with separately rounded products (the reference's affine,
+// model.hpp:100-108).  Wt is [K][ldw] with ldw >= round_up(N, 128), padding
+// columns zero.  If ctx_emb != nullptr, row m is the decoder input of packed
+// context (ctx_base + m): [emb[c / V] ; emb[c % V]], K = 2E.
+cudaError_t launch_gemm_exact(const float* X, int64_t ldx, const float* Wt,
+                              int32_t ldw, const float* bias, float* Y,
+                              int64_t ldy, int64_t M, int32_t N, int32_t K,
+                              bool apply_tanh, const float* ctx_emb,
+                              int32_t ctx_V, int64_t ctx_base,
+                              cudaStream_t stream);
+
+// ---- persistent decode kernels (decode.cu) ----
+struct DecodeArgs {
+  const DeviceModel* m;     // host struct, copied by value into kernel params
+  const float* pe;          // [sum T][J] encoder-side projections
+  const int32_t* frame_splits; // device [B+1]
+  int32_t B;
+  int32_t streams_per_cta;
+  int32_t* tokens;          // device [sum T] (per-stream slot at frame_splits)
+  int32_t* lengths;         // device [B]
+  double* scores;           // device [B]
+  unsigned long long* counters; // device [8]
+  // beam
+  int32_t beam_size, merge_op, length_norm, max_total;
+  uint32_t* backptr;        // device [(sum T + B) * kMaxBeam]
+  // fsa
+  const void* graph_arcs;   // device int4-packed arcs
+  const int32_t* graph_splits;
+  int32_t graph_states;
+  double fsa_beam;
+  int32_t max_states, max_contexts;
+  void* lattice;            // device lattice arc pool
+  int64_t lattice_cap;
+  int32_t* lat_frame_info;  // device per (stream, frame) [count, offset, nodes]
+  int32_t* error_flag;      // device
+};
+
+cudaError_t launch_decode_greedy(const DecodeArgs& a, cudaStream_t s);
+cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s);
+cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s);
+int decode_num_sms(int device);
+
+cudaError_t launch_tanhf_hash(int32_t first_chunk, int32_t num_chunks,
+                              unsigned long long* d_hashes, cudaStream_t s);
+cudaError_t launch_joiner_rows_exact(const DeviceModel& m, const float* pe,
+                                     const int32_t* ctxs, int32_t n,
+                                     float* logits, cudaStream_t s);
+
+}  // namespace rnntg

@@ -1,0 +1,47 @@
+"""Shared fixtures: seeded reference models, encoder frames and graphs.
+
+Inputs follow SURVEY.md §8(d): init_model weights (DetRng), blank bias on
+out_b[0], features ~ DetRng(seed + stream).gaussian(), encoder frames from
+the reference encoder (identical bits go to both sides)."""
+from __future__ import annotations
+
+import functools
+import os
+
+import numpy as np
+
+from oracle.py_oracle import Graph as OGraph
+from oracle.py_oracle import Oracle, Reference, Weights
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@functools.lru_cache(maxsize=1)
+def ref():
+    return Reference()
+
+
+@functools.lru_cache(maxsize=1)
+def orc():
+    return Oracle()
+
+
+@functools.lru_cache(maxsize=8)
+def model(V=500, F=80, D=512, E=512, J=512, seed=1, blank_bias=0.4):
+    return ref().model(V, F, D, E, J, seed, blank_bias)
+
+
+def frames(m, Ts, seed0=1000):
+    """(features, encoder frames, frame_splits) for streams of lengths Ts."""
+    F = m.w.F
+    splits = np.zeros(len(Ts) + 1, np.int32)
+    splits[1:] = np.cumsum(Ts)
+    feats = np.concatenate([ref().features(seed0 + i, T, F) for i, T in enumerate(Ts)] + [np.zeros((0, F), np.float32)])
+    enc = m.encoder(feats, splits)
+    return feats, enc, splits
+
+
+def api_weights(w: Weights):
+    from paper_2211_00484_b200.api import ModelWeights
+
+    return ModelWeights.from_dict(w.p)

@@ -1,0 +1,61 @@
+// Measures the non-fused fp32 multiply+add rate the exact joiner is bound by
+// (FMUL then FADD per MAC, as the reference's sequential affine requires),
+// beside the FFMA rate, on this GPU.  Prints one JSON line.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <bool kFused>
+__global__ void __launch_bounds__(512) mac_kernel(float* out, float seed, int iters) {
+  float acc[32], w[4], x[8];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) acc[i] = seed * (threadIdx.x + i);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) w[i] = seed + i;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = seed - i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (kFused) acc[i * 8 + j] = __fmaf_rn(w[i], x[j], acc[i * 8 + j]);
+        else acc[i * 8 + j] = __fadd_rn(acc[i * 8 + j], __fmul_rn(w[i], x[j]));
+      }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = __fadd_rn(w[i], 1e-7f);
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) s += acc[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+int main() {
+  int sms = 0, clk = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  float* out;
+  cudaMalloc(&out, sizeof(float) * sms * 4 * 512);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int iters = 20000;
+  double res[2];
+  for (int f = 0; f < 2; ++f) {
+    for (int rep = 0; rep < 4; ++rep) {
+      cudaEventRecord(a);
+      if (f) mac_kernel<true><<<sms * 2, 512>>>(out, 1.0f, iters);
+      else mac_kernel<false><<<sms * 2, 512>>>(out, 1.0f, iters);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      const double macs = double(sms) * 2 * 512 * iters * 32.0;
+      res[f] = macs / (ms * 1e-3);
+    }
+  }
+  printf("{\"sms\": %d, \"clock_khz_attr\": %d, \"nonfused_mac_per_s\": %.4e, \"ffma_mac_per_s\": %.4e, "
+         "\"nonfused_tflops\": %.3f, \"ffma_tflops\": %.3f}\n",
+         sms, clk, res[0], res[1], 2 * res[0] / 1e12, 2 * res[1] / 1e12);
+  return 0;
+}
