@@ -1,0 +1,402 @@
+#!/usr/bin/env python3
+"""Benchmark: modified beam search (beam 4, one symbol per frame), V=500,
+D=J=E=512, T=1000 frames per stream, 1024 streams per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one pass of the hot path (decoder-context lookup, exact joiner,
+log-softmax, beam pruning / merging, traceback) over one batch of 1024
+synthetic streams whose encoder frames are already resident in HBM.  Under
+torchrun each rank decodes its own 1024 streams (streams are independent;
+weak scaling, no collective on the data path); the timed region is
+barrier + synchronize on both sides and the reported time is the max over
+ranks.  Rank 0 prints ONE JSON line.
+
+`--impl reference` times the reference's own CPU implementation
+(rnnt-kit beam_search, compiled from /root/reference into
+oracle/_ref/librnnt_ref.so) on this host's cores over a bounded sample of the
+same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+V, F, D, E, J = 500, 80, 512, 512, 512
+T_FRAMES = 1000
+BATCH_PER_GPU = 1024
+BEAM = 4
+BLANK_BIAS = 0.4
+METRIC = "decoded frames/sec (and RTF) at beam=4, batch 1024, 1/2/4/8 B200 vs CPU ref"
+WORKLOAD = "modified_beam_search beam=4 max_symbols=1, 1024 streams/GPU x T=1000, V=500 D=E=J=512 (config 5 point)"
+
+
+def synthetic_weights(seed=1):
+    """init_model's distribution (model.hpp:129-169: uniform +-1/sqrt(fan_in)),
+    seeded numpy PCG64, blank bias on out_b[0]."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+
+    def u(shape, fan_in):
+        s = 1.0 / np.sqrt(fan_in)
+        return rng.uniform(-s, s, size=shape).astype(np.float32)
+
+    p = {
+        "emb": u((V, E), E),
+        "ctx_w": u((E, 2 * E), 2 * E),
+        "ctx_b": u((1, E), 2 * E),
+        "j_we": u((J, D), D),
+        "j_wd": u((J, E), E),
+        "j_b": u((1, J), D),
+        "out_w": u((V, J), J),
+        "out_b": u((1, V), J),
+    }
+    p["out_b"][0, 0] += BLANK_BIAS
+    return p
+
+
+def synthetic_frames(B, T, seed):
+    """Encoder-output-like frames in (-1, 1): tanh of N(0, 0.6^2), float32."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    enc = np.empty((B * T, D), np.float32)
+    step = 65536
+    for r in range(0, B * T, step):
+        n = min(step, B * T - r)
+        enc[r : r + n] = np.tanh(rng.standard_normal((n, D), dtype=np.float32) * 0.6)
+    splits = (np.arange(B + 1, dtype=np.int64) * T).astype(np.int32)
+    return enc, splits
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = (
+        "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+        "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+    )
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL,
+                text=True,
+            )
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) == 6:
+                self.rows.append(f)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "reasons": reasons,
+            "samples": len(self.rows),
+        }
+
+
+def fp32_nonfused_peak_tflops():
+    """Measured non-fused fp32 (FMUL+FADD) rate of this GPU: the bound of the
+    exact joiner, which may not fuse."""
+    exe = os.path.join(ROOT, "tools", "fp32_peak")
+    if not os.path.exists(exe):
+        src = os.path.join(ROOT, "tools", "fp32_peak.cu")
+        subprocess.run(
+            ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", exe, src], check=True, capture_output=True
+        )
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "beam_kernel_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return None
+    return None
+
+
+def cpu_baseline(threads, streams, T):
+    """The reference's beam_search on this host (oracle/_ref): a bounded
+    sample of the same workload, one utterance per thread task (the
+    reference CLI's parallel_for).  Includes the reference's internal encoder,
+    which is timed alone too and subtracted for the search-only rate."""
+    from oracle.py_oracle import Reference
+
+    ref = Reference()
+    m = ref.model(V, F, D, E, J, 1, BLANK_BIAS)
+    feats = np.concatenate([ref.features(5000 + i, T, F) for i in range(streams)])
+    splits = (np.arange(streams + 1) * T).astype(np.int32)
+    t0 = time.perf_counter()
+    m.encoder(feats, splits, threads=threads)
+    t_enc = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    m.beam(feats, splits, beam=BEAM, threads=threads)
+    t_all = time.perf_counter() - t0
+    frames = streams * T
+    return {
+        "value": frames / max(1e-9, t_all - t_enc),
+        "unit": "frames/s",
+        "cores": threads,
+        "kind": "reference",
+        "sample": f"{streams} streams x T={T} (beam 4, V=500), reference beam_search via parallel_for; "
+        f"search-only (encoder {t_enc:.2f}s subtracted from {t_all:.2f}s)",
+        "value_with_encoder": frames / t_all,
+        "rtf": (t_all - t_enc) / (frames * 0.01),
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    streams, T = threads, T_FRAMES
+    from oracle.py_oracle import Reference
+
+    ref = Reference()
+    m = ref.model(V, F, D, E, J, 1, BLANK_BIAS)
+    feats = np.concatenate([ref.features(7000 + i, T, F) for i in range(streams)])
+    splits = (np.arange(streams + 1) * T).astype(np.int32)
+    for _ in range(args.warmup):
+        m.beam(feats[: T * min(streams, threads)], splits[: min(streams, threads) + 1], beam=BEAM, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        m.beam(feats, splits, beam=BEAM, threads=threads)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(times)
+    value = streams * T / (ms * 1e-3)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": "frames/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 logits / f64 scores",
+        "data": "synthetic features (DetRng gaussian) through the reference encoder; reference init_model weights",
+        "config": {"workload": WORKLOAD, "sample_per_step": f"{streams} streams x T={T}", "threads": threads},
+        "rtf": (ms * 1e-3) / (streams * T * 0.01),
+        "cpu_baseline": {
+            "value": value,
+            "unit": "frames/s",
+            "cores": threads,
+            "kind": "reference",
+            "sample": f"{streams} streams x T={T} per step (reference beam_search incl. its encoder)",
+        },
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=BATCH_PER_GPU)
+    ap.add_argument("--frames", type=int, default=T_FRAMES)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2211_00484_b200.api import BeamParams, Decoder, ModelWeights
+
+    B, T = args.batch, args.frames
+    t0 = time.perf_counter()
+    dec = Decoder(ModelWeights.from_dict(synthetic_weights()), device=local)
+    torch.cuda.synchronize()
+    model_prep_s = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    dec.set_stream(stream.cuda_stream)
+
+    enc, splits = synthetic_frames(B, T, seed=100 + rank)
+    d_enc = torch.from_numpy(enc).to(f"cuda:{local}")
+    tok = torch.zeros(B * T, dtype=torch.int32, device=f"cuda:{local}")
+    sc = torch.zeros(B, dtype=torch.float64, device=f"cuda:{local}")
+    params = BeamParams(beam_size=BEAM)
+
+    def step():
+        return dec.beam_search_batch(d_enc, splits, params, tok, sc)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    decode_ms, rows, sfr, launches, ties = [], 0, 0, 0, 0
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+            st = dec.stats()
+            decode_ms.append(st["decode_ms"])
+            rows += st["joiner_rows"]
+            sfr += st["stream_frames"]
+            launches += st["kernel_launches"]
+            ties += st["tie_breaks"]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    tokens_emitted = int(dec.stats()["stream_frames"])  # placeholder overwritten below
+    osp, _, _ = step()
+    tokens_emitted = int(osp[-1])
+    t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t_max.item())
+    ms_per_step = elapsed_ms / args.steps
+    value = world * B * T / (ms_per_step * 1e-3)
+
+    # ---- e2e through the public API with pinned host buffers ----
+    pin = torch.from_numpy(enc).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    dec.beam_search_batch(pin, splits, params)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        toks_host, scores_host = dec.beam_search_batch(pin, splits, params)
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_step = float(e2e_s.item())
+
+    line = None
+    if rank == 0:
+        peak = fp32_nonfused_peak_tflops()
+        mean_decode_ms = statistics.mean(decode_ms)
+        rows_per_step = rows / args.steps
+        flops = 2.0 * rows_per_step * V * J  # exact joiner output projection per launch
+        achieved = flops / (mean_decode_ms * 1e-3) / 1e12
+        traffic = load_traffic()
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "frames/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(args.warmup, 3),
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32 (exact non-fused joiner) / f64 scores",
+            "data": "synthetic: encoder frames tanh(N(0,0.36)) resident in HBM, init_model-distributed random weights (numpy PCG64), blank bias 0.4",
+            "config": {
+                "workload": WORKLOAD,
+                "global_batch": world * B,
+                "batch_per_gpu": B,
+                "frames_per_stream": T,
+                "beam": BEAM,
+                "vocab": V,
+                "parallelism": f"dp{world} (streams sharded, no data-path collective)",
+                "l2": "inputs larger than L2 (enc %.1f GB per step per GPU)" % (B * T * D * 4 / 1e9),
+            },
+            "rtf": (ms_per_step * 1e-3) / (B * T * 0.01),
+            "e2e": {
+                "value": world * B * T / e2e_step,
+                "unit": "frames/s",
+                "h2d_bytes_per_step": int(B * T * D * 4 + (B + 1) * 4),
+                "d2h_bytes_per_step": int(B * T * 4 + B * 4 + B * 8 + 64),
+                "api": "Decoder.beam_search_batch(pinned host frames) -> rnntg_beam_search_batch(RNNTG_MEM_HOST)",
+            },
+            "gpu_launches": int(launches),
+            "roofline": {
+                "bound": "fp32-nonfused",
+                "achieved": achieved,
+                "peak": peak["nonfused_tflops"],
+                "unit": "TFLOP/s",
+                "frac": achieved / peak["nonfused_tflops"],
+                "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                "kernel": "beam_kernel (persistent decode; excludes the pe projection GEMM)",
+                "algorithmic": "2*V*J FLOP per joiner row (V=500, J=512); rows counted on device",
+                "peak_source": "tools/fp32_peak.cu measured at run time: FMUL+FADD (the reference's "
+                "unfused sequential fp32 dot product cannot use FFMA or tensor cores and stay bit-exact); "
+                f"FFMA peak {peak['ffma_tflops']:.1f} TF/s, bf16 tensor peak 1632 TF/s for context",
+            },
+            "decode_kernel_ms": mean_decode_ms,
+            "joiner_rows_per_stream_frame": rows / max(1, sfr),
+            "tokens_per_frame": tokens_emitted / (B * T),
+            "exact_score_ties": int(ties),
+            "model_prep_s": model_prep_s,
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline and world == 1:
+            threads = os.cpu_count() or 1
+            try:
+                line["cpu_baseline"] = cpu_baseline(threads, 2 * threads, T)
+            except Exception as e:  # reference build missing on this host
+                line["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    dec.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -29,6 +29,8 @@ struct rnntg_model_s {
   int num_sms = 1;
   int joiner_mode = RNNTG_JOINER_EXACT;
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
+  Scratch finfo, nodebest, lattice, flag;
+  int64_t lat_cap_hint = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   rnntg_stats stats{};
   std::mutex mu;
@@ -291,7 +293,8 @@ rnntg_status rnntg_model_destroy(rnntg_model_t h) {
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
   for (void* p : h->owned) cudaFree(p);
   for (Scratch* s : {&h->enc, &h->pe, &h->splits, &h->tok, &h->len, &h->score, &h->bp,
-                     &h->counters, &h->ctx, &h->out_tok, &h->out_splits, &h->logits})
+                     &h->counters, &h->ctx, &h->out_tok, &h->out_splits, &h->logits,
+                     &h->finfo, &h->nodebest, &h->lattice, &h->flag})
     s->release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -468,19 +471,95 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
                                    int32_t* out_splits, int32_t* out_tokens,
                                    double* out_scores) {
   if (!h || !p || !graph) return invalid("null argument");
+  if (graph->model != h) return invalid("graph belongs to another model handle");
   // check_fsa_search_params, fsa_search.hpp:83-90.
   if (!(p->beam >= 0.0)) return invalid("fsa search beam must be >= 0");
   if (p->max_states < 1) return invalid("max_states must be >= 1");
   if (p->max_contexts < 1) return invalid("max_contexts must be >= 1");
-  (void)enc;
-  (void)fs;
-  (void)B;
-  (void)mem;
-  (void)out_splits;
-  (void)out_tokens;
-  (void)out_scores;
-  set_error("fsa_beam_search device path not built yet");
-  return RNNTG_UNSUPPORTED;
+  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
+  rnntg_status st = check_frames(enc, fs, B);
+  if (st) return st;
+  if (!out_splits) return invalid("out_splits is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  const float* d_enc = nullptr;
+  if ((st = prepare(h, enc, fs, B, mem, &d_enc))) return st;
+  int64_t launches = fs[B] > 0 ? 1 : 0;
+  if (B > 0) {
+    const int64_t total = fs[B];
+    const int K = std::min(p->max_states, rnntg::kFsaMaxStates);
+    const int rows = std::min(p->max_contexts, K);
+    int G = 1;
+    const int want = std::min({4, std::max(1, (B + h->num_sms - 1) / h->num_sms), std::max(1, 32 / rows)});
+    while (G * 2 <= want) G *= 2;
+    RNNTG_CUDA_TRY(h->finfo.ensure(sizeof(int32_t) * 4 * (total + B)));
+    RNNTG_CUDA_TRY(h->nodebest.ensure(sizeof(double) * (total * K + B)));
+    RNNTG_CUDA_TRY(h->flag.ensure(16));
+    int64_t cap = std::max<int64_t>(1 << 20, h->lat_cap_hint);
+    for (int attempt = 0;; ++attempt) {
+      cap = std::max<int64_t>(cap, total * 4);
+      RNNTG_CUDA_TRY(h->lattice.ensure(static_cast<size_t>(cap) * 24));
+      cap = static_cast<int64_t>(h->lattice.bytes / 24);
+      RNNTG_CUDA_TRY(cudaMemsetAsync(h->flag.ptr, 0, 16, h->stream));
+      RNNTG_CUDA_TRY(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long) * 8, h->stream));
+      rnntg::DecodeArgs a{};
+      a.m = &h->d;
+      a.pe = h->pe.as<float>();
+      a.frame_splits = h->splits.as<int32_t>();
+      a.B = B;
+      a.streams_per_cta = G;
+      a.tokens = h->tok.as<int32_t>();
+      a.lengths = h->len.as<int32_t>();
+      a.scores = h->score.as<double>();
+      a.counters = h->counters.as<unsigned long long>();
+      a.graph_arcs = graph->arcs;
+      a.graph_splits = graph->splits;
+      a.graph_states = graph->num_states;
+      a.fsa_beam = p->beam;
+      a.max_states = p->max_states;
+      a.max_contexts = p->max_contexts;
+      a.lattice = h->lattice.ptr;
+      a.lattice_cap = cap;
+      a.error_flag = h->flag.as<int32_t>();
+      a.lattice_count = reinterpret_cast<unsigned long long*>(h->flag.as<char>() + 8);
+      a.lat_frame_info = h->finfo.as<int32_t>();
+      a.node_best = h->nodebest.as<double>();
+      RNNTG_CUDA_TRY(rnntg::launch_decode_fsa(a, h->stream));
+      ++launches;
+      int32_t flag = 0;
+      unsigned long long used = 0;
+      RNNTG_CUDA_TRY(cudaMemcpyAsync(&flag, h->flag.ptr, sizeof(flag), cudaMemcpyDeviceToHost, h->stream));
+      RNNTG_CUDA_TRY(cudaMemcpyAsync(&used, h->flag.as<char>() + 8, sizeof(used), cudaMemcpyDeviceToHost, h->stream));
+      RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+      if (flag == 1 && attempt < 4) {  // lattice pool overflow: grow and rerun
+        cap = static_cast<int64_t>(used) * 2 + 1024;
+        h->lat_cap_hint = cap;
+        continue;
+      }
+      if (flag == 2) {
+        set_error("more than 32 distinct contexts per CTA frame (max_contexts too large for this build)");
+        return RNNTG_UNSUPPORTED;
+      }
+      if (flag == 3) {
+        set_error("candidate hash overflow (too many exact-score duplicates near the beam cut)");
+        return RNNTG_UNSUPPORTED;
+      }
+      if (flag == 4) {
+        set_error("max_states binds above the device cap of 64 states per stream");
+        return RNNTG_UNSUPPORTED;
+      }
+      if (flag == 5) {
+        set_error("best_path trace failed (inconsistent scores)");
+        return RNNTG_INTERNAL;
+      }
+      if (flag != 0) {
+        set_error("fsa kernel error flag " + std::to_string(flag));
+        return RNNTG_INTERNAL;
+      }
+      break;
+    }
+  }
+  return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
 }
 
 rnntg_status rnntg_debug_decoder_projection(rnntg_model_t h, const int32_t* ctxs,

@@ -1,0 +1,223 @@
+// Device building blocks shared by the persistent decode kernels
+// (decode.cu: greedy / modified beam; fsa.cu: FSA beam search).
+#pragma once
+
+#include <float.h>
+#include <math.h>
+
+#include "exact_math.h"
+#include "internal.cuh"
+
+namespace rnntg {
+namespace dec {
+
+using rnntg_exact::fadd;
+using rnntg_exact::fmul;
+
+constexpr int kWarps = kDecodeThreads / 32;  // 16
+constexpr int kBK = 16;                      // k rows per out_w chunk
+constexpr int kRowCap = 32;                  // joiner rows per CTA per frame
+constexpr int kHStride = kRowCap + 4;        // padded k-major h tile stride
+
+struct ModelView {
+  int32_t V, J, Vp;
+  const float* __restrict__ out_wt;  // [J][Vp]
+  const float* __restrict__ out_b;   // [Vp]
+  const float* __restrict__ j_b;     // [J]
+  const float* __restrict__ pd;      // [V*V][J]
+};
+
+// ---------------------------------------------------------------------------
+// mbarrier + bulk copy helpers (sm_90+ PTX, SASS UBLKCP / SYNCS).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
+                                         uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// out_w chunk pipeline.  Chunk g (a running sequence number across frames)
+// holds k-rows [(g % nc) * kBK, ...) of out_wt and lives in stage g & 1.
+// ---------------------------------------------------------------------------
+struct WPipe {
+  float* stage[2];
+  uint64_t* bar;  // [2]
+  int32_t nc;     // chunks per frame
+};
+
+__device__ __forceinline__ void wpipe_issue(const WPipe& p, const ModelView& m,
+                                            uint32_t g) {
+  const int32_t c = static_cast<int32_t>(g % static_cast<uint32_t>(p.nc));
+  const int32_t rows = min(kBK, m.J - c * kBK);
+  const uint32_t bytes = static_cast<uint32_t>(rows) * m.Vp * 4u;
+  uint64_t* bar = p.bar + (g & 1u);
+  fence_proxy_async();
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(p.stage[g & 1u], m.out_wt + static_cast<int64_t>(c) * kBK * m.Vp,
+           bytes, bar);
+}
+
+// C. logits[r][n] = out_b[n] + sum_k out_w[n][k] * h[r][k], sequential in k.
+// Hs: k-major h tile [J][kHStride]; Ls (aliasing Hs): row-major [R][Vp].
+// Warp w owns rows 4*(w/NH) .. +3 and columns (w%NH)*256 + {4l..4l+3,
+// 128+4l..128+4l+3}, NH = Vp/256.
+__device__ __forceinline__ void joiner_gemm(const ModelView& m, const WPipe& p,
+                                            uint32_t& g, float* HL, int R) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NH = m.Vp >> 8;
+  const int items = ((R + 3) >> 2) * NH;
+  const bool active = warp < items;
+  const int rg = warp / NH, half = warp % NH;
+  const int col0 = half * 256 + lane * 4, col1 = col0 + 128;
+
+  float acc[4][8];
+  {
+    float4 b0 = make_float4(0, 0, 0, 0), b1 = b0;
+    if (active) {
+      b0 = *reinterpret_cast<const float4*>(m.out_b + col0);
+      b1 = *reinterpret_cast<const float4*>(m.out_b + col1);
+    }
+    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = bv[j];
+  }
+
+  for (int32_t c = 0; c < p.nc; ++c, ++g) {
+    const uint32_t st = g & 1u;
+    mbar_wait(p.bar + st, (g >> 1) & 1u);
+    if (active) {
+      const float* Ws = p.stage[st];
+      const int kk_end = min(kBK, m.J - c * kBK);
+      const float* hp = HL + static_cast<int64_t>(c * kBK) * kHStride + rg * 4;
+#pragma unroll 4
+      for (int kk = 0; kk < kk_end; ++kk) {
+        const float4 h4 = *reinterpret_cast<const float4*>(hp + kk * kHStride);
+        const float4 wa = *reinterpret_cast<const float4*>(Ws + kk * m.Vp + col0);
+        const float4 wb = *reinterpret_cast<const float4*>(Ws + kk * m.Vp + col1);
+        const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
+        const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            acc[i][j] = fadd(acc[i][j], fmul(wv[j], hv[i]));
+      }
+    }
+    __syncthreads();  // every warp is done with this stage
+    if (threadIdx.x == 0) wpipe_issue(p, m, g + 2);
+  }
+  // The last __syncthreads above also retired every read of Hs, so the logits
+  // may overwrite it.
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = rg * 4 + i;
+      if (r < R) {
+        float* lr = HL + static_cast<int64_t>(r) * m.Vp;
+        *reinterpret_cast<float4*>(lr + col0) =
+            make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        *reinterpret_cast<float4*>(lr + col1) =
+            make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// B. h[r][i] = tanhf((pe[r][i] + pd[ctx_r][i]) + j_b[i]) into the k-major tile.
+__device__ __forceinline__ void build_h(const ModelView& m, const float* pe,
+                                        const int64_t* row_pe,
+                                        const int32_t* row_ctx, int R,
+                                        float* HL) {
+  const int J = m.J;
+  const int total = R * J;
+  for (int idx = threadIdx.x; idx < total; idx += kDecodeThreads) {
+    const int r = idx / J, i = idx - r * J;
+    const float a = pe[row_pe[r] * J + i];
+    const float b = m.pd[static_cast<int64_t>(row_ctx[r]) * J + i];
+    HL[i * kHStride + r] = rnntg_exact::tanhf_glibc(fadd(fadd(a, b), m.j_b[i]));
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float warp_max_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Log-softmax normaliser of one logits row (model.hpp:115-125): float max,
+// double sum of exp(double(l) - max), lse = max + log(sum).  The sum is a
+// warp tree instead of the reference's index-order loop; the two differ by a
+// few fp64 ulps (documented in DESIGN.md; scores are checked to 1e-9 rel).
+__device__ __forceinline__ double row_lse(const float* L, int V) {
+  const int lane = threadIdx.x & 31;
+  float mx = -FLT_MAX;
+  for (int k = lane; k < V; k += 32) mx = fmaxf(mx, L[k]);
+  mx = warp_max_f(mx);
+  double s = 0.0;
+  for (int k = lane; k < V; k += 32) s += exp(static_cast<double>(L[k]) - static_cast<double>(mx));
+  s = warp_sum_d(s);
+  return static_cast<double>(mx) + log(s);
+}
+
+// (logit desc, token asc): the order of a hypothesis' extensions, whose
+// scores s + (double(l) - lse) are monotone in the float logit l.
+__device__ __forceinline__ bool tok_before(float la, int ka, float lb, int kb) {
+  return la > lb || (la == lb && ka < kb);
+}
+
+
+inline size_t smem_common(const ModelView& m) {
+  const size_t hl = static_cast<size_t>(max(m.J * kHStride, kRowCap * m.Vp)) * 4;
+  return hl + static_cast<size_t>(2) * kBK * m.Vp * 4;
+}
+
+inline ModelView view_of(const DeviceModel& d) {
+  return ModelView{d.V, d.J, d.Vp, d.out_wt, d.out_b, d.j_b, d.pd_table};
+}
+
+}  // namespace dec
+}  // namespace rnntg

@@ -1,0 +1,615 @@
+// FSA-based fast beam search (Algorithm 1 of arXiv 2211.00484), persistent
+// and stream-stationary like decode.cu.  Restates fsa_search.hpp:
+//
+//   get_contexts  (124-154)  distinct contexts of a stream's active tuples,
+//                            ascending (active is kept sorted by (ctx, state))
+//   joiner + log-softmax     exact fp32 logits (decode_common.cuh) and the
+//                            row normaliser; lp[k] = double(l_k) - lse as in
+//                            model.hpp:115-125
+//   expand_arcs   (161-223)  blank self-candidate and one candidate per
+//                            outgoing graph arc, read from 16-byte CSR arc
+//                            records; duplicates (ctx, state) merged by MAX
+//   prune_streams (230-297)  (score desc, ctx asc, state asc) order,
+//                            inclusive beam floor, max_states, then the first
+//                            max_contexts contexts; survivors numbered in
+//                            (ctx, state) order; every raw arc into a survivor
+//                            is kept, in generation order
+//   best_path     (fsa.hpp:345-376) on the HBM lattice after the last frame:
+//                            backward tropical suffix maxima, forward trace
+//                            taking the first arc that attains the remainder.
+//
+// Candidate selection without materialising all candidates: the top
+// max_states distinct keys all score >= the M-th largest raw candidate once
+// the raw candidates at or above that threshold hold >= max_states distinct
+// keys.  A per-stream 256-bin score histogram below the stream's best finds
+// such a threshold; only candidates above it enter a shared-memory hash
+// (key -> max score, atomicMax on order-preserving integers), whose distinct
+// entries are bitonic-sorted.  This is exact, not approximate: every key with
+// max >= threshold is present with its true max.
+#include "decode_common.cuh"
+
+namespace rnntg {
+namespace {
+
+using namespace dec;
+
+constexpr int kMaxStates = kFsaMaxStates;  // device cap on max_states
+constexpr int kHashCap = 256;    // hot-candidate hash entries per stream
+constexpr int kBins = 256;
+constexpr int kSurvHash = 128;
+constexpr int kMaxGroups = 4;    // streams per CTA
+constexpr uint64_t kEmptyKey = ~0ull;
+
+struct ArcRec {  // matches the host ArcRec in capi.cu
+  int32_t dst, label;
+  double w;
+};
+
+struct LatArc {  // one lattice arc
+  int32_t src, dst, label, pad;
+  double score;
+};
+
+struct FsaStream {
+  int32_t n_act, num_nodes, nrows, row_base;
+  int32_t n_raw, n_hot, n_sort, n_surv;
+  int32_t bstar, arc_count, arc_off, flag;
+  double best, floor;
+  int32_t act_ctx[kMaxStates], act_state[kMaxStates], act_node[kMaxStates], act_row[kMaxStates];
+  double act_score[kMaxStates];
+  int32_t act_off[kMaxStates + 1];
+  int32_t row_ctx[kMaxStates];
+  int32_t bins[kBins];
+  uint64_t hkey[kHashCap];
+  unsigned long long hval[kHashCap];
+  uint64_t s1[kHashCap], s2[kHashCap];  // sort keys
+  int32_t surv_ctx[kMaxStates], surv_state[kMaxStates];
+  double surv_score[kMaxStates];
+  uint64_t shkey[kSurvHash];
+  int32_t shnode[kSurvHash];
+  double red_d[16];
+  int32_t red_i[16];
+};
+
+struct FsaSmem {
+  uint64_t bar[2];
+  int64_t row_pe[kRowCap];
+  int32_t row_ctx[kRowCap];
+  double row_lse[kRowCap];
+  int32_t nrows;
+};
+
+__device__ __forceinline__ unsigned long long ord_of(double x) {
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dbl_of(unsigned long long o) {
+  const unsigned long long u = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+  return __longlong_as_double(static_cast<long long>(u));
+}
+__device__ __forceinline__ uint64_t key_of(int32_t ctx, int32_t state) {
+  return (static_cast<uint64_t>(static_cast<uint32_t>(ctx)) << 32) | static_cast<uint32_t>(state);
+}
+__device__ __forceinline__ uint32_t hash_slot(uint64_t k, uint32_t cap) {
+  k ^= k >> 29;
+  k *= 0xbf58476d1ce4e5b9ull;
+  k ^= k >> 32;
+  return static_cast<uint32_t>(k) & (cap - 1);
+}
+
+// Thread-group helpers (G groups of NT = 512/G threads; named barrier 1+grp).
+struct Group {
+  int id, tid, nt;
+  __device__ __forceinline__ void sync() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + id), "r"(nt) : "memory");
+  }
+};
+
+__device__ double group_max(const Group& g, FsaStream& S, double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = g.tid >> 5, nw = g.nt >> 5;
+  if ((g.tid & 31) == 0) S.red_d[w] = v;
+  g.sync();
+  double r = S.red_d[0];
+  for (int i = 1; i < nw; ++i) r = fmax(r, S.red_d[i]);
+  g.sync();
+  return r;
+}
+
+// Exclusive scan of one int per thread over the group; returns the prefix,
+// *total gets the sum.
+__device__ int group_scan(const Group& g, FsaStream& S, int v, int* total) {
+  const int lane = g.tid & 31, w = g.tid >> 5, nw = g.nt >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  if (lane == 31) S.red_i[w] = incl;
+  g.sync();
+  int base = 0, tot = 0;
+  for (int i = 0; i < nw; ++i) {
+    if (i < w) base += S.red_i[i];
+    tot += S.red_i[i];
+  }
+  g.sync();
+  *total = tot;
+  return base + incl - v;
+}
+
+// Raw candidate q of the stream (generation order of expand_arcs): active
+// tuple i = the segment of q; q == act_off[i] is its blank self-candidate,
+// otherwise graph arc (q - act_off[i] - 1) of its state.
+struct Raw {
+  int32_t i, ctx, state, label;
+  double arc_score, score;
+};
+
+__device__ __forceinline__ Raw raw_cand(const FsaStream& S, int q, const ArcRec* __restrict__ arcs,
+                                        const int32_t* __restrict__ splits, const float* L,
+                                        const double* row_lse, int Vp, int V) {
+  int lo = 0, hi = S.n_act - 1;  // last i with act_off[i] <= q
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (S.act_off[mid] <= q) lo = mid;
+    else hi = mid - 1;
+  }
+  Raw r;
+  r.i = lo;
+  const int row = S.act_row[lo];
+  const float* Lr = L + static_cast<int64_t>(S.row_base + row) * Vp;
+  const double lse = row_lse[S.row_base + row];
+  const double sc = S.act_score[lo];
+  const int j = q - S.act_off[lo];
+  if (j == 0) {
+    r.ctx = S.act_ctx[lo];
+    r.state = S.act_state[lo];
+    r.label = 0;
+    r.arc_score = static_cast<double>(Lr[0]) - lse;
+  } else {
+    const ArcRec a = arcs[splits[S.act_state[lo]] + j - 1];
+    r.ctx = (S.act_ctx[lo] % V) * V + a.label;
+    r.state = a.dst;
+    r.label = a.label;
+    r.arc_score = a.w + (static_cast<double>(Lr[a.label]) - lse);
+  }
+  r.score = sc + r.arc_score;
+  return r;
+}
+
+__device__ __forceinline__ int bin_of(double best, double score, double floor, double scale) {
+  if (!(score >= floor)) return -1;
+  const double d = (best - score) * scale;
+  return d >= kBins - 1 ? kBins - 1 : static_cast<int>(d);
+}
+
+__global__ void __launch_bounds__(kDecodeThreads, 1)
+    fsa_kernel(ModelView m, const float* __restrict__ pe, const int32_t* __restrict__ frame_splits,
+               int32_t B, int32_t G, const ArcRec* __restrict__ arcs,
+               const int32_t* __restrict__ gsplits, double beam, int32_t max_states,
+               int32_t max_contexts, LatArc* __restrict__ lat, int64_t lat_cap,
+               unsigned long long* __restrict__ lat_count, int4* __restrict__ finfo,
+               double* __restrict__ nodebest, int32_t* __restrict__ tokens,
+               int32_t* __restrict__ lengths, double* __restrict__ scores,
+               unsigned long long* __restrict__ counters, int32_t* __restrict__ error_flag) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* HL = reinterpret_cast<float*>(smem_raw);
+  const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
+  float* W0 = HL + hl_floats;
+  float* W1 = W0 + kBK * m.Vp;
+  FsaSmem& C = *reinterpret_cast<FsaSmem*>(W1 + kBK * m.Vp);
+  FsaStream* SS = reinterpret_cast<FsaStream*>(&C + 1);
+
+  const int s0 = blockIdx.x * G;
+  const int ns = min(G, B - s0);
+  if (ns <= 0) return;
+  WPipe pipe{{W0, W1}, C.bar, (m.J + kBK - 1) / kBK};
+  const int nt = kDecodeThreads / G;
+  const Group grp{static_cast<int>(threadIdx.x) / nt, static_cast<int>(threadIdx.x) % nt, nt};
+  const bool have = grp.id < ns;
+  FsaStream& S = SS[grp.id < ns ? grp.id : 0];
+  const int sidx = s0 + grp.id;
+  const int32_t fs = have ? frame_splits[sidx] : 0;
+  const int32_t T = have ? frame_splits[sidx + 1] - fs : 0;
+  const int K = min(max_states, kMaxStates);
+  const int64_t fbase = static_cast<int64_t>(fs) + sidx;          // frame info base
+  const int64_t nbase = static_cast<int64_t>(fs) * K + sidx;       // node-best base
+  const double scale = kBins / (beam < 8.0 ? (beam > 0.0 ? beam : 1.0) : 8.0);
+  const int M = K + 32;  // hot-candidate target
+
+  int32_t tmax = 0;
+  for (int i = 0; i < ns; ++i) tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
+  if (have && grp.tid == 0) {  // init_streams (95-120): ((0,0), state 0, 0.0, node 0)
+    S.n_act = 1;
+    S.num_nodes = 1;
+    S.act_ctx[0] = 0;
+    S.act_state[0] = 0;
+    S.act_score[0] = 0.0;
+    S.act_node[0] = 0;
+    S.flag = 0;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&C.bar[0], 1);
+    mbar_init(&C.bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    wpipe_issue(pipe, m, 0);
+    wpipe_issue(pipe, m, 1);
+  }
+  uint32_t gch = 0;
+  unsigned long long rows_total = 0, raw_total = 0, lat_total = 0;
+
+  for (int32_t t = 0; t < tmax; ++t) {
+    const bool live = have && t < T;
+    // get_contexts: distinct contexts in order; each tuple's row.
+    if (live && grp.tid == 0) {
+      int nr = 0;
+      for (int i = 0; i < S.n_act; ++i) {
+        if (nr == 0 || S.row_ctx[nr - 1] != S.act_ctx[i]) S.row_ctx[nr++] = S.act_ctx[i];
+        S.act_row[i] = nr - 1;
+      }
+      S.nrows = nr;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int R = 0;
+      for (int g2 = 0; g2 < ns; ++g2) {
+        FsaStream& X = SS[g2];
+        const int32_t f2 = frame_splits[s0 + g2];
+        if (t >= frame_splits[s0 + g2 + 1] - f2) continue;
+        X.row_base = R;
+        for (int r = 0; r < X.nrows; ++r) {
+          if (R < kRowCap) {
+            C.row_pe[R] = f2 + t;
+            C.row_ctx[R] = X.row_ctx[r];
+          }
+          ++R;
+        }
+      }
+      if (R > kRowCap) {
+        atomicExch(error_flag, 2);  // more joiner rows than the CTA tile holds
+        R = kRowCap;
+      }
+      C.nrows = R;
+    }
+    __syncthreads();
+    const int R = C.nrows;
+    rows_total += R;
+    build_h(m, pe, C.row_pe, C.row_ctx, R, HL);
+    joiner_gemm(m, pipe, gch, HL, R);
+    {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int r = warp; r < R; r += kDecodeThreads / 32) {
+        const double lse = row_lse(HL + static_cast<int64_t>(r) * m.Vp, m.V);
+        if (lane == 0) C.row_lse[r] = lse;
+      }
+    }
+    __syncthreads();
+
+    if (live) {
+      // ---- expand_arcs ----
+      if (grp.tid == 0) {
+        int off = 0;
+        for (int i = 0; i < S.n_act; ++i) {
+          S.act_off[i] = off;
+          off += 1 + gsplits[S.act_state[i] + 1] - gsplits[S.act_state[i]];
+        }
+        S.act_off[S.n_act] = off;
+        S.n_raw = off;
+      }
+      for (int b = grp.tid; b < kBins; b += nt) S.bins[b] = 0;
+      for (int b = grp.tid; b < kHashCap; b += nt) {
+        S.hkey[b] = kEmptyKey;
+        S.hval[b] = 0ull;
+      }
+      grp.sync();
+      const int nraw = S.n_raw;
+      raw_total += (grp.tid == 0) ? nraw : 0;
+      double mx = -INFINITY;
+      for (int q = grp.tid; q < nraw; q += nt)
+        mx = fmax(mx, raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V).score);
+      const double best = group_max(grp, S, mx);
+      const double floor = best - beam;  // prune_streams 247-248
+      for (int q = grp.tid; q < nraw; q += nt) {
+        const int b = bin_of(best, raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V).score,
+                             floor, scale);
+        if (b >= 0) atomicAdd(&S.bins[b], 1);
+      }
+      grp.sync();
+      if (grp.tid == 0) {
+        int cum = 0, b = 0;
+        for (; b < kBins; ++b) {
+          cum += S.bins[b];
+          if (cum >= M) break;
+        }
+        S.bstar = min(b, kBins - 1);
+        S.n_hot = 0;
+      }
+      grp.sync();
+      // Hot candidates into the hash; widen the threshold if duplicates left
+      // fewer than K distinct keys.
+      while (true) {
+        const int bstar = S.bstar;
+        for (int q = grp.tid; q < nraw; q += nt) {
+          const Raw rc = raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V);
+          const int b = bin_of(best, rc.score, floor, scale);
+          if (b < 0 || b > bstar) continue;
+          const uint64_t k = key_of(rc.ctx, rc.state);
+          uint32_t slot = hash_slot(k, kHashCap);
+          for (int probe = 0; probe < kHashCap; ++probe) {
+            const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(&S.hkey[slot]),
+                                            static_cast<unsigned long long>(kEmptyKey),
+                                            static_cast<unsigned long long>(k));
+            if (prev == kEmptyKey) atomicAdd(&S.n_hot, 1);
+            if (prev == kEmptyKey || prev == k) {
+              atomicMax(&S.hval[slot], ord_of(rc.score));
+              break;
+            }
+            slot = (slot + 1) & (kHashCap - 1);
+            if (probe == kHashCap - 1) atomicExch(error_flag, 3);
+          }
+        }
+        grp.sync();
+        if (S.n_hot >= K || bstar >= kBins - 1) break;
+        if (S.n_hot > kHashCap / 2) break;
+        grp.sync();
+        if (grp.tid == 0) {  // next bin with entries
+          int b = bstar + 1, cum = 0;
+          for (; b < kBins - 1; ++b) {
+            cum += S.bins[b];
+            if (cum >= M) break;
+          }
+          S.bstar = b;
+          // entries already inserted are re-offered: max is idempotent.
+        }
+        grp.sync();
+      }
+      if (grp.tid == 0 && S.n_hot > kHashCap * 3 / 4) atomicExch(error_flag, 3);
+      // Compact the distinct keys and bitonic-sort by (score desc, key asc).
+      if (grp.tid == 0) S.n_sort = 0;
+      grp.sync();
+      for (int b = grp.tid; b < kHashCap; b += nt)
+        if (S.hkey[b] != kEmptyKey) {
+          const int p = atomicAdd(&S.n_sort, 1);
+          S.s1[p] = ~S.hval[b];
+          S.s2[p] = S.hkey[b];
+        }
+      grp.sync();
+      const int D = S.n_sort;
+      int NP = 1;
+      while (NP < D) NP <<= 1;
+      for (int p = D + grp.tid; p < NP; p += nt) {
+        S.s1[p] = ~0ull;
+        S.s2[p] = ~0ull;
+      }
+      grp.sync();
+      for (int k2 = 2; k2 <= NP; k2 <<= 1)
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+          for (int p = grp.tid; p < NP; p += nt) {
+            const int q = p ^ j;
+            if (q > p) {
+              const bool up = (p & k2) == 0;
+              const uint64_t a1 = S.s1[p], a2 = S.s2[p], b1 = S.s1[q], b2 = S.s2[q];
+              const bool gt = a1 > b1 || (a1 == b1 && a2 > b2);
+              if (gt == up) {
+                S.s1[p] = b1;
+                S.s2[p] = b2;
+                S.s1[q] = a1;
+                S.s2[q] = a2;
+              }
+            }
+          }
+          grp.sync();
+        }
+      // ---- prune_streams ----
+      if (grp.tid == 0) {
+        if (max_states > kMaxStates && D > kMaxStates) atomicExch(error_flag, 4);
+        const int npass = min(K, D);  // all hot entries are >= floor
+        int kept[kMaxStates];
+        int nk = 0, nsurv = 0;
+        for (int p = 0; p < npass; ++p) {
+          const int32_t c = static_cast<int32_t>(S.s2[p] >> 32);
+          bool found = false;
+          for (int z = 0; z < nk; ++z) found = found || kept[z] == c;
+          if (!found && nk < max_contexts) kept[nk++] = c;
+        }
+        for (int p = 0; p < npass; ++p) {
+          const int32_t c = static_cast<int32_t>(S.s2[p] >> 32);
+          bool found = false;
+          for (int z = 0; z < nk; ++z) found = found || kept[z] == c;
+          if (found) {
+            S.surv_ctx[nsurv] = c;
+            S.surv_state[nsurv] = static_cast<int32_t>(S.s2[p] & 0xffffffffu);
+            S.surv_score[nsurv] = dbl_of(~S.s1[p]);
+            ++nsurv;
+          }
+        }
+        S.n_surv = nsurv;
+        S.best = best;
+        S.floor = floor;
+      }
+      for (int b = grp.tid; b < kSurvHash; b += nt) S.shkey[b] = kEmptyKey;
+      grp.sync();
+      // Node ids in (ctx, state) order (274-283): rank among survivors.
+      const int nsurv = S.n_surv;
+      int my_rank = -1;
+      int my_ctx = 0, my_state = 0;
+      double my_score = 0;
+      if (grp.tid < nsurv) {
+        my_ctx = S.surv_ctx[grp.tid];
+        my_state = S.surv_state[grp.tid];
+        my_score = S.surv_score[grp.tid];
+        const uint64_t mk = key_of(my_ctx, my_state);
+        int rk = 0;
+        for (int z = 0; z < nsurv; ++z) rk += key_of(S.surv_ctx[z], S.surv_state[z]) < mk ? 1 : 0;
+        my_rank = rk;
+        uint32_t slot = hash_slot(mk, kSurvHash);
+        while (atomicCAS(reinterpret_cast<unsigned long long*>(&S.shkey[slot]),
+                         static_cast<unsigned long long>(kEmptyKey),
+                         static_cast<unsigned long long>(mk)) != kEmptyKey)
+          slot = (slot + 1) & (kSurvHash - 1);
+        S.shnode[slot] = S.num_nodes + rk;
+      }
+      grp.sync();
+      // ---- lattice arcs: raw candidates into survivors, generation order ----
+      int cnt = 0;
+      for (int q = grp.tid; q < nraw; q += nt) {
+        const Raw rc = raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V);
+        const uint64_t k = key_of(rc.ctx, rc.state);
+        uint32_t slot = hash_slot(k, kSurvHash);
+        while (S.shkey[slot] != kEmptyKey && S.shkey[slot] != k) slot = (slot + 1) & (kSurvHash - 1);
+        cnt += S.shkey[slot] == k ? 1 : 0;
+      }
+      int total = 0;
+      group_scan(grp, S, cnt, &total);
+      if (grp.tid == 0) {
+        const unsigned long long off = atomicAdd(lat_count, static_cast<unsigned long long>(total));
+        if (static_cast<int64_t>(off + total) > lat_cap) {
+          atomicExch(error_flag, 1);
+          S.arc_off = -1;
+        } else {
+          S.arc_off = static_cast<int32_t>(off);
+        }
+        S.arc_count = total;
+      }
+      grp.sync();
+      const int arc_off = S.arc_off;
+      lat_total += grp.tid == 0 ? total : 0;
+      int written = 0;
+      for (int q0 = 0; q0 < nraw; q0 += nt) {
+        const int q = q0 + grp.tid;
+        int hit = 0, dst = -1;
+        Raw rc;
+        if (q < nraw) {
+          rc = raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V);
+          const uint64_t k = key_of(rc.ctx, rc.state);
+          uint32_t slot = hash_slot(k, kSurvHash);
+          while (S.shkey[slot] != kEmptyKey && S.shkey[slot] != k) slot = (slot + 1) & (kSurvHash - 1);
+          if (S.shkey[slot] == k) {
+            hit = 1;
+            dst = S.shnode[slot];
+          }
+        }
+        int tot = 0;
+        const int pos = group_scan(grp, S, hit, &tot);
+        if (hit && arc_off >= 0) {
+          LatArc a;
+          a.src = S.act_node[rc.i];
+          a.dst = dst;
+          a.label = rc.label;
+          a.pad = 0;
+          a.score = rc.arc_score;
+          lat[static_cast<int64_t>(arc_off) + written + pos] = a;
+        }
+        written += tot;
+      }
+      grp.sync();
+      // New active set, sorted by (ctx, state).
+      if (my_rank >= 0) {
+        S.act_ctx[my_rank] = my_ctx;
+        S.act_state[my_rank] = my_state;
+        S.act_score[my_rank] = my_score;
+        S.act_node[my_rank] = S.num_nodes + my_rank;
+      }
+      grp.sync();
+      if (grp.tid == 0) {
+        finfo[fbase + t] = make_int4(S.arc_off, S.arc_count, S.num_nodes, nsurv);
+        S.n_act = nsurv;
+        S.num_nodes += nsurv;
+        if (nsurv == 0) S.flag = 1;  // dead stream (233-238): cannot happen with finite scores
+      }
+      grp.sync();
+    }
+    __syncthreads();
+  }
+
+  // ---- lattice_to_best_seq(kMax) = best_path on the stream's lattice ----
+  if (have && grp.tid == 0) {
+    double* nb = nodebest + nbase;
+    const int32_t nn = S.num_nodes;
+    // Layer T nodes reach the super-final node by a score-0 arc.
+    const int32_t lastb = T > 0 ? finfo[fbase + T - 1].z : 0;
+    for (int32_t n = lastb; n < nn; ++n) nb[n] = 0.0;
+    for (int32_t t = T - 1; t >= 0; --t) {
+      const int4 fi = finfo[fbase + t];
+      const int32_t lb = t > 0 ? finfo[fbase + t - 1].z : 0;
+      const int32_t le = t > 0 ? lb + finfo[fbase + t - 1].w : 1;
+      for (int32_t n = lb; n < le; ++n) nb[n] = -INFINITY;
+      for (int32_t a = 0; a < fi.y; ++a) {
+        const LatArc& e = lat[static_cast<int64_t>(fi.x) + a];
+        const double v = e.score + nb[e.dst];
+        if (nb[e.src] < v) nb[e.src] = v;
+      }
+    }
+    int32_t len = 0;
+    double total = 0.0;
+    double remaining = nb[0];
+    if (remaining == -INFINITY || S.flag) {
+      total = -INFINITY;
+    } else {
+      int32_t n = 0;
+      for (int32_t t = 0; t < T; ++t) {
+        const int4 fi = finfo[fbase + t];
+        int32_t chosen = -1;
+        for (int32_t a = 0; a < fi.y; ++a) {
+          const LatArc& e = lat[static_cast<int64_t>(fi.x) + a];
+          if (e.src == n && e.score + nb[e.dst] == remaining) {
+            chosen = a;
+            break;
+          }
+        }
+        if (chosen < 0) {  // best_path "inconsistent scores"
+          atomicExch(error_flag, 5);
+          break;
+        }
+        const LatArc& e = lat[static_cast<int64_t>(fi.x) + chosen];
+        if (e.label != 0) tokens[fs + len++] = e.label;
+        total += e.score;
+        remaining = nb[e.dst];
+        n = e.dst;
+      }
+      total += 0.0;  // the score-0 hop into the super-final node
+      total += 0.0;  // its final score
+    }
+    lengths[sidx] = len;
+    scores[sidx] = total;
+  }
+  if (threadIdx.x == 0) {
+    mbar_wait(&C.bar[gch & 1u], (gch >> 1) & 1u);
+    mbar_wait(&C.bar[(gch + 1) & 1u], ((gch + 1) >> 1) & 1u);
+    unsigned long long sf = 0;
+    for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
+    atomicAdd(&counters[0], sf);
+    atomicAdd(&counters[1], rows_total);
+  }
+  if (have && grp.tid == 0) {
+    atomicAdd(&counters[2], raw_total);
+    atomicAdd(&counters[3], lat_total);
+  }
+}
+
+}  // namespace
+
+size_t fsa_stream_smem() { return sizeof(FsaStream); }
+
+cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s) {
+  const ModelView m = view_of(*a.m);
+  const int G = a.streams_per_cta;
+  const size_t smem = smem_common(m) + sizeof(FsaSmem) + sizeof(FsaStream) * G;
+  cudaError_t e = cudaFuncSetAttribute(fsa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int grid = (a.B + G - 1) / G;
+  fsa_kernel<<<grid, kDecodeThreads, smem, s>>>(
+      m, a.pe, a.frame_splits, a.B, G, static_cast<const ArcRec*>(a.graph_arcs), a.graph_splits,
+      a.fsa_beam, a.max_states, a.max_contexts, static_cast<LatArc*>(a.lattice), a.lattice_cap,
+      a.lattice_count, reinterpret_cast<int4*>(a.lat_frame_info), a.node_best, a.tokens, a.lengths,
+      a.scores, a.counters, a.error_flag);
+  return cudaGetLastError();
+}
+
+}  // namespace rnntg

@@ -14,6 +14,7 @@ namespace rnntg {
 constexpr int kMaxVocab = 512;      // joiner output row staged whole in smem
 constexpr int kMaxJoiner = 512;     // reference limit (model.hpp:287-288)
 constexpr int kMaxBeam = 8;         // hypotheses per stream (warp lanes)
+constexpr int kFsaMaxStates = 64;   // FSA active tuples per stream
 constexpr int kDecodeThreads = 512; // persistent decode CTA
 
 void set_error(const std::string& msg);
@@ -104,7 +105,9 @@ struct DecodeArgs {
   int32_t max_states, max_contexts;
   void* lattice;            // device lattice arc pool
   int64_t lattice_cap;
-  int32_t* lat_frame_info;  // device per (stream, frame) [count, offset, nodes]
+  unsigned long long* lattice_count; // device arc pool bump counter
+  int32_t* lat_frame_info;  // device int4 per (stream, frame): off, count, node base, nodes
+  double* node_best;        // device per-node suffix scores (best_path)
   int32_t* error_flag;      // device
 };
 
