@@ -1,0 +1,173 @@
+// rnnt_gpu.hpp — header-only C++ drop-in for the reference decoder API
+// (rnnt-kit) on top of the rnntg C ABI (rnntg.h).
+//
+// Include AFTER the reference headers (it uses rnnt::ToyTransducer, Mat,
+// SearchParams, Fsa, FsaSearchParams and the reference exception types) and
+// link librnntg.so.  Each function keeps the reference signature plus a
+// leading rnnt::gpu::Context& (the device-resident model):
+//
+//   rnnt::greedy_search_batch(m, batch, 1)      search.hpp:107-167
+//     -> rnnt::gpu::greedy_search_batch(ctx, m, batch, 1)
+//   rnnt::beam_search(m, features, params)      search.hpp:206-277
+//     -> rnnt::gpu::beam_search(ctx, m, features, params)
+//        (+ beam_search_batch: one call for a whole batch of utterances)
+//   rnnt::fsa_beam_search + lattice_to_best_seq(kMax)   fsa_search.hpp:326-409
+//     -> rnnt::gpu::fsa_best_sequences(ctx, m, batch, graph, params)
+//
+// Like the reference, each search takes acoustic features and runs the
+// reference's own encoder_forward on the host (model.hpp:224-238) before the
+// GPU decode; callers that already hold encoder frames use the C ABI directly.
+// Errors map back to the reference's types: RNNTG_INVALID_ARGUMENT ->
+// rnnt::ValidationError, RNNTG_INTERNAL -> std::logic_error, anything else ->
+// std::runtime_error.
+#ifndef RNNT_GPU_HPP_
+#define RNNT_GPU_HPP_
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rnntg.h"
+
+namespace rnnt {
+namespace gpu {
+
+inline void check(rnntg_status st) {
+  if (st == RNNTG_OK) return;
+  const std::string msg = rnntg_last_error();
+  if (st == RNNTG_INVALID_ARGUMENT) throw ValidationError(msg);
+  if (st == RNNTG_INTERNAL) throw std::logic_error(msg);
+  throw std::runtime_error("rnntg: " + msg);
+}
+
+// A model resident on one GPU.  Weights are taken from the reference model
+// in param_views naming (model.hpp:75-82).
+class Context {
+ public:
+  explicit Context(const ToyTransducer& m, int32_t device = 0) {
+    check_model_shapes(m);
+    rnntg_model_desc d{};
+    d.vocab_size = m.cfg.vocab_size;
+    d.enc_dim = m.cfg.enc_dim;
+    d.emb_dim = m.cfg.emb_dim;
+    d.joiner_dim = m.cfg.joiner_dim;
+    d.context_size = m.cfg.context_size;
+    d.emb = m.emb.data.data();
+    d.ctx_w = m.ctx_w.data.data();
+    d.ctx_b = m.ctx_b.data.data();
+    d.j_we = m.j_we.data.data();
+    d.j_wd = m.j_wd.data.data();
+    d.j_b = m.j_b.data.data();
+    d.out_w = m.out_w.data.data();
+    d.out_b = m.out_b.data.data();
+    check(rnntg_model_create(&d, device, &h_));
+  }
+  ~Context() { rnntg_model_destroy(h_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  rnntg_model_t handle() const { return h_; }
+
+ private:
+  rnntg_model_t h_ = nullptr;
+};
+
+namespace detail {
+
+struct Frames {
+  std::vector<float> enc;
+  std::vector<int32_t> splits;
+};
+
+inline Frames encode(const ToyTransducer& m, const std::vector<Mat<float>>& batch) {
+  Frames f;
+  f.splits.push_back(0);
+  for (const Mat<float>& x : batch) {
+    Mat<float> e = encoder_forward(m, x);
+    f.enc.insert(f.enc.end(), e.data.begin(), e.data.end());
+    f.splits.push_back(f.splits.back() + e.rows);
+  }
+  return f;
+}
+
+inline std::vector<std::vector<int32_t>> unpack(const std::vector<int32_t>& splits,
+                                                const std::vector<int32_t>& toks) {
+  std::vector<std::vector<int32_t>> out(splits.size() - 1);
+  for (size_t i = 0; i + 1 < splits.size(); ++i)
+    out[i].assign(toks.begin() + splits[i], toks.begin() + splits[i + 1]);
+  return out;
+}
+
+}  // namespace detail
+
+inline std::vector<std::vector<int32_t>> greedy_search_batch(
+    Context& ctx, const ToyTransducer& m, const std::vector<Mat<float>>& batch,
+    int32_t max_symbols = 1) {
+  if (max_symbols != 1)
+    throw ValidationError("greedy_search_batch supports max_symbols = 1 only");
+  detail::Frames f = detail::encode(m, batch);
+  const int32_t B = static_cast<int32_t>(batch.size());
+  std::vector<int32_t> splits(B + 1), toks(std::max<int32_t>(1, f.splits.back()));
+  check(rnntg_greedy_search_batch(ctx.handle(), f.enc.data(), f.splits.data(), B, max_symbols,
+                                  RNNTG_MEM_HOST, splits.data(), toks.data()));
+  return detail::unpack(splits, toks);
+}
+
+inline std::vector<std::vector<int32_t>> beam_search_batch(
+    Context& ctx, const ToyTransducer& m, const std::vector<Mat<float>>& batch,
+    const SearchParams& params, std::vector<double>* scores = nullptr) {
+  if (params.max_symbols < 1) throw ValidationError("max_symbols must be >= 1");
+  if (params.beam_size < 1) throw ValidationError("beam_size must be >= 1");
+  detail::Frames f = detail::encode(m, batch);
+  const int32_t B = static_cast<int32_t>(batch.size());
+  rnntg_beam_params p{params.beam_size, params.max_symbols,
+                      params.merge_op == MergeOp::kLogAdd ? RNNTG_MERGE_LOG_ADD : RNNTG_MERGE_MAX,
+                      params.length_norm ? 1 : 0, params.max_total_symbols};
+  std::vector<int32_t> splits(B + 1), toks(std::max<int32_t>(1, f.splits.back()));
+  std::vector<double> sc(std::max<int32_t>(1, B));
+  check(rnntg_beam_search_batch(ctx.handle(), f.enc.data(), f.splits.data(), B, &p,
+                                RNNTG_MEM_HOST, splits.data(), toks.data(), sc.data()));
+  if (scores) scores->assign(sc.begin(), sc.begin() + B);
+  return detail::unpack(splits, toks);
+}
+
+inline std::vector<int32_t> beam_search(Context& ctx, const ToyTransducer& m,
+                                        const Mat<float>& features,
+                                        const SearchParams& params) {
+  return beam_search_batch(ctx, m, {features}, params)[0];
+}
+
+// fsa_beam_search followed by lattice_to_best_seq(kMax) for every stream,
+// with one graph shared by all streams (the CLI's usage, rnnt_main.cpp:297).
+inline std::vector<std::vector<int32_t>> fsa_best_sequences(
+    Context& ctx, const ToyTransducer& m, const std::vector<Mat<float>>& batch,
+    const Fsa& graph, const FsaSearchParams& params,
+    std::vector<double>* scores = nullptr) {
+  std::vector<int32_t> dst, label;
+  std::vector<double> w;
+  for (const Arc& a : graph.arcs) {
+    dst.push_back(a.dst);
+    label.push_back(a.label);
+    w.push_back(a.score);
+  }
+  rnntg_graph_t g = nullptr;
+  check(rnntg_graph_create(ctx.handle(), graph.num_states, graph.arc_splits.data(),
+                           static_cast<int32_t>(graph.arcs.size()), dst.data(), label.data(),
+                           w.data(), &g));
+  detail::Frames f = detail::encode(m, batch);
+  const int32_t B = static_cast<int32_t>(batch.size());
+  rnntg_fsa_params p{params.beam, params.max_states, params.max_contexts};
+  std::vector<int32_t> splits(B + 1), toks(std::max<int32_t>(1, f.splits.back()));
+  std::vector<double> sc(std::max<int32_t>(1, B));
+  const rnntg_status st = rnntg_fsa_beam_search(ctx.handle(), f.enc.data(), f.splits.data(), B, g, &p,
+                                                RNNTG_MEM_HOST, splits.data(), toks.data(), sc.data());
+  rnntg_graph_destroy(g);
+  check(st);
+  if (scores) scores->assign(sc.begin(), sc.begin() + B);
+  return detail::unpack(splits, toks);
+}
+
+}  // namespace gpu
+}  // namespace rnnt
+
+#endif  // RNNT_GPU_HPP_

@@ -1,0 +1,64 @@
+// Drop-in check: the same caller code decodes through the reference
+// (rnnt::greedy_search_batch / beam_search / fsa_beam_search +
+// lattice_to_best_seq) and through rnnt::gpu (include/rnnt_gpu.hpp over
+// librnntg.so); outputs must be identical.  Built against the reference
+// headers by tests/cpp/Makefile; run on the GPU by tests/test_cpp_shim.py.
+#include <cstdio>
+#include <vector>
+
+#include "rnnt/fsa_search.hpp"
+#include "rnnt/model.hpp"
+#include "rnnt/search.hpp"
+#include "rnnt_gpu.hpp"
+
+int main() {
+  using namespace rnnt;
+  ModelConfig cfg;
+  cfg.vocab_size = 500;
+  cfg.feat_dim = 80;
+  cfg.enc_dim = cfg.emb_dim = cfg.joiner_dim = 512;
+  cfg.seed = 3;
+  ToyTransducer m = init_model(cfg);
+  m.out_b.at(0, 0) += 0.4f;
+  std::vector<Mat<float>> batch;
+  for (int i = 0; i < 6; ++i) {
+    DetRng rng(900 + i);
+    Mat<float> f(10 + 7 * i, cfg.feat_dim);
+    for (float& v : f.data) v = static_cast<float>(rng.gaussian());
+    batch.push_back(f);
+  }
+  gpu::Context ctx(m, 0);
+  int bad = 0;
+  if (gpu::greedy_search_batch(ctx, m, batch) != greedy_search_batch(m, batch)) {
+    std::printf("greedy mismatch\n");
+    ++bad;
+  }
+  SearchParams sp;
+  sp.beam_size = 4;
+  auto gb = gpu::beam_search_batch(ctx, m, batch, sp);
+  for (size_t i = 0; i < batch.size(); ++i)
+    if (gb[i] != beam_search(m, batch[i], sp)) {
+      std::printf("beam mismatch %zu\n", i);
+      ++bad;
+    }
+  Fsa g = trivial_graph(cfg.vocab_size);
+  FsaSearchParams fp;
+  fp.beam = 4.0;
+  fp.max_states = 8;
+  fp.max_contexts = 4;
+  auto gf = gpu::fsa_best_sequences(ctx, m, batch, g, fp);
+  std::vector<Fsa> graphs(batch.size(), g);
+  auto lats = fsa_beam_search(m, batch, graphs, fp);
+  for (size_t i = 0; i < batch.size(); ++i)
+    if (gf[i] != lattice_to_best_seq(lats[i], MergeOp::kMax)) {
+      std::printf("fsa mismatch %zu\n", i);
+      ++bad;
+    }
+  try {
+    gpu::greedy_search_batch(ctx, m, batch, 2);
+    ++bad;
+  } catch (const ValidationError&) {
+  }
+  std::printf(bad ? "FAIL %d\n" : "OK\n", bad);
+  return bad ? 1 : 0;
+}
