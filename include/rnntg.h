@@ -114,6 +114,8 @@ typedef struct {
   int64_t kernel_launches;/* CUDA kernels launched by the call */
   float gpu_ms;           /* device time of the call (CUDA events) */
   float decode_ms;        /* device time of the persistent decode kernel */
+  int64_t phase_cycles[4];/* beam kernel, summed over CTAs: h build, joiner
+                             GEMM, row reduction, search step (SM cycles) */
 } rnntg_stats;
 
 const char* rnntg_last_error(void);

@@ -81,6 +81,7 @@ class _Stats(C.Structure):
         ("kernel_launches", C.c_int64),
         ("gpu_ms", C.c_float),
         ("decode_ms", C.c_float),
+        ("phase_cycles", C.c_int64 * 4),
     ]
 
 
@@ -283,7 +284,9 @@ class Decoder:
     def stats(self) -> dict:
         s = _Stats()
         _check(self._lib.rnntg_get_stats(self.h, C.byref(s)))
-        return {f: getattr(s, f) for f, _ in _Stats._fields_}
+        d = {f: getattr(s, f) for f, _ in _Stats._fields_}
+        d["phase_cycles"] = list(d["phase_cycles"])
+        return d
 
     # ---- searches ----
     def greedy_search_batch(self, enc, frame_splits, max_symbols=1, out_tokens=None):

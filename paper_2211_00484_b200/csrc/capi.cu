@@ -101,8 +101,8 @@ rnntg_status prepare(rnntg_model_t h, const float* enc, const int32_t* fs,
   RNNTG_CUDA_TRY(h->tok.ensure(sizeof(int32_t) * std::max<int64_t>(1, total)));
   RNNTG_CUDA_TRY(h->len.ensure(sizeof(int32_t) * std::max(1, B)));
   RNNTG_CUDA_TRY(h->score.ensure(sizeof(double) * std::max(1, B)));
-  RNNTG_CUDA_TRY(h->counters.ensure(sizeof(unsigned long long) * 8));
-  RNNTG_CUDA_TRY(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long) * 8, h->stream));
+  RNNTG_CUDA_TRY(h->counters.ensure(sizeof(unsigned long long) * 16));
+  RNNTG_CUDA_TRY(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long) * 16, h->stream));
   RNNTG_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
   if (total > 0)
     RNNTG_CUDA_TRY(rnntg::launch_gemm_exact(*d_enc, D, h->d.j_wet, h->d.Jp, nullptr,
@@ -133,7 +133,7 @@ rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
   if (B > 0)
     RNNTG_CUDA_TRY(cudaMemcpyAsync(lens.data(), h->len.ptr, sizeof(int32_t) * B,
                                    cudaMemcpyDeviceToHost, h->stream));
-  unsigned long long cnt[8];
+  unsigned long long cnt[16];
   RNNTG_CUDA_TRY(cudaMemcpyAsync(cnt, h->counters.ptr, sizeof(cnt), cudaMemcpyDeviceToHost, h->stream));
   RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
   out_splits[0] = 0;
@@ -176,6 +176,7 @@ rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
   h->stats.lattice_arcs = static_cast<int64_t>(cnt[3]);
   h->stats.tie_breaks = static_cast<int64_t>(cnt[4]);
   h->stats.kernel_launches = launches;
+  for (int i = 0; i < 4; ++i) h->stats.phase_cycles[i] = static_cast<int64_t>(cnt[8 + i]);
   h->stats.gpu_ms = ms_all;
   h->stats.decode_ms = ms_dec;
   return RNNTG_OK;
@@ -501,7 +502,7 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
       RNNTG_CUDA_TRY(h->lattice.ensure(static_cast<size_t>(cap) * 24));
       cap = static_cast<int64_t>(h->lattice.bytes / 24);
       RNNTG_CUDA_TRY(cudaMemsetAsync(h->flag.ptr, 0, 16, h->stream));
-      RNNTG_CUDA_TRY(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long) * 8, h->stream));
+      RNNTG_CUDA_TRY(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long) * 16, h->stream));
       rnntg::DecodeArgs a{};
       a.m = &h->d;
       a.pe = h->pe.as<float>();

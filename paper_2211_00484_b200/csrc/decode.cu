@@ -252,6 +252,7 @@ __device__ __forceinline__ bool cand_before(const BeamCand& a, double ka,
   return c < 0;
 }
 
+template <int BCAP>
 __global__ void __launch_bounds__(kDecodeThreads, 1)
     beam_kernel(ModelView m, const float* __restrict__ pe,
                 const int32_t* __restrict__ frame_splits, int32_t B, int32_t G,
@@ -267,8 +268,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   float* W1 = W0 + kBK * m.Vp;
   BeamSmem& S = *reinterpret_cast<BeamSmem*>(W1 + kBK * m.Vp);
   Hyps* H = reinterpret_cast<Hyps*>(&S + 1);          // [G]
-  BeamCand* C = reinterpret_cast<BeamCand*>(H + G);   // [G][kMaxBeam*kMaxBeam + kMaxBeam]
-  constexpr int kCandPerStream = kMaxBeam * kMaxBeam + 2 * kMaxBeam;
+  BeamCand* C = reinterpret_cast<BeamCand*>(H + G);   // [G][BCAP*BCAP + 2*BCAP]
+  constexpr int kCandPerStream = BCAP * BCAP + 2 * BCAP;
 
   const int s0 = blockIdx.x * G;
   const int ns = min(G, B - s0);
@@ -302,6 +303,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   }
   uint32_t g = 0;
   unsigned long long rows_total = 0, ties = 0;
+  long long ph_h = 0, ph_gemm = 0, ph_epi = 0, ph_step = 0;  // phase cycles (thread 0)
 
   for (int32_t t = 0; t < tmax; ++t) {
     // A. rows: distinct contexts per live stream (lane = stream, G <= 32).
@@ -344,8 +346,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     __syncthreads();
     const int R = S.nrows;
     rows_total += R;
+    long long c0 = clock64();
     build_h(m, pe, S.row_pe, S.row_ctx, R, HL);
+    long long c1 = clock64();
     joiner_gemm(m, pipe, g, HL, R);
+    long long c2 = clock64();
 
     // D. per row: lse, blank logit, top-`beam` tokens k >= 1 by (logit desc,
     // token asc).  Each lane keeps a sorted local top-kMaxBeam, then `beam`
@@ -353,19 +358,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     for (int r = warp; r < R; r += kWarps) {
       const float* L = HL + static_cast<int64_t>(r) * m.Vp;
       const double lse = row_lse(L, m.V);
-      float tl[kMaxBeam];
-      int tk[kMaxBeam];
+      float tl[BCAP];
+      int tk[BCAP];
 #pragma unroll
-      for (int q = 0; q < kMaxBeam; ++q) {
+      for (int q = 0; q < BCAP; ++q) {
         tl[q] = -FLT_MAX;
         tk[q] = 0x7fffffff;
       }
       for (int k = (lane == 0 ? 32 : lane); k < m.V; k += 32) {
         float cv = L[k];
         int ck = k;
-        if (!tok_before(cv, ck, tl[kMaxBeam - 1], tk[kMaxBeam - 1])) continue;
+        if (!tok_before(cv, ck, tl[BCAP - 1], tk[BCAP - 1])) continue;
 #pragma unroll
-        for (int q = 0; q < kMaxBeam; ++q) {
+        for (int q = 0; q < BCAP; ++q) {
           if (tok_before(cv, ck, tl[q], tk[q])) {
             const float tv = tl[q];
             const int tkk = tk[q];
@@ -396,12 +401,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         }
         if (lane == bl) {
 #pragma unroll
-          for (int z = 0; z < kMaxBeam - 1; ++z) {
+          for (int z = 0; z < BCAP - 1; ++z) {
             tl[z] = tl[z + 1];
             tk[z] = tk[z + 1];
           }
-          tl[kMaxBeam - 1] = -FLT_MAX;
-          tk[kMaxBeam - 1] = 0x7fffffff;
+          tl[BCAP - 1] = -FLT_MAX;
+          tk[BCAP - 1] = 0x7fffffff;
         }
       }
       if (lane == 0) {
@@ -411,6 +416,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     }
     __syncthreads();
 
+    long long c3 = clock64();
     // E. beam step, one warp per stream.  Reference order (search.hpp:
     // 223-259 at S = 1): the extensions are cut to the beam first
     // (prune_to_beam of next_level), then merged with the blank
@@ -421,7 +427,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       if (t >= T) continue;
       Hyps& h = H[i];
       BeamCand* cand = C + static_cast<int64_t>(i) * kCandPerStream;
-      BeamCand* merged = cand + kMaxBeam * kMaxBeam;  // [2 * kMaxBeam]
+      BeamCand* merged = cand + BCAP * BCAP;  // [2 * BCAP]
       uint32_t* bp = backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam;
       const int nh = h.nh;
 
@@ -588,6 +594,13 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       }
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long c4 = clock64();
+      ph_h += c1 - c0;
+      ph_gemm += c2 - c1;
+      ph_epi += c3 - c2;
+      ph_step += c4 - c3;
+    }
   }
   // Zero-frame streams: empty result, score 0.
   for (int i = threadIdx.x; i < ns; i += kDecodeThreads)
@@ -596,6 +609,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       scores[s0 + i] = 0.0;
     }
   atomicAdd(&counters[4], ties);
+  if (threadIdx.x == 0) {
+    atomicAdd(&counters[8], static_cast<unsigned long long>(ph_h));
+    atomicAdd(&counters[9], static_cast<unsigned long long>(ph_gemm));
+    atomicAdd(&counters[10], static_cast<unsigned long long>(ph_epi));
+    atomicAdd(&counters[11], static_cast<unsigned long long>(ph_step));
+  }
   if (threadIdx.x == 0) {
     mbar_wait(&S.bar[g & 1u], (g >> 1) & 1u);
     mbar_wait(&S.bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);
@@ -628,20 +647,31 @@ cudaError_t launch_decode_greedy(const DecodeArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s) {
+namespace {
+template <int BCAP>
+cudaError_t launch_beam_cap(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);
   const int G = a.streams_per_cta;
   const size_t smem = smem_common(m) + sizeof(BeamSmem) + sizeof(Hyps) * G +
-                      sizeof(BeamCand) * G * (kMaxBeam * kMaxBeam + 2 * kMaxBeam);
-  cudaError_t e = cudaFuncSetAttribute(
-      beam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-      static_cast<int>(smem));
+                      sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
+  cudaError_t e = cudaFuncSetAttribute(beam_kernel<BCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int grid = (a.B + G - 1) / G;
-  beam_kernel<<<grid, kDecodeThreads, smem, s>>>(
-      m, a.pe, a.frame_splits, a.B, G, a.beam_size, a.merge_op, a.length_norm,
-      a.max_total, a.backptr, a.tokens, a.lengths, a.scores, a.counters);
+  beam_kernel<BCAP><<<grid, kDecodeThreads, smem, s>>>(
+      m, a.pe, a.frame_splits, a.B, G, a.beam_size, a.merge_op, a.length_norm, a.max_total,
+      a.backptr, a.tokens, a.lengths, a.scores, a.counters);
   return cudaGetLastError();
+}
+}  // namespace
+
+// Hypothesis capacity is a compile-time bound (local top-k lists live in
+// registers); the runtime beam_size selects the smallest capacity >= it.
+cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s) {
+  if (a.beam_size <= 1) return launch_beam_cap<1>(a, s);
+  if (a.beam_size <= 2) return launch_beam_cap<2>(a, s);
+  if (a.beam_size <= 4) return launch_beam_cap<4>(a, s);
+  return launch_beam_cap<8>(a, s);
 }
 
 }  // namespace rnntg

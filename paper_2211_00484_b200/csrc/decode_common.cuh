@@ -33,6 +33,20 @@ struct ModelView {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// Explicit shared-space loads: the out_w stage is addressed through a
+// runtime stage index, which defeats nvcc's address-space inference (it
+// would emit generic LD.E instead of LDS).  Not volatile: the compiler may
+// schedule them; the mbarrier wait / __syncthreads asm carry "memory".
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float2 lds64(uint32_t a) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(count));
@@ -94,49 +108,63 @@ __device__ __forceinline__ void wpipe_issue(const WPipe& p, const ModelView& m,
 
 // C. logits[r][n] = out_b[n] + sum_k out_w[n][k] * h[r][k], sequential in k.
 // Hs: k-major h tile [J][kHStride]; Ls (aliasing Hs): row-major [R][Vp].
-// Warp w owns rows 4*(w/NH) .. +3 and columns (w%NH)*256 + {4l..4l+3,
-// 128+4l..128+4l+3}, NH = Vp/256.
-__device__ __forceinline__ void joiner_gemm(const ModelView& m, const WPipe& p,
-                                            uint32_t& g, float* HL, int R) {
+// Work item = (4 rows, a block of 32*TN columns); warp w takes item w.  TN
+// is picked per frame so that as many of the 16 warps as possible hold an
+// item (TN=8: lane columns {4l..4l+3, 128+4l..}; TN=4: {4l..4l+3};
+// TN=2: {2l, 2l+1}).  Every warp walks the k chunks in order, so each
+// accumulator still sees k = 0..J-1 sequentially.
+template <int TN>
+__device__ __forceinline__ void gemm_pass(const ModelView& m, const WPipe& p,
+                                          uint32_t& g, float* HL, int R) {
+  constexpr int CW = 32 * TN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int NH = m.Vp >> 8;
-  const int items = ((R + 3) >> 2) * NH;
+  const int NB = m.Vp / CW;
+  const int items = ((R + 3) >> 2) * NB;
   const bool active = warp < items;
-  const int rg = warp / NH, half = warp % NH;
-  const int col0 = half * 256 + lane * 4, col1 = col0 + 128;
-
-  float acc[4][8];
-  {
-    float4 b0 = make_float4(0, 0, 0, 0), b1 = b0;
-    if (active) {
-      b0 = *reinterpret_cast<const float4*>(m.out_b + col0);
-      b1 = *reinterpret_cast<const float4*>(m.out_b + col1);
-    }
-    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+  const int rg = warp / NB, blk = warp % NB;
+  const int cbase = blk * CW;
+  int col[TN];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j] = bv[j];
+  for (int j = 0; j < TN; ++j) {
+    if constexpr (TN == 8) col[j] = cbase + (j < 4 ? lane * 4 + j : 128 + lane * 4 + (j - 4));
+    else col[j] = cbase + lane * TN + j;
   }
-
+  float acc[4][TN];
+#pragma unroll
+  for (int j = 0; j < TN; ++j) {
+    const float b = active ? m.out_b[col[j]] : 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][j] = b;
+  }
   for (int32_t c = 0; c < p.nc; ++c, ++g) {
     const uint32_t st = g & 1u;
     mbar_wait(p.bar + st, (g >> 1) & 1u);
     if (active) {
-      const float* Ws = p.stage[st];
+      const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(kBK * m.Vp * 4);
       const int kk_end = min(kBK, m.J - c * kBK);
       const float* hp = HL + static_cast<int64_t>(c * kBK) * kHStride + rg * 4;
 #pragma unroll 4
       for (int kk = 0; kk < kk_end; ++kk) {
         const float4 h4 = *reinterpret_cast<const float4*>(hp + kk * kHStride);
-        const float4 wa = *reinterpret_cast<const float4*>(Ws + kk * m.Vp + col0);
-        const float4 wb = *reinterpret_cast<const float4*>(Ws + kk * m.Vp + col1);
         const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
-        const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+        float wv[TN];
+        const uint32_t wr = ws + static_cast<uint32_t>(kk * m.Vp) * 4u;
+        if constexpr (TN == 8) {
+          const float4 wa = lds128(wr + col[0] * 4u);
+          const float4 wb = lds128(wr + col[4] * 4u);
+          wv[0] = wa.x; wv[1] = wa.y; wv[2] = wa.z; wv[3] = wa.w;
+          wv[4] = wb.x; wv[5] = wb.y; wv[6] = wb.z; wv[7] = wb.w;
+        } else if constexpr (TN == 4) {
+          const float4 wa = lds128(wr + col[0] * 4u);
+          wv[0] = wa.x; wv[1] = wa.y; wv[2] = wa.z; wv[3] = wa.w;
+        } else {
+          const float2 wa = lds64(wr + col[0] * 4u);
+          wv[0] = wa.x; wv[1] = wa.y;
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
+          for (int j = 0; j < TN; ++j)
             acc[i][j] = fadd(acc[i][j], fmul(wv[j], hv[i]));
       }
     }
@@ -151,14 +179,32 @@ __device__ __forceinline__ void joiner_gemm(const ModelView& m, const WPipe& p,
       const int r = rg * 4 + i;
       if (r < R) {
         float* lr = HL + static_cast<int64_t>(r) * m.Vp;
-        *reinterpret_cast<float4*>(lr + col0) =
-            make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-        *reinterpret_cast<float4*>(lr + col1) =
-            make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        if constexpr (TN == 8) {
+          *reinterpret_cast<float4*>(lr + col[0]) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+          *reinterpret_cast<float4*>(lr + col[4]) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        } else if constexpr (TN == 4) {
+          *reinterpret_cast<float4*>(lr + col[0]) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        } else {
+          *reinterpret_cast<float2*>(lr + col[0]) = make_float2(acc[i][0], acc[i][1]);
+        }
       }
     }
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ void joiner_gemm(const ModelView& m, const WPipe& p,
+                                            uint32_t& g, float* HL, int R) {
+  const int rg = (R + 3) >> 2;
+  const int nb256 = m.Vp >> 8, nb128 = m.Vp >> 7, nb64 = m.Vp >> 6;
+  constexpr int W = kDecodeThreads / 32;
+  if (rg * nb256 >= 12 || rg * nb128 > W) {
+    gemm_pass<8>(m, p, g, HL, R);
+  } else if (rg * nb128 >= 12 || rg * nb64 > W) {
+    gemm_pass<4>(m, p, g, HL, R);
+  } else {
+    gemm_pass<2>(m, p, g, HL, R);
+  }
 }
 
 // B. h[r][i] = tanhf((pe[r][i] + pd[ctx_r][i]) + j_b[i]) into the k-major tile.
