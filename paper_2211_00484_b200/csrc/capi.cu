@@ -31,6 +31,9 @@ struct rnntg_model_s {
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
   Scratch finfo, nodebest, lattice, flag;
   int64_t lat_cap_hint = 0;
+  cudaStream_t cstream[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t done[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool pipelined = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   rnntg_stats stats{};
   std::mutex mu;
@@ -80,35 +83,73 @@ rnntg_status check_frames(const float* enc, const int32_t* fs, int32_t B) {
   return RNNTG_OK;
 }
 
-// Common front half of a decode call: frames on the device, pe = j_we . enc.
-rnntg_status prepare(rnntg_model_t h, const float* enc, const int32_t* fs,
-                     int32_t B, int32_t mem, const float** d_enc) {
+// Common front half of a decode call: buffers, splits, counters.
+rnntg_status prepare(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem) {
   const int64_t total = B > 0 ? fs[B] : 0;
   const int32_t D = h->d.D, J = h->d.J;
   RNNTG_CUDA_TRY(h->splits.ensure(sizeof(int32_t) * (B + 1)));
   RNNTG_CUDA_TRY(cudaMemcpyAsync(h->splits.ptr, fs, sizeof(int32_t) * (B + 1),
                                  cudaMemcpyHostToDevice, h->stream));
-  if (mem == RNNTG_MEM_HOST) {
+  if (mem == RNNTG_MEM_HOST)
     RNNTG_CUDA_TRY(h->enc.ensure(sizeof(float) * std::max<int64_t>(1, total) * D));
-    if (total > 0)
-      RNNTG_CUDA_TRY(cudaMemcpyAsync(h->enc.ptr, enc, sizeof(float) * total * D,
-                                     cudaMemcpyHostToDevice, h->stream));
-    *d_enc = h->enc.as<float>();
-  } else {
-    *d_enc = enc;
-  }
   RNNTG_CUDA_TRY(h->pe.ensure(sizeof(float) * std::max<int64_t>(1, total) * J));
   RNNTG_CUDA_TRY(h->tok.ensure(sizeof(int32_t) * std::max<int64_t>(1, total)));
   RNNTG_CUDA_TRY(h->len.ensure(sizeof(int32_t) * std::max(1, B)));
   RNNTG_CUDA_TRY(h->score.ensure(sizeof(double) * std::max(1, B)));
   RNNTG_CUDA_TRY(h->counters.ensure(sizeof(unsigned long long) * 16));
   RNNTG_CUDA_TRY(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long) * 16, h->stream));
+  return RNNTG_OK;
+}
+
+// Runs frames -> pe -> decode.  Device-resident frames: one pe GEMM and one
+// decode launch on the handle's stream.  Host frames: the batch is cut into
+// up to kChunks stream ranges (multiples of the CTA stream group G); chunk c
+// is copied, projected and decoded on its own CUDA stream, so the H2D copy of
+// chunk c+1 overlaps the decode of chunk c and the decode kernels of
+// different chunks share the SMs.  launch(b0, b1, stream) issues the decode
+// kernel for streams [b0, b1).
+template <typename Launch>
+rnntg_status run_pipeline(rnntg_model_t h, const float* enc, const int32_t* fs, int32_t B,
+                          int32_t mem, int32_t G, int64_t* launches, Launch&& launch) {
+  constexpr int kChunks = 4;
+  const int32_t D = h->d.D, J = h->d.J;
+  const float* d_enc = mem == RNNTG_MEM_HOST ? h->enc.as<float>() : enc;
+  int nch = 1;
+  if (mem == RNNTG_MEM_HOST && B >= 2 * G) nch = std::min(kChunks, B / G);
+  std::vector<int32_t> cut(nch + 1, 0);
+  for (int c = 1; c < nch; ++c) cut[c] = static_cast<int32_t>((static_cast<int64_t>(B) / G * c / nch) * G);
+  cut[nch] = B;
   RNNTG_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
-  if (total > 0)
-    RNNTG_CUDA_TRY(rnntg::launch_gemm_exact(*d_enc, D, h->d.j_wet, h->d.Jp, nullptr,
-                                            h->pe.as<float>(), J, total, J, D, false,
-                                            nullptr, 0, 0, h->stream));
-  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+  for (int c = 0; c < nch; ++c) {
+    const int32_t b0 = cut[c], b1 = cut[c + 1];
+    if (b1 <= b0) continue;
+    cudaStream_t cs = h->stream;
+    if (nch > 1) {
+      if (!h->cstream[c]) RNNTG_CUDA_TRY(cudaStreamCreateWithFlags(&h->cstream[c], cudaStreamNonBlocking));
+      cs = h->cstream[c];
+      RNNTG_CUDA_TRY(cudaStreamWaitEvent(cs, h->ev[0], 0));
+    }
+    const int64_t r0 = fs[b0], rows = fs[b1] - fs[b0];
+    if (rows > 0) {
+      if (mem == RNNTG_MEM_HOST)
+        RNNTG_CUDA_TRY(cudaMemcpyAsync(h->enc.as<float>() + r0 * D, enc + r0 * D,
+                                       sizeof(float) * rows * D, cudaMemcpyHostToDevice, cs));
+      RNNTG_CUDA_TRY(rnntg::launch_gemm_exact(d_enc + r0 * D, D, h->d.j_wet, h->d.Jp, nullptr,
+                                              h->pe.as<float>() + r0 * J, J, rows, J, D, false,
+                                              nullptr, 0, 0, cs));
+      ++*launches;
+    }
+    if (nch == 1) RNNTG_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+    RNNTG_CUDA_TRY(launch(b0, b1, cs));
+    ++*launches;
+    if (nch > 1) {
+      if (!h->done[c]) RNNTG_CUDA_TRY(cudaEventCreateWithFlags(&h->done[c], cudaEventDisableTiming));
+      RNNTG_CUDA_TRY(cudaEventRecord(h->done[c], cs));
+      RNNTG_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->done[c], 0));
+    }
+  }
+  if (nch > 1) RNNTG_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+  h->pipelined = nch > 1;
   return RNNTG_OK;
 }
 
@@ -169,7 +210,10 @@ rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
   }
   float ms_all = 0, ms_dec = 0;
   cudaEventElapsedTime(&ms_all, h->ev[0], h->ev[2]);
-  cudaEventElapsedTime(&ms_dec, h->ev[1], h->ev[2]);
+  if (h->pipelined)  // decode overlaps the copies; report the whole call
+    ms_dec = ms_all;
+  else
+    cudaEventElapsedTime(&ms_dec, h->ev[1], h->ev[2]);
   h->stats.stream_frames = static_cast<int64_t>(cnt[0]);
   h->stats.joiner_rows = static_cast<int64_t>(cnt[1]);
   h->stats.arcs_expanded = static_cast<int64_t>(cnt[2]);
@@ -299,6 +343,10 @@ rnntg_status rnntg_model_destroy(rnntg_model_t h) {
     s->release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  for (int c = 0; c < 4; ++c) {
+    if (h->cstream[c]) cudaStreamDestroy(h->cstream[c]);
+    if (h->done[c]) cudaEventDestroy(h->done[c]);
+  }
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
   return RNNTG_OK;
@@ -340,23 +388,25 @@ rnntg_status rnntg_greedy_search_batch(rnntg_model_t h, const float* enc,
   if (!out_splits) return invalid("out_splits is null");
   std::lock_guard<std::mutex> lk(h->mu);
   RNNTG_CUDA_TRY(cudaSetDevice(h->device));
-  const float* d_enc = nullptr;
-  if ((st = prepare(h, enc, fs, B, mem, &d_enc))) return st;
-  int64_t launches = fs[B] > 0 ? 1 : 0;
+  if ((st = prepare(h, fs, B, mem))) return st;
+  int64_t launches = 0;
   if (B > 0) {
-    rnntg::DecodeArgs a{};
-    a.m = &h->d;
-    a.pe = h->pe.as<float>();
-    a.frame_splits = h->splits.as<int32_t>();
-    a.B = B;
-    a.streams_per_cta = std::min(32, std::max(1, (B + h->num_sms - 1) / h->num_sms));
-    a.tokens = h->tok.as<int32_t>();
-    a.lengths = h->len.as<int32_t>();
-    a.scores = h->score.as<double>();
-    a.counters = h->counters.as<unsigned long long>();
+    const int G = std::min(32, std::max(1, (B + h->num_sms - 1) / h->num_sms));
     RNNTG_CUDA_TRY(cudaMemsetAsync(h->score.ptr, 0, sizeof(double) * B, h->stream));
-    RNNTG_CUDA_TRY(rnntg::launch_decode_greedy(a, h->stream));
-    ++launches;
+    st = run_pipeline(h, enc, fs, B, mem, G, &launches, [&](int32_t b0, int32_t b1, cudaStream_t cs) {
+      rnntg::DecodeArgs a{};
+      a.m = &h->d;
+      a.pe = h->pe.as<float>();
+      a.frame_splits = h->splits.as<int32_t>() + b0;
+      a.B = b1 - b0;
+      a.streams_per_cta = G;
+      a.tokens = h->tok.as<int32_t>();
+      a.lengths = h->len.as<int32_t>() + b0;
+      a.scores = h->score.as<double>() + b0;
+      a.counters = h->counters.as<unsigned long long>();
+      return rnntg::launch_decode_greedy(a, cs);
+    });
+    if (st) return st;
   }
   return finish(h, fs, B, mem, out_splits, out_tokens, nullptr, launches);
 }
@@ -385,30 +435,33 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
   if (!out_splits) return invalid("out_splits is null");
   std::lock_guard<std::mutex> lk(h->mu);
   RNNTG_CUDA_TRY(cudaSetDevice(h->device));
-  const float* d_enc = nullptr;
-  if ((st = prepare(h, enc, fs, B, mem, &d_enc))) return st;
-  int64_t launches = fs[B] > 0 ? 1 : 0;
+  if ((st = prepare(h, fs, B, mem))) return st;
+  int64_t launches = 0;
   if (B > 0) {
     const int64_t total = fs[B];
     RNNTG_CUDA_TRY(h->bp.ensure(sizeof(uint32_t) * (total + B) * rnntg::kMaxBeam));
-    rnntg::DecodeArgs a{};
-    a.m = &h->d;
-    a.pe = h->pe.as<float>();
-    a.frame_splits = h->splits.as<int32_t>();
-    a.B = B;
     const int gmax = std::max(1, 32 / p->beam_size);
-    a.streams_per_cta = std::min(gmax, std::max(1, (B + h->num_sms - 1) / h->num_sms));
-    a.tokens = h->tok.as<int32_t>();
-    a.lengths = h->len.as<int32_t>();
-    a.scores = h->score.as<double>();
-    a.counters = h->counters.as<unsigned long long>();
-    a.beam_size = p->beam_size;
-    a.merge_op = p->merge_op;
-    a.length_norm = p->length_norm;
-    a.max_total = p->max_total_symbols;
-    a.backptr = h->bp.as<uint32_t>();
-    RNNTG_CUDA_TRY(rnntg::launch_decode_beam(a, h->stream));
-    ++launches;
+    const int G = std::min(gmax, std::max(1, (B + h->num_sms - 1) / h->num_sms));
+    st = run_pipeline(h, enc, fs, B, mem, G, &launches, [&](int32_t b0, int32_t b1, cudaStream_t cs) {
+      rnntg::DecodeArgs a{};
+      a.m = &h->d;
+      a.pe = h->pe.as<float>();
+      a.frame_splits = h->splits.as<int32_t>() + b0;
+      a.B = b1 - b0;
+      a.streams_per_cta = G;
+      a.tokens = h->tok.as<int32_t>();
+      a.lengths = h->len.as<int32_t>() + b0;
+      a.scores = h->score.as<double>() + b0;
+      a.counters = h->counters.as<unsigned long long>();
+      a.beam_size = p->beam_size;
+      a.merge_op = p->merge_op;
+      a.length_norm = p->length_norm;
+      a.max_total = p->max_total_symbols;
+      // back-pointer rows are indexed (frame offset + stream index)
+      a.backptr = h->bp.as<uint32_t>() + static_cast<int64_t>(b0) * rnntg::kMaxBeam;
+      return rnntg::launch_decode_beam(a, cs);
+    });
+    if (st) return st;
   }
   return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
 }
@@ -483,9 +536,8 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
   if (!out_splits) return invalid("out_splits is null");
   std::lock_guard<std::mutex> lk(h->mu);
   RNNTG_CUDA_TRY(cudaSetDevice(h->device));
-  const float* d_enc = nullptr;
-  if ((st = prepare(h, enc, fs, B, mem, &d_enc))) return st;
-  int64_t launches = fs[B] > 0 ? 1 : 0;
+  if ((st = prepare(h, fs, B, mem))) return st;
+  int64_t launches = 0;
   if (B > 0) {
     const int64_t total = fs[B];
     const int K = std::min(p->max_states, rnntg::kFsaMaxStates);
@@ -503,30 +555,33 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
       cap = static_cast<int64_t>(h->lattice.bytes / 24);
       RNNTG_CUDA_TRY(cudaMemsetAsync(h->flag.ptr, 0, 16, h->stream));
       RNNTG_CUDA_TRY(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long) * 16, h->stream));
-      rnntg::DecodeArgs a{};
-      a.m = &h->d;
-      a.pe = h->pe.as<float>();
-      a.frame_splits = h->splits.as<int32_t>();
-      a.B = B;
-      a.streams_per_cta = G;
-      a.tokens = h->tok.as<int32_t>();
-      a.lengths = h->len.as<int32_t>();
-      a.scores = h->score.as<double>();
-      a.counters = h->counters.as<unsigned long long>();
-      a.graph_arcs = graph->arcs;
-      a.graph_splits = graph->splits;
-      a.graph_states = graph->num_states;
-      a.fsa_beam = p->beam;
-      a.max_states = p->max_states;
-      a.max_contexts = p->max_contexts;
-      a.lattice = h->lattice.ptr;
-      a.lattice_cap = cap;
-      a.error_flag = h->flag.as<int32_t>();
-      a.lattice_count = reinterpret_cast<unsigned long long*>(h->flag.as<char>() + 8);
-      a.lat_frame_info = h->finfo.as<int32_t>();
-      a.node_best = h->nodebest.as<double>();
-      RNNTG_CUDA_TRY(rnntg::launch_decode_fsa(a, h->stream));
-      ++launches;
+      st = run_pipeline(h, enc, fs, B, mem, G, &launches, [&](int32_t b0, int32_t b1, cudaStream_t cs) {
+        rnntg::DecodeArgs a{};
+        a.m = &h->d;
+        a.pe = h->pe.as<float>();
+        a.frame_splits = h->splits.as<int32_t>() + b0;
+        a.B = b1 - b0;
+        a.streams_per_cta = G;
+        a.tokens = h->tok.as<int32_t>();
+        a.lengths = h->len.as<int32_t>() + b0;
+        a.scores = h->score.as<double>() + b0;
+        a.counters = h->counters.as<unsigned long long>();
+        a.graph_arcs = graph->arcs;
+        a.graph_splits = graph->splits;
+        a.graph_states = graph->num_states;
+        a.fsa_beam = p->beam;
+        a.max_states = p->max_states;
+        a.max_contexts = p->max_contexts;
+        a.lattice = h->lattice.ptr;
+        a.lattice_cap = cap;
+        a.error_flag = h->flag.as<int32_t>();
+        a.lattice_count = reinterpret_cast<unsigned long long*>(h->flag.as<char>() + 8);
+        // per-(stream, frame) and per-node tables are indexed (frame offset + stream index)
+        a.lat_frame_info = h->finfo.as<int32_t>() + 4 * static_cast<int64_t>(b0);
+        a.node_best = h->nodebest.as<double>() + b0;
+        return rnntg::launch_decode_fsa(a, cs);
+      });
+      if (st) return st;
       int32_t flag = 0;
       unsigned long long used = 0;
       RNNTG_CUDA_TRY(cudaMemcpyAsync(&flag, h->flag.ptr, sizeof(flag), cudaMemcpyDeviceToHost, h->stream));

@@ -186,3 +186,23 @@ def test_invalid_arguments(big):
         dec.beam_search_batch(enc, splits, BeamParams(max_symbols=0))
     with pytest.raises(ValidationError):
         dec.greedy_search_batch(enc, np.array([1, 5], np.int32))
+
+
+def test_shard_transparency_gpu(big):
+    """Per-rank shards decoded separately == the whole batch (multi-GPU
+    correctness by construction; emulated on one GPU)."""
+    from paper_2211_00484_b200.api import BeamParams
+    from paper_2211_00484_b200.shard import local_batch
+
+    m, dec = big
+    Ts = [int(x) for x in np.random.default_rng(21).integers(0, 40, 300)]
+    _, enc, splits = H.frames(m, Ts, seed0=7000)
+    whole, wsc = dec.beam_search_batch(enc, splits, BeamParams(beam_size=4))
+    parts, psc = [], []
+    for r in range(4):
+        le, lfs, _ = local_batch(enc, splits, r, 4)
+        t, s = dec.beam_search_batch(le, lfs, BeamParams(beam_size=4))
+        parts += t
+        psc += s.tolist()
+    assert parts == whole
+    assert np.array_equal(np.array(psc), wsc)
