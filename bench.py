@@ -52,6 +52,10 @@ def synthetic_weights(seed=1):
         return rng.uniform(-s, s, size=shape).astype(np.float32)
 
     p = {
+        "enc_w1": u((D, F), F),
+        "enc_b1": u((1, D), F),
+        "enc_w2": u((D, D), D),
+        "enc_b2": u((1, D), D),
         "emb": u((V, E), E),
         "ctx_w": u((E, 2 * E), 2 * E),
         "ctx_b": u((1, E), 2 * E),
@@ -65,15 +69,18 @@ def synthetic_weights(seed=1):
     return p
 
 
-def synthetic_frames(B, T, seed):
-    """Encoder-output-like frames in (-1, 1): tanh of N(0, 0.6^2), float32."""
-    rng = np.random.Generator(np.random.PCG64(seed))
-    enc = np.empty((B * T, D), np.float32)
-    step = 65536
-    for r in range(0, B * T, step):
-        n = min(step, B * T - r)
-        enc[r : r + n] = np.tanh(rng.standard_normal((n, D), dtype=np.float32) * 0.6)
+def synthetic_frames(dec, B, T, seed, device):
+    """Encoder frames of the reference's toy encoder: features ~ N(0,1)
+     through rnntg_encoder_forward on the GPU (bit-exact
+    encoder_forward).  Returns the frames in HBM and the frame splits."""
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    feats = torch.randn((B * T, F), generator=g, device=device, dtype=torch.float32)
     splits = (np.arange(B + 1, dtype=np.int64) * T).astype(np.int32)
+    enc = torch.empty((B * T, D), dtype=torch.float32, device=device)
+    dec.encoder_forward(feats, splits, enc)
+    del feats
     return enc, splits
 
 
@@ -261,14 +268,17 @@ def main():
 
     B, T = args.batch, args.frames
     t0 = time.perf_counter()
-    dec = Decoder(ModelWeights.from_dict(synthetic_weights()), device=local)
+    weights = synthetic_weights()
+    dec = Decoder(ModelWeights.from_dict(weights), device=local)
     torch.cuda.synchronize()
     model_prep_s = time.perf_counter() - t0
+    dec.set_encoder(weights)
     stream = torch.cuda.current_stream()
     dec.set_stream(stream.cuda_stream)
 
-    enc, splits = synthetic_frames(B, T, seed=100 + rank)
-    d_enc = torch.from_numpy(enc).to(f"cuda:{local}")
+    d_enc, splits = synthetic_frames(dec, B, T, seed=100 + rank, device=f"cuda:{local}")
+    torch.cuda.synchronize()
+    enc = d_enc.cpu().numpy()
     tok = torch.zeros(B * T, dtype=torch.int32, device=f"cuda:{local}")
     sc = torch.zeros(B, dtype=torch.float64, device=f"cuda:{local}")
     params = BeamParams(beam_size=BEAM)
@@ -345,7 +355,7 @@ def main():
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f32 (exact non-fused joiner) / f64 scores",
-            "data": "synthetic: encoder frames tanh(N(0,0.36)) resident in HBM, init_model-distributed random weights (numpy PCG64), blank bias 0.4",
+            "data": "synthetic: features ~ N(0,1) through the reference toy encoder (bit-exact on GPU), frames resident in HBM; init_model-distributed random weights (numpy PCG64), blank bias 0.4",
             "config": {
                 "workload": WORKLOAD,
                 "global_batch": world * B,

@@ -172,6 +172,27 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t model, const float* enc,
                                    int32_t* out_splits, int32_t* out_tokens,
                                    double* out_scores);
 
+/* The reference's toy encoder on the GPU (encoder_forward, model.hpp:224-238;
+ * SURVEY.md §8f "next" row 3): enc[t] = tanhf(b2 + W2 . tanhf(b1 + W1 . f[t])),
+ * bit-exact with the reference (same sequential fp32 affine and glibc tanhf
+ * as the joiner).  Weights are fp32 row-major host arrays in param_views
+ * naming; enc_dim must equal the model's enc_dim. */
+typedef struct {
+  int32_t feat_dim;      /* F */
+  const float* enc_w1;   /* [D][F] */
+  const float* enc_b1;   /* [D]    */
+  const float* enc_w2;   /* [D][D] */
+  const float* enc_b2;   /* [D]    */
+} rnntg_encoder_desc;
+
+rnntg_status rnntg_model_set_encoder(rnntg_model_t model,
+                                     const rnntg_encoder_desc* desc);
+/* feats: [frame_splits[B]][F]; enc_out: [frame_splits[B]][D].  `mem` says
+ * where feats and enc_out live (host or this model's device). */
+rnntg_status rnntg_encoder_forward(rnntg_model_t model, const float* feats,
+                                   const int32_t* frame_splits, int32_t B,
+                                   int32_t mem, float* enc_out);
+
 /* Kernel-level entry points (bit-exactness tests of the joiner pieces).
  * All pointers are host memory. */
 rnntg_status rnntg_debug_decoder_projection(rnntg_model_t model,

@@ -57,6 +57,12 @@ class _Desc(C.Structure):
     ] + [(n, C.POINTER(C.c_float)) for n in PARAM_NAMES]
 
 
+class _EncDesc(C.Structure):
+    _fields_ = [("feat_dim", C.c_int32)] + [
+        (n, C.POINTER(C.c_float)) for n in ("enc_w1", "enc_b1", "enc_w2", "enc_b2")
+    ]
+
+
 class _BeamParams(C.Structure):
     _fields_ = [
         ("beam_size", C.c_int32),
@@ -109,6 +115,8 @@ def _load():
     lib.rnntg_graph_create.argtypes = [vp, i32, i32p, i32, i32p, i32p, f64p, C.POINTER(vp)]
     lib.rnntg_graph_destroy.argtypes = [vp]
     lib.rnntg_fsa_beam_search.argtypes = [vp, f32p, i32p, i32, vp, C.POINTER(_FsaParams), i32, i32p, vp, f64p]
+    lib.rnntg_model_set_encoder.argtypes = [vp, C.POINTER(_EncDesc)]
+    lib.rnntg_encoder_forward.argtypes = [vp, f32p, i32p, i32, i32, vp]
     lib.rnntg_debug_decoder_projection.argtypes = [vp, i32p, i32, f32p]
     lib.rnntg_debug_joiner_logits.argtypes = [vp, f32p, i32p, i32, f32p]
     lib.rnntg_debug_tanhf_chunk_hashes.argtypes = [i32, i32, i32, C.POINTER(C.c_uint64)]
@@ -123,6 +131,8 @@ def _load():
         "rnntg_graph_create",
         "rnntg_graph_destroy",
         "rnntg_fsa_beam_search",
+        "rnntg_model_set_encoder",
+        "rnntg_encoder_forward",
         "rnntg_debug_decoder_projection",
         "rnntg_debug_joiner_logits",
         "rnntg_debug_tanhf_chunk_hashes",
@@ -277,6 +287,32 @@ class Decoder:
 
     def __del__(self):
         self.close()
+
+    def set_encoder(self, p: dict):
+        """Uploads the reference toy encoder (enc_w1/enc_b1/enc_w2/enc_b2)."""
+        self._enc_keep = [np.ascontiguousarray(p[n], np.float32) for n in ("enc_w1", "enc_b1", "enc_w2", "enc_b2")]
+        desc = _EncDesc(
+            int(self._enc_keep[0].shape[1]), *[a.ctypes.data_as(C.POINTER(C.c_float)) for a in self._enc_keep]
+        )
+        _check(self._lib.rnntg_model_set_encoder(self.h, C.byref(desc)))
+        self.F = int(self._enc_keep[0].shape[1])
+
+    def encoder_forward(self, feats, frame_splits, out=None):
+        """encoder_forward (model.hpp:224-238) on the GPU, bit-exact.  Host
+        numpy in -> numpy out; CUDA tensor in -> `out` (CUDA tensor) filled."""
+        p, mem, splits, keep = _frames(feats, frame_splits)
+        B = len(splits) - 1
+        if mem == MEM_DEVICE:
+            _check(self._lib.rnntg_encoder_forward(self.h, p, _i32p(splits), B, mem, C.c_void_p(out.data_ptr())))
+            return out
+        enc = np.zeros((int(splits[-1]), self.D), np.float32)
+        _check(self._lib.rnntg_encoder_forward(self.h, p, _i32p(splits), B, mem, _ptr(enc)))
+        return enc
+
+    def set_joiner_mode(self, mode: str):
+        """"exact" (default, bit-exact fp32 on CUDA cores) or "bf16" (tcgen05
+        tensor cores, bf16 operands, fp32 accumulation; not token-exact)."""
+        _check(self._lib.rnntg_set_joiner_mode(self.h, {"exact": 0, "bf16": 1}[mode]))
 
     def set_stream(self, stream_handle: int | None):
         _check(self._lib.rnntg_set_stream(self.h, C.c_void_p(stream_handle or 0)))

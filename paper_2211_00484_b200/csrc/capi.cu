@@ -29,7 +29,7 @@ struct rnntg_model_s {
   int num_sms = 1;
   int joiner_mode = RNNTG_JOINER_EXACT;
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
-  Scratch finfo, nodebest, lattice, flag;
+  Scratch finfo, nodebest, lattice, flag, feat, hid;
   int64_t lat_cap_hint = 0;
   cudaStream_t cstream[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t done[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -295,6 +295,25 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
     std::copy(desc->out_b, desc->out_b + V, ob.begin());
     if ((st = upload(h, &d.out_b, ob))) return fail(st);
   }
+  if (J % 16 == 0) {
+    // bf16 out_w for the tcgen05 variant, pre-arranged chunk by chunk (16
+    // k-values per chunk) in the no-swizzle K-major UMMA core-matrix layout
+    // so each chunk is one contiguous cp.async.bulk (decode_common.cuh).
+    const int BK = 16;
+    std::vector<uint16_t> wt(static_cast<size_t>(J) * d.Vp, 0);
+    for (int32_t c = 0; c < J / BK; ++c)
+      for (int32_t v = 0; v < d.Vp; ++v)
+        for (int32_t kk = 0; kk < BK; ++kk) {
+          const float x = v < V ? desc->out_w[static_cast<size_t>(v) * J + c * BK + kk] : 0.0f;
+          uint32_t u;
+          std::memcpy(&u, &x, 4);
+          const uint32_t rnd = u + 0x7fffu + ((u >> 16) & 1u);  // round to nearest even
+          const size_t off = static_cast<size_t>(c) * d.Vp * BK +
+                             ((v >> 3) * (BK / 8) * 64 + (kk >> 3) * 64 + (v & 7) * 8 + (kk & 7));
+          wt[off] = static_cast<uint16_t>(rnd >> 16);
+        }
+    if ((st = upload(h, &d.out_w_bf16, wt))) return fail(st);
+  }
   // K0: the decoder-side joiner projection of every packed context,
   // pd[c] = j_wd . tanh(ctx_b + ctx_w . [emb[c/V]; emb[c%V]]), chunked.
   const int64_t C = static_cast<int64_t>(V) * V;
@@ -339,7 +358,7 @@ rnntg_status rnntg_model_destroy(rnntg_model_t h) {
   for (void* p : h->owned) cudaFree(p);
   for (Scratch* s : {&h->enc, &h->pe, &h->splits, &h->tok, &h->len, &h->score, &h->bp,
                      &h->counters, &h->ctx, &h->out_tok, &h->out_splits, &h->logits,
-                     &h->finfo, &h->nodebest, &h->lattice, &h->flag})
+                     &h->finfo, &h->nodebest, &h->lattice, &h->flag, &h->feat, &h->hid})
     s->release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -361,10 +380,12 @@ rnntg_status rnntg_set_stream(rnntg_model_t h, void* stream) {
 
 rnntg_status rnntg_set_joiner_mode(rnntg_model_t h, int32_t mode) {
   if (!h) return invalid("null model");
-  if (mode != RNNTG_JOINER_EXACT) {
-    set_error("bf16 tcgen05 joiner is not built in this version");
+  if (mode != RNNTG_JOINER_EXACT && mode != RNNTG_JOINER_BF16) return invalid("bad joiner mode");
+  if (mode == RNNTG_JOINER_BF16 && !h->d.out_w_bf16) {
+    set_error("bf16 tcgen05 joiner needs joiner_dim % 16 == 0");
     return RNNTG_UNSUPPORTED;
   }
+  std::lock_guard<std::mutex> lk(h->mu);
   h->joiner_mode = mode;
   return RNNTG_OK;
 }
@@ -459,6 +480,7 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       a.max_total = p->max_total_symbols;
       // back-pointer rows are indexed (frame offset + stream index)
       a.backptr = h->bp.as<uint32_t>() + static_cast<int64_t>(b0) * rnntg::kMaxBeam;
+      a.joiner_bf16 = h->joiner_mode == RNNTG_JOINER_BF16;
       return rnntg::launch_decode_beam(a, cs);
     });
     if (st) return st;
@@ -616,6 +638,59 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
     }
   }
   return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+}
+
+rnntg_status rnntg_model_set_encoder(rnntg_model_t h, const rnntg_encoder_desc* e) {
+  if (!h || !e) return invalid("null argument");
+  if (e->feat_dim < 1) return invalid("model dims must be >= 1");
+  if (!e->enc_w1 || !e->enc_b1 || !e->enc_w2 || !e->enc_b2) return invalid("encoder weight pointer is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  rnntg::DeviceModel& d = h->d;
+  const int32_t D = d.D, F = e->feat_dim, Dp = round_up(D, 128);
+  rnntg_status st;
+  if ((st = upload(h, &d.enc_w1t, transpose_pad(e->enc_w1, D, F, Dp))) ||
+      (st = upload(h, &d.enc_b1, std::vector<float>(e->enc_b1, e->enc_b1 + D))) ||
+      (st = upload(h, &d.enc_w2t, transpose_pad(e->enc_w2, D, D, Dp))) ||
+      (st = upload(h, &d.enc_b2, std::vector<float>(e->enc_b2, e->enc_b2 + D))))
+    return st;
+  d.F = F;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_encoder_forward(rnntg_model_t h, const float* feats, const int32_t* fs,
+                                   int32_t B, int32_t mem, float* enc_out) {
+  if (!h) return invalid("null model");
+  if (h->d.F == 0) return invalid("no encoder weights (rnntg_model_set_encoder)");
+  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
+  rnntg_status st = check_frames(feats, fs, B);
+  if (st) return st;
+  const int64_t total = B > 0 ? fs[B] : 0;
+  if (total == 0) return RNNTG_OK;
+  if (!enc_out) return invalid("enc_out is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  const int32_t D = h->d.D, F = h->d.F, Dp = round_up(D, 128);
+  const float* x = feats;
+  float* y = enc_out;
+  if (mem == RNNTG_MEM_HOST) {
+    RNNTG_CUDA_TRY(h->feat.ensure(sizeof(float) * total * F));
+    RNNTG_CUDA_TRY(h->enc.ensure(sizeof(float) * total * D));
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(h->feat.ptr, feats, sizeof(float) * total * F,
+                                   cudaMemcpyHostToDevice, h->stream));
+    x = h->feat.as<float>();
+    y = h->enc.as<float>();
+  }
+  RNNTG_CUDA_TRY(h->hid.ensure(sizeof(float) * total * D));
+  // encoder_forward (model.hpp:224-238): two affine + tanh layers per frame.
+  RNNTG_CUDA_TRY(rnntg::launch_gemm_exact(x, F, h->d.enc_w1t, Dp, h->d.enc_b1, h->hid.as<float>(), D,
+                                          total, D, F, true, nullptr, 0, 0, h->stream));
+  RNNTG_CUDA_TRY(rnntg::launch_gemm_exact(h->hid.as<float>(), D, h->d.enc_w2t, Dp, h->d.enc_b2, y, D,
+                                          total, D, D, true, nullptr, 0, 0, h->stream));
+  if (mem == RNNTG_MEM_HOST)
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(enc_out, y, sizeof(float) * total * D, cudaMemcpyDeviceToHost, h->stream));
+  RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return RNNTG_OK;
 }
 
 rnntg_status rnntg_debug_decoder_projection(rnntg_model_t h, const int32_t* ctxs,

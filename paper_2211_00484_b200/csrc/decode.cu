@@ -191,6 +191,11 @@ struct BeamSmem {
   int32_t nrows;
 };
 
+struct TcBars {  // tcgen05 variant: stage and completion barriers, TMEM base
+  uint64_t full[kTcStages], empty[kTcStages], done;
+  uint32_t tmem_addr;
+};
+
 // Walks two equal-length sequences backwards through the back-pointer
 // lattice and returns <0, 0, >0 for lexicographic X<Y, X==Y, X>Y.  Each
 // sequence is (layer tau, slot, pending token or -1).  Only reached on exact
@@ -252,7 +257,7 @@ __device__ __forceinline__ bool cand_before(const BeamCand& a, double ka,
   return c < 0;
 }
 
-template <int BCAP>
+template <int BCAP, bool TC>
 __global__ void __launch_bounds__(kDecodeThreads, 1)
     beam_kernel(ModelView m, const float* __restrict__ pe,
                 const int32_t* __restrict__ frame_splits, int32_t B, int32_t G,
@@ -270,12 +275,17 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   Hyps* H = reinterpret_cast<Hyps*>(&S + 1);          // [G]
   BeamCand* C = reinterpret_cast<BeamCand*>(H + G);   // [G][BCAP*BCAP + 2*BCAP]
   constexpr int kCandPerStream = BCAP * BCAP + 2 * BCAP;
+  // bf16 variant: tensor-core operand tile and its barriers after the rest.
+  unsigned char* hb = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(C + G * kCandPerStream) + 1023) & ~static_cast<uintptr_t>(1023));
+  TcBars* tb = reinterpret_cast<TcBars*>(hb + kRowCap * m.J * 2);
 
   const int s0 = blockIdx.x * G;
   const int ns = min(G, B - s0);
   if (ns <= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WPipe pipe{{W0, W1}, S.bar, (m.J + kBK - 1) / kBK};
+  TcPipe tp{smem_u32(W0), tb->full, tb->empty, &tb->done, smem_u32(hb), 0u, m.J / kTcBK};
 
   int32_t tmax = 0;
   for (int i = 0; i < ns; ++i)
@@ -292,12 +302,29 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     h.p1[0] = h.p2[0] = 0;
   }
   if (threadIdx.x == 0) {
-    mbar_init(&S.bar[0], 1);
-    mbar_init(&S.bar[1], 1);
+    if constexpr (TC) {
+      for (int i = 0; i < kTcStages; ++i) {
+        mbar_init(&tb->full[i], 1);
+        mbar_init(&tb->empty[i], 1);
+      }
+      mbar_init(&tb->done, 1);
+    } else {
+      mbar_init(&S.bar[0], 1);
+      mbar_init(&S.bar[1], 1);
+    }
     fence_mbar_init();
   }
+  if constexpr (TC) {
+    if (warp == 0) tc::tmem_alloc(&tb->tmem_addr, kTmemCols);
+    tc::fence_before_sync();
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if constexpr (TC) {
+    tc::fence_after_sync();
+    tp.tmem = tb->tmem_addr;
+    if (threadIdx.x == 0)
+      for (int i = 0; i < kTcStages; ++i) tc_issue(tp, m, i);
+  } else if (threadIdx.x == 0) {
     wpipe_issue(pipe, m, 0);
     wpipe_issue(pipe, m, 1);
   }
@@ -347,9 +374,15 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     const int R = S.nrows;
     rows_total += R;
     long long c0 = clock64();
-    build_h(m, pe, S.row_pe, S.row_ctx, R, HL);
+    if constexpr (TC)
+      build_h_tc(m, pe, S.row_pe, S.row_ctx, R, R <= 16 ? 16 : 32, hb);
+    else
+      build_h(m, pe, S.row_pe, S.row_ctx, R, HL);
     long long c1 = clock64();
-    joiner_gemm(m, pipe, g, HL, R);
+    if constexpr (TC)
+      tc_gemm(m, tp, g, static_cast<uint32_t>(t), HL, R);
+    else
+      joiner_gemm(m, pipe, g, HL, R);
     long long c2 = clock64();
 
     // D. per row: lse, blank logit, top-`beam` tokens k >= 1 by (logit desc,
@@ -615,9 +648,22 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     atomicAdd(&counters[10], static_cast<unsigned long long>(ph_epi));
     atomicAdd(&counters[11], static_cast<unsigned long long>(ph_step));
   }
+  if constexpr (TC) {
+    // Chunks g .. g+kTcStages-2 were prefetched for a frame that never came.
+    if (threadIdx.x == 0)
+      for (uint32_t x = g; x < g + kTcStages - 1; ++x) mbar_wait(&tb->full[x % kTcStages], (x / kTcStages) & 1u);
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+      tc::fence_after_sync();
+      tc::tmem_dealloc(tp.tmem, kTmemCols);
+    }
+  }
   if (threadIdx.x == 0) {
-    mbar_wait(&S.bar[g & 1u], (g >> 1) & 1u);
-    mbar_wait(&S.bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);
+    if constexpr (!TC) {
+      mbar_wait(&S.bar[g & 1u], (g >> 1) & 1u);
+      mbar_wait(&S.bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);
+    }
     unsigned long long sf = 0;
     for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
     atomicAdd(&counters[0], sf);
@@ -648,30 +694,37 @@ cudaError_t launch_decode_greedy(const DecodeArgs& a, cudaStream_t s) {
 }
 
 namespace {
-template <int BCAP>
+template <int BCAP, bool TC>
 cudaError_t launch_beam_cap(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);
   const int G = a.streams_per_cta;
-  const size_t smem = smem_common(m) + sizeof(BeamSmem) + sizeof(Hyps) * G +
-                      sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
-  cudaError_t e = cudaFuncSetAttribute(beam_kernel<BCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  size_t smem = smem_common(m) + sizeof(BeamSmem) + sizeof(Hyps) * G +
+                sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
+  if (TC) smem += 1024 + static_cast<size_t>(kRowCap) * m.J * 2 + sizeof(TcBars);
+  cudaError_t e = cudaFuncSetAttribute(beam_kernel<BCAP, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int grid = (a.B + G - 1) / G;
-  beam_kernel<BCAP><<<grid, kDecodeThreads, smem, s>>>(
+  beam_kernel<BCAP, TC><<<grid, kDecodeThreads, smem, s>>>(
       m, a.pe, a.frame_splits, a.B, G, a.beam_size, a.merge_op, a.length_norm, a.max_total,
       a.backptr, a.tokens, a.lengths, a.scores, a.counters);
   return cudaGetLastError();
+}
+
+template <bool TC>
+cudaError_t launch_beam_mode(const DecodeArgs& a, cudaStream_t s) {
+  if (a.beam_size <= 1) return launch_beam_cap<1, TC>(a, s);
+  if (a.beam_size <= 2) return launch_beam_cap<2, TC>(a, s);
+  if (a.beam_size <= 4) return launch_beam_cap<4, TC>(a, s);
+  return launch_beam_cap<8, TC>(a, s);
 }
 }  // namespace
 
 // Hypothesis capacity is a compile-time bound (local top-k lists live in
 // registers); the runtime beam_size selects the smallest capacity >= it.
+// a.joiner_bf16 selects the tcgen05 joiner variant.
 cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s) {
-  if (a.beam_size <= 1) return launch_beam_cap<1>(a, s);
-  if (a.beam_size <= 2) return launch_beam_cap<2>(a, s);
-  if (a.beam_size <= 4) return launch_beam_cap<4>(a, s);
-  return launch_beam_cap<8>(a, s);
+  return a.joiner_bf16 ? launch_beam_mode<true>(a, s) : launch_beam_mode<false>(a, s);
 }
 
 }  // namespace rnntg

@@ -3,10 +3,12 @@
 #pragma once
 
 #include <float.h>
+#include <cuda_bf16.h>
 #include <math.h>
 
 #include "exact_math.h"
 #include "internal.cuh"
+#include "tc_common.cuh"
 
 namespace rnntg {
 namespace dec {
@@ -25,6 +27,7 @@ struct ModelView {
   const float* __restrict__ out_b;   // [Vp]
   const float* __restrict__ j_b;     // [J]
   const float* __restrict__ pd;      // [V*V][J]
+  const uint16_t* __restrict__ out_w_tc;  // bf16 out_w in UMMA chunk layout (tcgen05 variant)
 };
 
 // ---------------------------------------------------------------------------
@@ -256,13 +259,125 @@ __device__ __forceinline__ bool tok_before(float la, int ka, float lb, int kb) {
 }
 
 
+// ---------------------------------------------------------------------------
+// bf16 tcgen05 joiner variant (RNNTG_JOINER_BF16; not token-exact).
+//
+// logits^T = out_w[Vp x J] . h^T[J x N] with out_w as the UMMA A operand
+// (M = 128-row tiles of the vocabulary) and the CTA's h rows as B (N = 16 or
+// 32): "swap-AB", so a handful of rows still fills 128-row MMA tiles.  out_w
+// is pre-arranged in global memory chunk by chunk (kTcBK k-values, no-swizzle
+// K-major core matrices) so one cp.async.bulk moves a chunk; kTcStages
+// chunks are in flight.  One thread issues the MMAs and commits each stage
+// back to its producer through an mbarrier; fp32 accumulators live in TMEM
+// (4 M-tiles x 32 columns) and are read with tcgen05.ld by lane quarter.
+// ---------------------------------------------------------------------------
+constexpr int kTcBK = 16;      // one UMMA K step per chunk
+constexpr int kTcStages = 4;   // 4 x 16 KB = the fp32 path's 64 KB stage area
+constexpr uint32_t kTmemCols = 128;
+
+struct TcPipe {
+  uint32_t stage0;   // smem address of stage 0
+  uint64_t* full;    // [kTcStages] chunk landed
+  uint64_t* empty;   // [kTcStages] MMAs finished reading the stage
+  uint64_t* done;    // frame's MMAs complete
+  uint32_t hb;       // smem address of the bf16 h tile (K-major, 32 x J)
+  uint32_t tmem;     // TMEM base address
+  int32_t nc;        // chunks per frame (J / kTcBK)
+};
+
+__device__ __forceinline__ uint32_t tc_stage_bytes(const ModelView& m) {
+  return static_cast<uint32_t>(m.Vp) * kTcBK * 2u;
+}
+
+__device__ __forceinline__ void tc_issue(const TcPipe& p, const ModelView& m, uint32_t g) {
+  const uint32_t c = g % static_cast<uint32_t>(p.nc), st = g % kTcStages;
+  const uint32_t bytes = tc_stage_bytes(m);
+  fence_proxy_async();
+  mbar_expect_tx(p.full + st, bytes);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          p.stage0 + st * bytes),
+      "l"(m.out_w_tc + static_cast<int64_t>(c) * m.Vp * kTcBK), "r"(bytes),
+      "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p.full + st)))
+      : "memory");
+}
+
+// h[r][i] = tanh((pe + pd[ctx]) + j_b) with the hardware tanh, stored bf16
+// into the K-major B tile; rows R..N-1 zero.
+__device__ __forceinline__ void build_h_tc(const ModelView& m, const float* pe, const int64_t* row_pe,
+                                           const int32_t* row_ctx, int R, int N, unsigned char* hb) {
+  const int J = m.J;
+  for (int idx = threadIdx.x; idx < N * J; idx += kDecodeThreads) {
+    const int r = idx / J, i = idx - r * J;
+    float h = 0.0f;
+    if (r < R) {
+      const float x = pe[row_pe[r] * J + i] + m.pd[static_cast<int64_t>(row_ctx[r]) * J + i] + m.j_b[i];
+      asm("tanh.approx.f32 %0, %1;" : "=f"(h) : "f"(x));
+    }
+    *reinterpret_cast<__nv_bfloat16*>(hb + tc::kmajor_off(r, i, J)) = __float2bfloat16_rn(h);
+  }
+  fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
+  __syncthreads();
+}
+
+__device__ __forceinline__ void tc_gemm(const ModelView& m, const TcPipe& p, uint32_t& g, uint32_t frame,
+                                        float* Ls, int R) {
+  const int N = R <= 16 ? 16 : 32;
+  const int MT = m.Vp >> 7;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = tc::idesc_bf16_f32(128, N);
+    const uint32_t sbo_a = (kTcBK / 8) * 128, sbo_b = static_cast<uint32_t>(m.J / 8) * 128;
+    const uint32_t bytes = tc_stage_bytes(m);
+    for (int c = 0; c < p.nc; ++c, ++g) {
+      const uint32_t st = g % kTcStages;
+      mbar_wait(p.full + st, (g / kTcStages) & 1u);
+      tc::fence_after_sync();
+      const uint32_t sa = p.stage0 + st * bytes;
+      const uint64_t b = tc::smem_desc(p.hb + static_cast<uint32_t>(c * kTcBK / 8) * 128u, 128u, sbo_b);
+      for (int mt = 0; mt < MT; ++mt) {
+        const uint64_t a = tc::smem_desc(sa + static_cast<uint32_t>(mt) * 16u * sbo_a, 128u, sbo_a);
+        tc::mma_bf16(p.tmem + static_cast<uint32_t>(mt) * 32u, a, b, idesc, c > 0);
+      }
+      tc::commit(p.empty + st);
+      if (g >= 1) {  // the previous chunk's stage is free once its MMAs finished
+        const uint32_t gp = g - 1;
+        mbar_wait(p.empty + gp % kTcStages, (gp / kTcStages) & 1u);
+        tc_issue(p, m, gp + kTcStages);
+      }
+    }
+    tc::commit(p.done);
+  }
+  mbar_wait(p.done, frame & 1u);
+  tc::fence_after_sync();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, mt = warp >> 2;
+  if (mt < MT) {
+    const int v = mt * 128 + q * 32 + lane;
+    const float bias = m.out_b[v];
+    const uint32_t ta = p.tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(mt) * 32u;
+    float acc[16];
+    tc::ld_32x32b_x16(ta, acc);
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (r < R) Ls[static_cast<int64_t>(r) * m.Vp + v] = acc[r] + bias;
+    if (N > 16) {
+      tc::ld_32x32b_x16(ta + 16u, acc);
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (16 + r < R) Ls[static_cast<int64_t>(16 + r) * m.Vp + v] = acc[r] + bias;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+}
+
 inline size_t smem_common(const ModelView& m) {
   const size_t hl = static_cast<size_t>(max(m.J * kHStride, kRowCap * m.Vp)) * 4;
   return hl + static_cast<size_t>(2) * kBK * m.Vp * 4;
 }
 
 inline ModelView view_of(const DeviceModel& d) {
-  return ModelView{d.V, d.J, d.Vp, d.out_wt, d.out_b, d.j_b, d.pd_table};
+  return ModelView{d.V, d.J, d.Vp, d.out_wt, d.out_b, d.j_b, d.pd_table, d.out_w_bf16};
 }
 
 }  // namespace dec

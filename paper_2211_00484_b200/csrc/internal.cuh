@@ -42,7 +42,13 @@ struct DeviceModel {
   float* out_b = nullptr;  // [Vp]
   float* pd_table = nullptr; // [V*V][J]: decoder-side joiner projection of
                              // every packed context (K0)
-  uint16_t* out_w_bf16 = nullptr; // [Vp][J] bf16 (tcgen05 variant)
+  uint16_t* out_w_bf16 = nullptr; // bf16 out_w, UMMA chunk layout (tcgen05 variant)
+  // optional encoder (rnntg_model_set_encoder): k-major transposed weights
+  int32_t F = 0;
+  float* enc_w1t = nullptr; // [F][Dp]
+  float* enc_b1 = nullptr;  // [D]
+  float* enc_w2t = nullptr; // [D][Dp]
+  float* enc_b2 = nullptr;  // [D]
   int32_t Ep = 0, Jp = 0;
 };
 
@@ -96,6 +102,7 @@ struct DecodeArgs {
   unsigned long long* counters; // device [8]
   // beam
   int32_t beam_size, merge_op, length_norm, max_total;
+  int32_t joiner_bf16;      // 1: tcgen05 bf16 joiner variant (not token-exact)
   uint32_t* backptr;        // device [(sum T + B) * kMaxBeam]
   // fsa
   const void* graph_arcs;   // device int4-packed arcs
