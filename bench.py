@@ -84,6 +84,20 @@ def synthetic_frames(dec, B, T, seed, device):
     return enc, splits
 
 
+def token_agreement(ref, hyp):
+    """1 - (token edit distance / reference tokens), pooled over streams."""
+    errs = 0
+    for a, b in zip(ref, hyp):
+        d = list(range(len(b) + 1))
+        for i, x in enumerate(a, 1):
+            prev, d[0] = d[0], i
+            for j, y in enumerate(b, 1):
+                cur = min(d[j] + 1, d[j - 1] + 1, prev + (x != y))
+                prev, d[j] = d[j], cur
+        errs += d[-1]
+    return 1.0 - errs / max(1, sum(len(a) for a in ref))
+
+
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons sampled during the timed region."""
 
@@ -300,6 +314,7 @@ def main():
             step()
             st = dec.stats()
             decode_ms.append(st["decode_ms"])
+            phase = st["phase_cycles"]
             rows += st["joiner_rows"]
             sfr += st["stream_frames"]
             launches += st["kernel_launches"]
@@ -319,6 +334,37 @@ def main():
     elapsed_ms = float(t_max.item())
     ms_per_step = elapsed_ms / args.steps
     value = world * B * T / (ms_per_step * 1e-3)
+
+    # ---- bf16 tcgen05 joiner variant (reported separately, not token-exact) ----
+    bf16 = None
+    if rank == 0:
+        ex_osp = osp.copy()
+        ex_tok = tok.cpu().numpy()
+        dec.set_joiner_mode("bf16")
+        step()
+        torch.cuda.synchronize()
+        b0 = torch.cuda.Event(enable_timing=True)
+        b1 = torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(args.steps):
+            bosp, _, _ = step()
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bms = b0.elapsed_time(b1) / args.steps
+        bf_tok = tok.cpu().numpy()
+        dec.set_joiner_mode("exact")
+        n = min(B, 256)
+        ref_seqs = [ex_tok[ex_osp[i] : ex_osp[i + 1]].tolist() for i in range(n)]
+        hyp_seqs = [bf_tok[bosp[i] : bosp[i + 1]].tolist() for i in range(n)]
+        bf16 = {
+            "value": B * T / (bms * 1e-3),
+            "unit": "frames/s",
+            "ms_per_step": bms,
+            "token_agreement": token_agreement(ref_seqs, hyp_seqs),
+            "identical_streams": float(np.mean([a == b for a, b in zip(ref_seqs, hyp_seqs)])),
+            "agreement_sample": f"first {n} streams vs the exact path (1 - token edit distance / exact tokens)",
+            "joiner": "tcgen05.mma kind::f16 (bf16 x bf16 -> fp32 TMEM), swap-AB M=128 vocab tiles, N=16/32 rows",
+        }
 
     # ---- e2e through the public API with pinned host buffers ----
     pin = torch.from_numpy(enc).pin_memory()
@@ -389,9 +435,14 @@ def main():
                 f"FFMA peak {peak['ffma_tflops']:.1f} TF/s, bf16 tensor peak 1632 TF/s for context",
             },
             "decode_kernel_ms": mean_decode_ms,
+            "decode_phase_share": {
+                k: round(v / max(1, sum(phase)), 3)
+                for k, v in zip(("h_build", "joiner_gemm", "row_reduce", "beam_step"), phase)
+            },
             "joiner_rows_per_stream_frame": rows / max(1, sfr),
             "tokens_per_frame": tokens_emitted / (B * T),
             "exact_score_ties": int(ties),
+            "bf16_variant": bf16,
             "model_prep_s": model_prep_s,
             "clocks": clk.summary(),
         }
