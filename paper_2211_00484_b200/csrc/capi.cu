@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -28,6 +29,7 @@ struct rnntg_model_s {
   cudaStream_t stream = nullptr;
   int num_sms = 1;
   int joiner_mode = RNNTG_JOINER_EXACT;
+  bool warp_specialized = true;  // RNNTG_WS=0 selects the single-group beam kernel
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
   Scratch finfo, nodebest, lattice, flag, feat, hid;
   int64_t lat_cap_hint = 0;
@@ -273,6 +275,7 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
   h->stream = h->own_stream;
   for (auto& e : h->ev) cudaEventCreate(&e);
   h->num_sms = rnntg::decode_num_sms(device);
+  if (const char* ws = std::getenv("RNNTG_WS")) h->warp_specialized = std::atoi(ws) != 0;
   rnntg::DeviceModel& d = h->d;
   d.V = V;
   d.D = D;
@@ -461,8 +464,12 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
   if (B > 0) {
     const int64_t total = fs[B];
     RNNTG_CUDA_TRY(h->bp.ensure(sizeof(uint32_t) * (total + B) * rnntg::kMaxBeam));
-    const int gmax = std::max(1, 32 / p->beam_size);
+    // Streams per CTA: enough to give every SM work, capped by the 32-row
+    // joiner tile (and, for the warp-specialised kernel, 16 rows per half).
+    const bool exact = h->joiner_mode == RNNTG_JOINER_EXACT;
+    const int gmax = std::max(1, exact ? 2 * (16 / p->beam_size) : 32 / p->beam_size);
     const int G = std::min(gmax, std::max(1, (B + h->num_sms - 1) / h->num_sms));
+    const bool ws = exact && G >= 2 && h->warp_specialized;
     st = run_pipeline(h, enc, fs, B, mem, G, &launches, [&](int32_t b0, int32_t b1, cudaStream_t cs) {
       rnntg::DecodeArgs a{};
       a.m = &h->d;
@@ -481,6 +488,7 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       // back-pointer rows are indexed (frame offset + stream index)
       a.backptr = h->bp.as<uint32_t>() + static_cast<int64_t>(b0) * rnntg::kMaxBeam;
       a.joiner_bf16 = h->joiner_mode == RNNTG_JOINER_BF16;
+      a.warp_specialized = ws;
       return rnntg::launch_decode_beam(a, cs);
     });
     if (st) return st;

@@ -23,6 +23,8 @@
 #include <float.h>
 #include <math.h>
 
+#include <algorithm>
+
 #include "decode_common.cuh"
 
 namespace rnntg {
@@ -257,6 +259,291 @@ __device__ __forceinline__ bool cand_before(const BeamCand& a, double ka,
   return c < 0;
 }
 
+// Per-row results of the row reduction, consumed by the beam step.
+struct RowRes {
+  double* lse;
+  float* l0;
+  float (*tl)[kMaxBeam];
+  int32_t (*tk)[kMaxBeam];
+};
+
+// A. joiner rows for n streams (one warp, lane = stream): one row per
+// distinct context among a live stream's hypotheses; writes the row tables
+// and each hypothesis' row index.  Returns the row count (warp-uniform).
+__device__ __forceinline__ int beam_rows(Hyps* H, int n, const int32_t* fsp, int t,
+                                         int64_t* row_pe, int32_t* row_ctx) {
+  const int lane = threadIdx.x & 31;
+  const int i = lane;
+  int cnt = 0;
+  if (i < n && t < fsp[i + 1] - fsp[i]) {
+    const Hyps& h = H[i];
+    for (int j = 0; j < h.nh; ++j) {
+      bool fresh = true;
+      for (int q = 0; q < j; ++q) fresh = fresh && h.ctx[q] != h.ctx[j];
+      cnt += fresh ? 1 : 0;
+    }
+  }
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (cnt > 0) {
+    Hyps& h = H[i];
+    const int64_t pr = fsp[i] + t;
+    int r = incl - cnt;
+    for (int j = 0; j < h.nh; ++j) {
+      int first = j;
+      for (int q = j - 1; q >= 0; --q)
+        if (h.ctx[q] == h.ctx[j]) first = q;
+      if (first == j) {
+        row_pe[r] = pr;
+        row_ctx[r] = h.ctx[j];
+        h.row[j] = r++;
+      } else {
+        h.row[j] = h.row[first];
+      }
+    }
+  }
+  return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+// D. one logits row (one warp): lse, blank logit, top-`beam` tokens k >= 1
+// by (logit desc, token asc).  Each lane keeps a sorted local top-BCAP,
+// then `beam` warp-wide pops.
+template <int BCAP>
+__device__ __forceinline__ void beam_row_reduce(const float* L, int V, int beam, int r, RowRes rr) {
+  const int lane = threadIdx.x & 31;
+  const double lse = row_lse(L, V);
+  float tl[BCAP];
+  int tk[BCAP];
+#pragma unroll
+  for (int q = 0; q < BCAP; ++q) {
+    tl[q] = -FLT_MAX;
+    tk[q] = 0x7fffffff;
+  }
+  for (int k = (lane == 0 ? 32 : lane); k < V; k += 32) {
+    float cv = L[k];
+    int ck = k;
+    if (!tok_before(cv, ck, tl[BCAP - 1], tk[BCAP - 1])) continue;
+#pragma unroll
+    for (int q = 0; q < BCAP; ++q) {
+      if (tok_before(cv, ck, tl[q], tk[q])) {
+        const float tv = tl[q];
+        const int tkk = tk[q];
+        tl[q] = cv;
+        tk[q] = ck;
+        cv = tv;
+        ck = tkk;
+      }
+    }
+  }
+  for (int q = 0; q < beam; ++q) {
+    float bv = tl[0];
+    int bk = tk[0], bl = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (tok_before(ov, ok, bv, bk)) {
+        bv = ov;
+        bk = ok;
+        bl = ol;
+      }
+    }
+    if (lane == 0) {
+      rr.tl[r][q] = bv;
+      rr.tk[r][q] = bk;
+    }
+    if (lane == bl) {
+#pragma unroll
+      for (int z = 0; z < BCAP - 1; ++z) {
+        tl[z] = tl[z + 1];
+        tk[z] = tk[z + 1];
+      }
+      tl[BCAP - 1] = -FLT_MAX;
+      tk[BCAP - 1] = 0x7fffffff;
+    }
+  }
+  if (lane == 0) {
+    rr.lse[r] = lse;
+    rr.l0[r] = L[0];
+  }
+}
+
+// E. one stream's frame (one warp).  Reference order (search.hpp:223-259 at
+// S = 1): the extensions are cut to the beam first (prune_to_beam of
+// next_level), then merged with the blank continuations by full-sequence
+// equality, then the frame set is cut.  At the stream's last frame the
+// winner (search.hpp:261-276) is traced back through the lattice.
+template <int BCAP>
+__device__ void beam_stream_step(const ModelView& m, Hyps& h, BeamCand* cand, uint32_t* bp, int t,
+                                 int T, int fs, int beam, int merge_log, int length_norm,
+                                 int max_total, RowRes rr, int32_t* tokens, int32_t* out_len,
+                                 double* out_score, unsigned long long* ties) {
+  const int lane = threadIdx.x & 31;
+  BeamCand* merged = cand + BCAP * BCAP;  // [2 * BCAP]
+  const int nh = h.nh;
+  // Stage 1: every hypothesis' top-`beam` extensions; the global top `beam`
+  // of those is the reference's pruned next_level.
+  const int next = nh * beam;
+  for (int c = lane; c < next; c += 32) {
+    const int j = c / beam, q = c % beam;
+    const int r = h.row[j];
+    const bool may_emit = max_total <= 0 || h.len[j] < max_total;
+    const int k = rr.tk[r][q];
+    BeamCand& e = cand[c];
+    e.score = (may_emit && k < m.V) ? h.score[j] + (static_cast<double>(rr.tl[r][q]) - rr.lse[r])
+                                    : -INFINITY;
+    e.parent = j;
+    e.tok = k;
+    e.len = h.len[j] + 1;
+  }
+  __syncwarp();
+  int rank[2] = {0x7fffffff, 0x7fffffff};
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int c = lane + u * 32;
+    if (c >= next || cand[c].score == -INFINITY) continue;
+    const BeamCand a = cand[c];
+    int rk = 0;
+    for (int d = 0; d < next; ++d) {
+      const BeamCand& b = cand[d];
+      if (d == c || b.score == -INFINITY) continue;
+      if (cand_before(b, b.score, a, a.score, bp, t, ties)) ++rk;
+    }
+    rank[u] = rk;
+  }
+  BeamCand sel[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+    if (rank[u] < beam) sel[u] = cand[lane + u * 32];
+  int nsel = (rank[0] < beam ? 1 : 0) + (rank[1] < beam ? 1 : 0);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nsel += __shfl_xor_sync(0xffffffffu, nsel, o);
+  __syncwarp();
+  // Stage 2 inputs: blank continuations in merged[0..nh), selected
+  // extensions (with their new identities) in cand[0..nsel) by rank.
+  if (lane < nh) {
+    const int r = h.row[lane];
+    BeamCand& b = merged[lane];
+    b.score = h.score[lane] + (static_cast<double>(rr.l0[r]) - rr.lse[r]);
+    b.h1 = h.h1[lane];
+    b.h2 = h.h2[lane];
+    b.p1 = h.p1[lane];
+    b.p2 = h.p2[lane];
+    b.parent = lane;
+    b.tok = 0;
+    b.len = h.len[lane];
+    b.ctx = h.ctx[lane];
+    b.last = h.last[lane];
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    if (rank[u] >= beam) continue;
+    BeamCand e = sel[u];
+    const int gp = e.parent;
+    e.h1 = hash_ext1(h.h1[gp], e.tok);
+    e.h2 = hash_ext2(h.h2[gp], e.tok);
+    e.p1 = h.h1[gp];
+    e.p2 = h.h2[gp];
+    e.ctx = (h.ctx[gp] % m.V) * m.V + e.tok;
+    e.last = e.tok;
+    cand[rank[u]] = e;
+  }
+  __syncwarp();
+  // merge_into (search.hpp:180-187): an extension ys_g+k equals the blank
+  // continuation of hypothesis j iff |ys_j| = |ys_g|+1, last(ys_j) = k and
+  // prefix(ys_j) = ys_g.
+  int nm = nh;
+  if (lane == 0) {
+    for (int q = 0; q < nsel; ++q) {
+      const BeamCand& e = cand[q];
+      int hit = -1;
+      for (int j = 0; j < nh; ++j)
+        if (merged[j].last == e.tok && merged[j].len == e.len && merged[j].p1 == e.p1 &&
+            merged[j].p2 == e.p2) {
+          hit = j;
+          break;
+        }
+      if (hit >= 0) {
+        double& sc = merged[hit].score;
+        if (merge_log) {  // log_add, common.hpp:48-54
+          const double a = sc, b = e.score;
+          if (a == -INFINITY) {
+            sc = b;
+          } else if (b != -INFINITY) {
+            const double hi = a > b ? a : b, lo = a > b ? b : a;
+            sc = hi + log1p(exp(lo - hi));
+          }
+        } else {
+          sc = sc > e.score ? sc : e.score;
+        }
+      } else {
+        merged[nm++] = e;
+      }
+    }
+  }
+  nm = __shfl_sync(0xffffffffu, nm, 0);
+  __syncwarp();
+  // prune_to_beam of the frame set by hyp_better.
+  int myrank = 0x7fffffff;
+  BeamCand mine;
+  if (lane < nm) {
+    mine = merged[lane];
+    int rk = 0;
+    for (int d = 0; d < nm; ++d) {
+      if (d == lane) continue;
+      if (cand_before(merged[d], merged[d].score, mine, mine.score, bp, t, ties)) ++rk;
+    }
+    myrank = rk;
+  }
+  __syncwarp();
+  if (myrank < beam) {
+    h.score[myrank] = mine.score;
+    h.h1[myrank] = mine.h1;
+    h.h2[myrank] = mine.h2;
+    h.p1[myrank] = mine.p1;
+    h.p2[myrank] = mine.p2;
+    h.ctx[myrank] = mine.ctx;
+    h.len[myrank] = mine.len;
+    h.last[myrank] = mine.last;
+    bp[(t + 1) * kMaxBeam + myrank] =
+        (static_cast<uint32_t>(mine.tok) << 8) | static_cast<uint32_t>(mine.parent);
+  }
+  if (lane == 0) h.nh = min(nm, beam);
+  __syncwarp();
+  if (t + 1 == T && lane == 0) {
+    const int nf = h.nh;
+    int best = 0;
+    for (int j = 1; j < nf; ++j) {
+      const double kj = length_norm ? h.score[j] / max(1, h.len[j]) : h.score[j];
+      const double kb = length_norm ? h.score[best] / max(1, h.len[best]) : h.score[best];
+      BeamCand a, b;
+      a.len = h.len[j];
+      a.parent = j;
+      a.tok = 0;
+      b.len = h.len[best];
+      b.parent = best;
+      b.tok = 0;
+      if (cand_before(a, kj, b, kb, bp, T, ties)) best = j;
+    }
+    *out_score = h.score[best];
+    *out_len = h.len[best];
+    int pos = h.len[best];
+    int tau = T, slot = best;
+    while (tau > 0) {
+      const uint32_t e = bp[tau * kMaxBeam + slot];
+      --tau;
+      slot = static_cast<int>(e & 0xffu);
+      const int tok = static_cast<int>(e >> 8);
+      if (tok != 0) tokens[fs + --pos] = tok;
+    }
+  }
+}
+
 template <int BCAP, bool TC>
 __global__ void __launch_bounds__(kDecodeThreads, 1)
     beam_kernel(ModelView m, const float* __restrict__ pe,
@@ -335,40 +622,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   for (int32_t t = 0; t < tmax; ++t) {
     // A. rows: distinct contexts per live stream (lane = stream, G <= 32).
     if (warp == 0) {
-      const int i = lane;
-      int cnt = 0;
-      if (i < ns && t < frame_splits[s0 + i + 1] - frame_splits[s0 + i]) {
-        const Hyps& h = H[i];
-        for (int j = 0; j < h.nh; ++j) {
-          bool fresh = true;
-          for (int q = 0; q < j; ++q) fresh = fresh && h.ctx[q] != h.ctx[j];
-          cnt += fresh ? 1 : 0;
-        }
-      }
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      if (cnt > 0) {
-        Hyps& h = H[i];
-        const int64_t pr = frame_splits[s0 + i] + t;
-        int r = incl - cnt;
-        for (int j = 0; j < h.nh; ++j) {
-          int first = j;
-          for (int q = j - 1; q >= 0; --q)
-            if (h.ctx[q] == h.ctx[j]) first = q;
-          if (first == j) {
-            S.row_pe[r] = pr;
-            S.row_ctx[r] = h.ctx[j];
-            h.row[j] = r++;
-          } else {
-            h.row[j] = h.row[first];
-          }
-        }
-      }
-      if (lane == 31) S.nrows = incl;
+      const int R0 = beam_rows(H, ns, frame_splits + s0, t, S.row_pe, S.row_ctx);
+      if (lane == 0) S.nrows = R0;
     }
     __syncthreads();
     const int R = S.nrows;
@@ -388,65 +643,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     // D. per row: lse, blank logit, top-`beam` tokens k >= 1 by (logit desc,
     // token asc).  Each lane keeps a sorted local top-kMaxBeam, then `beam`
     // warp-wide pops.
-    for (int r = warp; r < R; r += kWarps) {
-      const float* L = HL + static_cast<int64_t>(r) * m.Vp;
-      const double lse = row_lse(L, m.V);
-      float tl[BCAP];
-      int tk[BCAP];
-#pragma unroll
-      for (int q = 0; q < BCAP; ++q) {
-        tl[q] = -FLT_MAX;
-        tk[q] = 0x7fffffff;
-      }
-      for (int k = (lane == 0 ? 32 : lane); k < m.V; k += 32) {
-        float cv = L[k];
-        int ck = k;
-        if (!tok_before(cv, ck, tl[BCAP - 1], tk[BCAP - 1])) continue;
-#pragma unroll
-        for (int q = 0; q < BCAP; ++q) {
-          if (tok_before(cv, ck, tl[q], tk[q])) {
-            const float tv = tl[q];
-            const int tkk = tk[q];
-            tl[q] = cv;
-            tk[q] = ck;
-            cv = tv;
-            ck = tkk;
-          }
-        }
-      }
-      for (int q = 0; q < beam; ++q) {
-        float bv = tl[0];
-        int bk = tk[0], bl = lane;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
-          const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-          if (tok_before(ov, ok, bv, bk)) {
-            bv = ov;
-            bk = ok;
-            bl = ol;
-          }
-        }
-        if (lane == 0) {
-          S.row_tl[r][q] = bv;
-          S.row_tk[r][q] = bk;
-        }
-        if (lane == bl) {
-#pragma unroll
-          for (int z = 0; z < BCAP - 1; ++z) {
-            tl[z] = tl[z + 1];
-            tk[z] = tk[z + 1];
-          }
-          tl[BCAP - 1] = -FLT_MAX;
-          tk[BCAP - 1] = 0x7fffffff;
-        }
-      }
-      if (lane == 0) {
-        S.row_lse[r] = lse;
-        S.row_l0[r] = L[0];
-      }
-    }
+    const RowRes rr{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
+    for (int r = warp; r < R; r += kWarps)
+      beam_row_reduce<BCAP>(HL + static_cast<int64_t>(r) * m.Vp, m.V, beam, r, rr);
     __syncthreads();
 
     long long c3 = clock64();
@@ -458,173 +657,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       const int32_t fs = frame_splits[s0 + i];
       const int32_t T = frame_splits[s0 + i + 1] - fs;
       if (t >= T) continue;
-      Hyps& h = H[i];
-      BeamCand* cand = C + static_cast<int64_t>(i) * kCandPerStream;
-      BeamCand* merged = cand + BCAP * BCAP;  // [2 * BCAP]
-      uint32_t* bp = backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam;
-      const int nh = h.nh;
-
-      // Stage 1: every hypothesis' top-`beam` extensions; the global top
-      // `beam` of those is the reference's pruned next_level.
-      const int next = nh * beam;
-      for (int c = lane; c < next; c += 32) {
-        const int j = c / beam, q = c % beam;
-        const int r = h.row[j];
-        const bool may_emit = max_total <= 0 || h.len[j] < max_total;
-        const int k = S.row_tk[r][q];
-        BeamCand& e = cand[c];
-        e.score = (may_emit && k < m.V)
-                      ? h.score[j] + (static_cast<double>(S.row_tl[r][q]) - S.row_lse[r])
-                      : -INFINITY;
-        e.parent = j;
-        e.tok = k;
-        e.len = h.len[j] + 1;
-      }
-      __syncwarp();
-      int rank[2] = {0x7fffffff, 0x7fffffff};
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int c = lane + u * 32;
-        if (c >= next || cand[c].score == -INFINITY) continue;
-        const BeamCand a = cand[c];
-        int rk = 0;
-        for (int d = 0; d < next; ++d) {
-          const BeamCand& b = cand[d];
-          if (d == c || b.score == -INFINITY) continue;
-          if (cand_before(b, b.score, a, a.score, bp, t, &ties)) ++rk;
-        }
-        rank[u] = rk;
-      }
-      BeamCand sel[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-        if (rank[u] < beam) sel[u] = cand[lane + u * 32];
-      int nsel = (rank[0] < beam ? 1 : 0) + (rank[1] < beam ? 1 : 0);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) nsel += __shfl_xor_sync(0xffffffffu, nsel, o);
-      __syncwarp();
-      // Stage 2 inputs: blank continuations in merged[0..nh), selected
-      // extensions (with their new identities) in cand[0..nsel) by rank.
-      if (lane < nh) {
-        const int r = h.row[lane];
-        BeamCand& b = merged[lane];
-        b.score = h.score[lane] + (static_cast<double>(S.row_l0[r]) - S.row_lse[r]);
-        b.h1 = h.h1[lane];
-        b.h2 = h.h2[lane];
-        b.p1 = h.p1[lane];
-        b.p2 = h.p2[lane];
-        b.parent = lane;
-        b.tok = 0;
-        b.len = h.len[lane];
-        b.ctx = h.ctx[lane];
-        b.last = h.last[lane];
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (rank[u] >= beam) continue;
-        BeamCand e = sel[u];
-        const int gp = e.parent;
-        e.h1 = hash_ext1(h.h1[gp], e.tok);
-        e.h2 = hash_ext2(h.h2[gp], e.tok);
-        e.p1 = h.h1[gp];
-        e.p2 = h.h2[gp];
-        e.ctx = (h.ctx[gp] % m.V) * m.V + e.tok;
-        e.last = e.tok;
-        cand[rank[u]] = e;
-      }
-      __syncwarp();
-      // merge_into (search.hpp:180-187): an extension ys_g+k equals the blank
-      // continuation of hypothesis j iff |ys_j| = |ys_g|+1, last(ys_j) = k
-      // and prefix(ys_j) = ys_g.
-      int nm = nh;
-      if (lane == 0) {
-        for (int q = 0; q < nsel; ++q) {
-          const BeamCand& e = cand[q];
-          int hit = -1;
-          for (int j = 0; j < nh; ++j)
-            if (merged[j].last == e.tok && merged[j].len == e.len &&
-                merged[j].p1 == e.p1 && merged[j].p2 == e.p2) {
-              hit = j;
-              break;
-            }
-          if (hit >= 0) {
-            double& sc = merged[hit].score;
-            if (merge_log) {  // log_add, common.hpp:48-54
-              const double a = sc, b = e.score;
-              if (a == -INFINITY) {
-                sc = b;
-              } else if (b != -INFINITY) {
-                const double hi = a > b ? a : b, lo = a > b ? b : a;
-                sc = hi + log1p(exp(lo - hi));
-              }
-            } else {
-              sc = sc > e.score ? sc : e.score;
-            }
-          } else {
-            merged[nm++] = e;
-          }
-        }
-      }
-      nm = __shfl_sync(0xffffffffu, nm, 0);
-      __syncwarp();
-      // prune_to_beam of the frame set by hyp_better.
-      int myrank = 0x7fffffff;
-      BeamCand mine;
-      if (lane < nm) {
-        mine = merged[lane];
-        int rk = 0;
-        for (int d = 0; d < nm; ++d) {
-          if (d == lane) continue;
-          if (cand_before(merged[d], merged[d].score, mine, mine.score, bp, t, &ties)) ++rk;
-        }
-        myrank = rk;
-      }
-      __syncwarp();
-      if (myrank < beam) {
-        h.score[myrank] = mine.score;
-        h.h1[myrank] = mine.h1;
-        h.h2[myrank] = mine.h2;
-        h.p1[myrank] = mine.p1;
-        h.p2[myrank] = mine.p2;
-        h.ctx[myrank] = mine.ctx;
-        h.len[myrank] = mine.len;
-        h.last[myrank] = mine.last;
-        bp[(t + 1) * kMaxBeam + myrank] =
-            (static_cast<uint32_t>(mine.tok) << 8) | static_cast<uint32_t>(mine.parent);
-      }
-      if (lane == 0) h.nh = min(nm, beam);
-      __syncwarp();
-
-      // Stream finished: the winner by hyp_better on score or length-normed
-      // score (search.hpp:261-276), traced back through the lattice.
-      if (t + 1 == T && lane == 0) {
-        const int nf = h.nh;
-        int best = 0;
-        for (int j = 1; j < nf; ++j) {
-          const double kj = length_norm ? h.score[j] / max(1, h.len[j]) : h.score[j];
-          const double kb =
-              length_norm ? h.score[best] / max(1, h.len[best]) : h.score[best];
-          BeamCand a, b;
-          a.len = h.len[j];
-          a.parent = j;
-          a.tok = 0;
-          b.len = h.len[best];
-          b.parent = best;
-          b.tok = 0;
-          if (cand_before(a, kj, b, kb, bp, T, &ties)) best = j;
-        }
-        scores[s0 + i] = h.score[best];
-        lengths[s0 + i] = h.len[best];
-        int pos = h.len[best];
-        int tau = T, slot = best;
-        while (tau > 0) {
-          const uint32_t e = bp[tau * kMaxBeam + slot];
-          --tau;
-          slot = static_cast<int>(e & 0xffu);
-          const int tok = static_cast<int>(e >> 8);
-          if (tok != 0) tokens[fs + --pos] = tok;
-        }
-      }
+      beam_stream_step<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
+                             backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs, beam,
+                             merge_log, length_norm, max_total, rr, tokens, lengths + s0 + i,
+                             scores + s0 + i, &ties);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -694,6 +730,184 @@ cudaError_t launch_decode_greedy(const DecodeArgs& a, cudaStream_t s) {
 }
 
 namespace {
+// ---------------------------------------------------------------------------
+// Warp-specialised exact beam kernel.  The CTA's streams are split into two
+// halves with their own h/logits tiles.  Warps 0-11 (GEMM group) run the
+// exact joiner for half 0 then half 1 of each frame; warps 12-15 (POST
+// group) reduce the rows, step the beams and build the next frame's rows and
+// h tile of one half while the GEMM group computes the other half, so the
+// non-GEMM phases hide behind the dense contraction.  Hand-offs are named
+// barriers (bar.arrive by the producer group, bar.sync by the consumer):
+//   1+h  h tile of half h ready      (POST -> GEMM)
+//   3+h  logits of half h ready      (GEMM -> POST)
+//   5    GEMM group stage hand-off, 6 POST group internal.
+// Arithmetic and decisions are identical to beam_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kWsGemmWarps = 12;
+constexpr int kWsPostWarps = 4;
+constexpr int kWsHalfRows = 16;
+constexpr int kWsHStride = kWsHalfRows + 4;
+
+struct WsHalf {
+  int64_t row_pe[kWsHalfRows];
+  int32_t row_ctx[kWsHalfRows];
+  double row_lse[kWsHalfRows];
+  float row_l0[kWsHalfRows];
+  float row_tl[kWsHalfRows][kMaxBeam];
+  int32_t row_tk[kWsHalfRows][kMaxBeam];
+  int32_t nrows;
+};
+
+struct WsSmem {
+  uint64_t bar[2];
+  WsHalf half[2];
+};
+
+__device__ __forceinline__ int ws_hl_floats(const ModelView& m) {
+  return max(m.J * kWsHStride, kWsHalfRows * m.Vp);
+}
+
+template <int BCAP>
+__global__ void __launch_bounds__(kDecodeThreads, 1)
+    beam_ws_kernel(ModelView m, const float* __restrict__ pe,
+                   const int32_t* __restrict__ frame_splits, int32_t B, int32_t G, int32_t beam,
+                   int32_t merge_log, int32_t length_norm, int32_t max_total,
+                   uint32_t* __restrict__ backptr, int32_t* __restrict__ tokens,
+                   int32_t* __restrict__ lengths, double* __restrict__ scores,
+                   unsigned long long* __restrict__ counters) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int hl = ws_hl_floats(m);
+  float* HL0 = reinterpret_cast<float*>(smem_raw);
+  float* HL1 = HL0 + hl;
+  float* W0 = HL1 + hl;
+  float* W1 = W0 + kBK * m.Vp;
+  WsSmem& S = *reinterpret_cast<WsSmem*>(W1 + kBK * m.Vp);
+  Hyps* H = reinterpret_cast<Hyps*>(&S + 1);         // [G]
+  BeamCand* C = reinterpret_cast<BeamCand*>(H + G);  // [G][BCAP*BCAP + 2*BCAP]
+  constexpr int kCandPerStream = BCAP * BCAP + 2 * BCAP;
+  constexpr int kAll = kDecodeThreads;
+
+  const int s0 = blockIdx.x * G;
+  const int ns = min(G, B - s0);
+  if (ns <= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WPipe pipe{{W0, W1}, S.bar, (m.J + kBK - 1) / kBK};
+  const int nA = (ns + 1) >> 1;
+  const int hfirst[2] = {0, nA}, hcount[2] = {nA, ns - nA};
+  float* const HLh[2] = {HL0, HL1};
+
+  int32_t tmax = 0;
+  for (int i = 0; i < ns; ++i) tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
+  for (int i = threadIdx.x; i < ns; i += kAll) {
+    Hyps& h = H[i];
+    h.nh = 1;
+    h.score[0] = 0.0;
+    h.ctx[0] = 0;
+    h.len[0] = 0;
+    h.last[0] = -1;
+    h.h1[0] = 0x243f6a8885a308d3ull;
+    h.h2[0] = 0x13198a2e03707344ull;
+    h.p1[0] = h.p2[0] = 0;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  unsigned long long ties = 0, rows_total = 0;
+
+  if (warp < kWsGemmWarps) {
+    // ---- GEMM group ----
+    if (threadIdx.x == 0) {
+      wpipe_issue(pipe, m, 0);
+      wpipe_issue(pipe, m, 1);
+    }
+    uint32_t g = 0;
+    for (int32_t t = 0; t < tmax; ++t)
+      for (int hh = 0; hh < 2; ++hh) {
+        nbar_sync(1 + hh, kAll);
+        const int R = S.half[hh].nrows;
+        if (R > 0) joiner_gemm_g(m, pipe, g, HLh[hh], kWsHStride, R, kWsGemmWarps, warp, 5);
+        nbar_arrive(3 + hh, kAll);
+      }
+    if (threadIdx.x == 0) {
+      mbar_wait(&S.bar[g & 1u], (g >> 1) & 1u);
+      mbar_wait(&S.bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);
+    }
+  } else {
+    // ---- POST group ----
+    const int pw = warp - kWsGemmWarps, ptid = threadIdx.x - kWsGemmWarps * 32;
+    constexpr int kPost = kWsPostWarps * 32;
+    auto prepare = [&](int hh, int t) {  // rows + h tile of half hh for frame t
+      WsHalf& X = S.half[hh];
+      if (pw == 0) {
+        const int R = beam_rows(H + hfirst[hh], hcount[hh], frame_splits + s0 + hfirst[hh], t,
+                                X.row_pe, X.row_ctx);
+        if (lane == 0) X.nrows = R;
+      }
+      nbar_sync(6, kPost);
+      build_h_g(m, pe, X.row_pe, X.row_ctx, X.nrows, HLh[hh], kWsHStride, ptid, kPost);
+      if (ptid == 0) rows_total += X.nrows;
+      nbar_arrive(1 + hh, kAll);
+    };
+    prepare(0, 0);
+    prepare(1, 0);
+    for (int32_t t = 0; t < tmax; ++t)
+      for (int hh = 0; hh < 2; ++hh) {
+        nbar_sync(3 + hh, kAll);
+        WsHalf& X = S.half[hh];
+        const int R = X.nrows;
+        const RowRes rr{X.row_lse, X.row_l0, X.row_tl, X.row_tk};
+        for (int r = pw; r < R; r += kWsPostWarps)
+          beam_row_reduce<BCAP>(HLh[hh] + static_cast<int64_t>(r) * m.Vp, m.V, beam, r, rr);
+        nbar_sync(6, kPost);
+        for (int k = pw; k < hcount[hh]; k += kWsPostWarps) {
+          const int i = hfirst[hh] + k;
+          const int32_t fs = frame_splits[s0 + i];
+          const int32_t T = frame_splits[s0 + i + 1] - fs;
+          if (t >= T) continue;
+          beam_stream_step<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
+                                 backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs,
+                                 beam, merge_log, length_norm, max_total, rr, tokens,
+                                 lengths + s0 + i, scores + s0 + i, &ties);
+        }
+        nbar_sync(6, kPost);
+        if (t + 1 < tmax) prepare(hh, t + 1);
+      }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ns; i += kAll)
+    if (frame_splits[s0 + i + 1] == frame_splits[s0 + i]) {
+      lengths[s0 + i] = 0;
+      scores[s0 + i] = 0.0;
+    }
+  atomicAdd(&counters[4], ties);
+  if (threadIdx.x == kWsGemmWarps * 32) atomicAdd(&counters[1], rows_total);
+  if (threadIdx.x == 0) {
+    unsigned long long sf = 0;
+    for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
+    atomicAdd(&counters[0], sf);
+  }
+}
+
+template <int BCAP>
+cudaError_t launch_beam_ws(const DecodeArgs& a, cudaStream_t s) {
+  const ModelView m = view_of(*a.m);
+  const int G = a.streams_per_cta;
+  const size_t hl = static_cast<size_t>(std::max(m.J * kWsHStride, kWsHalfRows * m.Vp)) * 4;
+  const size_t smem = 2 * hl + static_cast<size_t>(2) * kBK * m.Vp * 4 + sizeof(WsSmem) +
+                      sizeof(Hyps) * G + sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
+  cudaError_t e = cudaFuncSetAttribute(beam_ws_kernel<BCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int grid = (a.B + G - 1) / G;
+  beam_ws_kernel<BCAP><<<grid, kDecodeThreads, smem, s>>>(
+      m, a.pe, a.frame_splits, a.B, G, a.beam_size, a.merge_op, a.length_norm, a.max_total,
+      a.backptr, a.tokens, a.lengths, a.scores, a.counters);
+  return cudaGetLastError();
+}
+
 template <int BCAP, bool TC>
 cudaError_t launch_beam_cap(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);
@@ -713,6 +927,12 @@ cudaError_t launch_beam_cap(const DecodeArgs& a, cudaStream_t s) {
 
 template <bool TC>
 cudaError_t launch_beam_mode(const DecodeArgs& a, cudaStream_t s) {
+  if (!TC && a.warp_specialized) {  // exact joiner, >= 2 streams per CTA
+    if (a.beam_size <= 1) return launch_beam_ws<1>(a, s);
+    if (a.beam_size <= 2) return launch_beam_ws<2>(a, s);
+    if (a.beam_size <= 4) return launch_beam_ws<4>(a, s);
+    return launch_beam_ws<8>(a, s);
+  }
   if (a.beam_size <= 1) return launch_beam_cap<1, TC>(a, s);
   if (a.beam_size <= 2) return launch_beam_cap<2, TC>(a, s);
   if (a.beam_size <= 4) return launch_beam_cap<4, TC>(a, s);

@@ -103,6 +103,7 @@ struct DecodeArgs {
   // beam
   int32_t beam_size, merge_op, length_norm, max_total;
   int32_t joiner_bf16;      // 1: tcgen05 bf16 joiner variant (not token-exact)
+  int32_t warp_specialized; // 1: beam_ws_kernel (GEMM / POST warp groups)
   uint32_t* backptr;        // device [(sum T + B) * kMaxBeam]
   // fsa
   const void* graph_arcs;   // device int4-packed arcs
