@@ -167,6 +167,45 @@ inline std::vector<std::vector<int32_t>> fsa_best_sequences(
   return detail::unpack(splits, toks);
 }
 
+// fsa_beam_search (fsa_search.hpp:326-387) with the reference's signature
+// and return type: one lattice per stream, node numbering and arc order as
+// build_lattice + make_fsa produce them.  Streams sharing a graph (by
+// content) are decoded in one device call.
+inline std::vector<Fsa> fsa_beam_search(Context& ctx, const ToyTransducer& m,
+                                        const std::vector<Mat<float>>& batch,
+                                        const std::vector<Fsa>& graphs,
+                                        const FsaSearchParams& params) {
+  if (batch.size() != graphs.size())
+    throw ValidationError("fsa_beam_search: |batch| != |graphs|");
+  std::vector<Fsa> out(batch.size());
+  std::vector<bool> done(batch.size(), false);
+  for (size_t i = 0; i < batch.size(); ++i) {
+    if (done[i]) continue;
+    std::vector<size_t> idx;
+    std::vector<Mat<float>> sub;
+    for (size_t j = i; j < batch.size(); ++j)
+      if (!done[j] && (j == i || graphs[j] == graphs[i])) {
+        idx.push_back(j);
+        sub.push_back(batch[j]);
+        done[j] = true;
+      }
+    fsa_best_sequences(ctx, m, sub, graphs[i], params);
+    for (size_t k = 0; k < idx.size(); ++k) {
+      int32_t nn = 0, na = 0;
+      check(rnntg_fsa_lattice(ctx.handle(), static_cast<int32_t>(k), &nn, &na, 0, nullptr, nullptr,
+                              nullptr, nullptr));
+      std::vector<int32_t> src(na), dst(na), lab(na);
+      std::vector<double> sc(na);
+      check(rnntg_fsa_lattice(ctx.handle(), static_cast<int32_t>(k), &nn, &na, na, src.data(),
+                              dst.data(), lab.data(), sc.data()));
+      std::vector<Arc> arcs(na);
+      for (int32_t a = 0; a < na; ++a) arcs[a] = {src[a], dst[a], lab[a], sc[a]};
+      out[idx[k]] = make_fsa(nn, std::move(arcs), {{nn - 1, 0.0}});
+    }
+  }
+  return out;
+}
+
 }  // namespace gpu
 }  // namespace rnnt
 

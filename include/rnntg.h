@@ -172,6 +172,19 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t model, const float* enc,
                                    int32_t* out_splits, int32_t* out_tokens,
                                    double* out_scores);
 
+/* Lattice of stream `stream` from the handle's last rnntg_fsa_beam_search
+ * call, exactly as the reference's fsa_beam_search returns it
+ * (fsa_search.hpp:301-317 build_lattice + make_fsa): nodes numbered frame by
+ * frame in (context, state) order, arcs grouped by source node in generation
+ * order, then one label-0 score-0 arc from every final-frame node into the
+ * super-final node num_nodes-1 (final score 0).  Host arrays of `capacity`
+ * entries; *num_arcs is always set (call with capacity 0 to size).  Returns
+ * INVALID_ARGUMENT if capacity is too small. */
+rnntg_status rnntg_fsa_lattice(rnntg_model_t model, int32_t stream,
+                               int32_t* num_nodes, int32_t* num_arcs,
+                               int32_t capacity, int32_t* src, int32_t* dst,
+                               int32_t* label, double* score);
+
 /* The reference's toy encoder on the GPU (encoder_forward, model.hpp:224-238;
  * SURVEY.md §8f "next" row 3): enc[t] = tanhf(b2 + W2 . tanhf(b1 + W1 . f[t])),
  * bit-exact with the reference (same sequential fp32 affine and glibc tanhf

@@ -115,6 +115,8 @@ def _load():
     lib.rnntg_graph_create.argtypes = [vp, i32, i32p, i32, i32p, i32p, f64p, C.POINTER(vp)]
     lib.rnntg_graph_destroy.argtypes = [vp]
     lib.rnntg_fsa_beam_search.argtypes = [vp, f32p, i32p, i32, vp, C.POINTER(_FsaParams), i32, i32p, vp, f64p]
+    lib.rnntg_fsa_lattice.argtypes = [vp, i32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), i32, vp, vp, vp, vp]
+    lib.rnntg_fsa_lattice.restype = C.c_int
     lib.rnntg_model_set_encoder.argtypes = [vp, C.POINTER(_EncDesc)]
     lib.rnntg_encoder_forward.argtypes = [vp, f32p, i32p, i32, i32, vp]
     lib.rnntg_debug_decoder_projection.argtypes = [vp, i32p, i32, f32p]
@@ -376,6 +378,21 @@ class Decoder:
             )
         )
         return _ragged(osp, tok), sc[:B].copy()
+
+    def fsa_lattice(self, stream: int) -> dict:
+        """Lattice of `stream` from the last fsa_beam_search, in the
+        reference's Fsa layout (build_lattice + make_fsa order)."""
+        nn, na = C.c_int32(), C.c_int32()
+        _check(self._lib.rnntg_fsa_lattice(self.h, stream, C.byref(nn), C.byref(na), 0, None, None, None, None))
+        n = na.value
+        src, dst, lab = (np.zeros(max(1, n), np.int32) for _ in range(3))
+        sc = np.zeros(max(1, n), np.float64)
+        _check(
+            self._lib.rnntg_fsa_lattice(
+                self.h, stream, C.byref(nn), C.byref(na), n, _ptr(src), _ptr(dst), _ptr(lab), _ptr(sc)
+            )
+        )
+        return dict(num_nodes=nn.value, src=src[:n], dst=dst[:n], label=lab[:n], score=sc[:n])
 
     # ---- kernel-level parity ----
     def decoder_projection(self, ctxs):

@@ -29,13 +29,16 @@ struct rnntg_model_s {
   cudaStream_t stream = nullptr;
   int num_sms = 1;
   int joiner_mode = RNNTG_JOINER_EXACT;
-  bool warp_specialized = true;  // RNNTG_WS=0 selects the single-group beam kernel
+  // RNNTG_WS=1 selects the warp-specialised beam kernel (measured slower on
+  // B200 at batch 1024: profiles/r01/README.md); default single-group kernel.
+  bool warp_specialized = false;
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
   Scratch finfo, nodebest, lattice, flag, feat, hid;
   int64_t lat_cap_hint = 0;
   cudaStream_t cstream[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t done[4] = {nullptr, nullptr, nullptr, nullptr};
   bool pipelined = false;
+  std::vector<int32_t> last_fsa_fs;  // frame splits of the last FSA call (lattice export)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   rnntg_stats stats{};
   std::mutex mu;
@@ -47,6 +50,7 @@ struct rnntg_graph_s {
   int32_t num_states = 0, num_arcs = 0;
   int32_t* splits = nullptr;  // device [S+1]
   void* arcs = nullptr;       // device 16-byte records {dst, label, weight}
+  double* maxw = nullptr;     // device [S]: max outgoing arc weight per state
 };
 
 namespace {
@@ -536,6 +540,17 @@ rnntg_status rnntg_graph_create(rnntg_model_t h, int32_t num_states,
   }
   cudaMemcpy(g->arcs, rec.data(), sizeof(ArcRec) * rec.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(g->splits, arc_splits, sizeof(int32_t) * (num_states + 1), cudaMemcpyHostToDevice);
+  {
+    std::vector<double> mw(num_states, -HUGE_VAL);
+    for (int32_t s = 0; s < num_states; ++s)
+      for (int32_t a = arc_splits[s]; a < arc_splits[s + 1]; ++a) mw[s] = std::max(mw[s], weight[a]);
+    if (cudaMalloc(reinterpret_cast<void**>(&g->maxw), sizeof(double) * num_states) != cudaSuccess) {
+      rnntg_graph_destroy(g);
+      set_error("cannot allocate the device graph");
+      return RNNTG_CUDA_ERROR;
+    }
+    cudaMemcpy(g->maxw, mw.data(), sizeof(double) * num_states, cudaMemcpyHostToDevice);
+  }
   *out = g;
   return RNNTG_OK;
 }
@@ -544,6 +559,7 @@ rnntg_status rnntg_graph_destroy(rnntg_graph_t g) {
   if (!g) return RNNTG_OK;
   if (g->arcs) cudaFree(g->arcs);
   if (g->splits) cudaFree(g->splits);
+  if (g->maxw) cudaFree(g->maxw);
   delete g;
   return RNNTG_OK;
 }
@@ -598,6 +614,7 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
         a.counters = h->counters.as<unsigned long long>();
         a.graph_arcs = graph->arcs;
         a.graph_splits = graph->splits;
+        a.graph_maxw = graph->maxw;
         a.graph_states = graph->num_states;
         a.fsa_beam = p->beam;
         a.max_states = p->max_states;
@@ -634,6 +651,10 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
         set_error("max_states binds above the device cap of 64 states per stream");
         return RNNTG_UNSUPPORTED;
       }
+      if (flag == 6) {
+        set_error("more than 32768 expansion candidates in one stream-frame (graph out-degree too high)");
+        return RNNTG_UNSUPPORTED;
+      }
       if (flag == 5) {
         set_error("best_path trace failed (inconsistent scores)");
         return RNNTG_INTERNAL;
@@ -645,7 +666,64 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
       break;
     }
   }
+  h->last_fsa_fs.assign(fs, fs + B + 1);
   return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+}
+
+rnntg_status rnntg_fsa_lattice(rnntg_model_t h, int32_t s, int32_t* num_nodes, int32_t* num_arcs,
+                               int32_t capacity, int32_t* src, int32_t* dst, int32_t* label,
+                               double* score) {
+  if (!h || !num_nodes || !num_arcs) return invalid("null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->last_fsa_fs.empty()) return invalid("no fsa_beam_search has run on this handle");
+  const int32_t B = static_cast<int32_t>(h->last_fsa_fs.size()) - 1;
+  if (s < 0 || s >= B) return invalid("stream index out of range");
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  const int32_t f0 = h->last_fsa_fs[s], T = h->last_fsa_fs[s + 1] - f0;
+  struct I4 {
+    int32_t off, cnt, base, n;
+  };
+  struct Arc24 {
+    int32_t src, dst, label, pad;
+    double score;
+  };
+  std::vector<I4> fi(std::max(1, T));
+  if (T > 0)
+    RNNTG_CUDA_TRY(cudaMemcpy(fi.data(), h->finfo.as<int32_t>() + 4 * (static_cast<int64_t>(f0) + s),
+                              sizeof(I4) * T, cudaMemcpyDeviceToHost));
+  // build_lattice (fsa_search.hpp:309-317): frame layers, then the hops from
+  // the final-frame nodes into the super-final node.
+  const int32_t nn = T == 0 ? 1 : fi[T - 1].base + fi[T - 1].n;
+  const int32_t first_final = T == 0 ? 0 : fi[T - 1].base;
+  const int32_t n_final = T == 0 ? 1 : fi[T - 1].n;
+  int64_t total = n_final;
+  for (int32_t t = 0; t < T; ++t) total += fi[t].cnt;
+  *num_nodes = nn + 1;
+  *num_arcs = static_cast<int32_t>(total);
+  if (capacity == 0) return RNNTG_OK;
+  if (capacity < total || !src || !dst || !label || !score) return invalid("lattice capacity too small");
+  std::vector<Arc24> buf;
+  int64_t k = 0;
+  for (int32_t t = 0; t < T; ++t) {
+    if (fi[t].cnt == 0) continue;
+    buf.resize(fi[t].cnt);
+    RNNTG_CUDA_TRY(cudaMemcpy(buf.data(), h->lattice.as<char>() + static_cast<int64_t>(fi[t].off) * 24,
+                              sizeof(Arc24) * fi[t].cnt, cudaMemcpyDeviceToHost));
+    for (const Arc24& a : buf) {
+      src[k] = a.src;
+      dst[k] = a.dst;
+      label[k] = a.label;
+      score[k] = a.score;
+      ++k;
+    }
+  }
+  for (int32_t i = 0; i < n_final; ++i, ++k) {
+    src[k] = first_final + i;
+    dst[k] = nn;
+    label[k] = 0;
+    score[k] = 0.0;
+  }
+  return RNNTG_OK;
 }
 
 rnntg_status rnntg_model_set_encoder(rnntg_model_t h, const rnntg_encoder_desc* e) {

@@ -745,6 +745,7 @@ namespace {
 // ---------------------------------------------------------------------------
 constexpr int kWsGemmWarps = 12;
 constexpr int kWsPostWarps = 4;
+constexpr int kWsThreads = (kWsGemmWarps + kWsPostWarps) * 32;
 constexpr int kWsHalfRows = 16;
 constexpr int kWsHStride = kWsHalfRows + 4;
 
@@ -785,7 +786,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   Hyps* H = reinterpret_cast<Hyps*>(&S + 1);         // [G]
   BeamCand* C = reinterpret_cast<BeamCand*>(H + G);  // [G][BCAP*BCAP + 2*BCAP]
   constexpr int kCandPerStream = BCAP * BCAP + 2 * BCAP;
-  constexpr int kAll = kDecodeThreads;
+  constexpr int kAll = kWsThreads;
 
   const int s0 = blockIdx.x * G;
   const int ns = min(G, B - s0);
@@ -826,8 +827,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     uint32_t g = 0;
     for (int32_t t = 0; t < tmax; ++t)
       for (int hh = 0; hh < 2; ++hh) {
-        nbar_sync(1 + hh, kAll);
-        const int R = S.half[hh].nrows;
+        nbar_sync(1 + hh, kAll);  // rows of half hh ready (POST group)
+        WsHalf& X = S.half[hh];
+        const int R = X.nrows;
+        build_h_g(m, pe, X.row_pe, X.row_ctx, R, HLh[hh], kWsHStride, threadIdx.x, kWsGemmWarps * 32);
+        nbar_sync(5, kWsGemmWarps * 32);
         if (R > 0) joiner_gemm_g(m, pipe, g, HLh[hh], kWsHStride, R, kWsGemmWarps, warp, 5);
         nbar_arrive(3 + hh, kAll);
       }
@@ -839,16 +843,16 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     // ---- POST group ----
     const int pw = warp - kWsGemmWarps, ptid = threadIdx.x - kWsGemmWarps * 32;
     constexpr int kPost = kWsPostWarps * 32;
-    auto prepare = [&](int hh, int t) {  // rows + h tile of half hh for frame t
+    auto prepare = [&](int hh, int t) {  // joiner rows of half hh for frame t
       WsHalf& X = S.half[hh];
       if (pw == 0) {
         const int R = beam_rows(H + hfirst[hh], hcount[hh], frame_splits + s0 + hfirst[hh], t,
                                 X.row_pe, X.row_ctx);
-        if (lane == 0) X.nrows = R;
+        if (lane == 0) {
+          X.nrows = R;
+          rows_total += R;
+        }
       }
-      nbar_sync(6, kPost);
-      build_h_g(m, pe, X.row_pe, X.row_ctx, X.nrows, HLh[hh], kWsHStride, ptid, kPost);
-      if (ptid == 0) rows_total += X.nrows;
       nbar_arrive(1 + hh, kAll);
     };
     prepare(0, 0);
@@ -902,7 +906,7 @@ cudaError_t launch_beam_ws(const DecodeArgs& a, cudaStream_t s) {
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int grid = (a.B + G - 1) / G;
-  beam_ws_kernel<BCAP><<<grid, kDecodeThreads, smem, s>>>(
+  beam_ws_kernel<BCAP><<<grid, kWsThreads, smem, s>>>(
       m, a.pe, a.frame_splits, a.B, G, a.beam_size, a.merge_op, a.length_norm, a.max_total,
       a.backptr, a.tokens, a.lengths, a.scores, a.counters);
   return cudaGetLastError();

@@ -323,11 +323,66 @@ __device__ __forceinline__ void build_h_g(const ModelView& m, const float* pe, c
                                           const int32_t* row_ctx, int R, float* HL, int hstride,
                                           int tid, int nt) {
   const int J = m.J;
-  for (int idx = tid; idx < R * J; idx += nt) {
+  const int total = R * J;
+  // Pass 1: gather (pe + pd) + j_b with many independent global loads in
+  // flight per thread; pass 2: tanhf in place.  Splitting the passes keeps
+  // the glibc-tanhf dependency chains from serialising the HBM/L2 latency.
+  if ((J & 3) == 0) {
+    // 16-byte loads: unit = 4 consecutive i of one row.
+    const int J4 = J >> 2, units = R * J4;
+    for (int base = tid; base < units; base += 4 * nt) {
+      float4 a[4], b[4];
+      int rr[4], ii[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int x = base + u * nt;
+        const bool ok = x < units;
+        rr[u] = ok ? x / J4 : 0;
+        ii[u] = ok ? (x - rr[u] * J4) * 4 : 0;
+        a[u] = ok ? *reinterpret_cast<const float4*>(pe + row_pe[rr[u]] * J + ii[u]) : make_float4(0, 0, 0, 0);
+        b[u] = ok ? *reinterpret_cast<const float4*>(m.pd + static_cast<int64_t>(row_ctx[rr[u]]) * J + ii[u])
+                  : make_float4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (base + u * nt >= units) continue;
+        const float* jb = m.j_b + ii[u];
+        float* o = HL + ii[u] * hstride + rr[u];
+        o[0] = fadd(fadd(a[u].x, b[u].x), jb[0]);
+        o[hstride] = fadd(fadd(a[u].y, b[u].y), jb[1]);
+        o[2 * hstride] = fadd(fadd(a[u].z, b[u].z), jb[2]);
+        o[3 * hstride] = fadd(fadd(a[u].w, b[u].w), jb[3]);
+      }
+    }
+    // Pass 2 over the same units (each thread reads back what it wrote).
+    for (int x = tid; x < units; x += nt) {
+      const int r = x / J4, i = (x - r * J4) * 4;
+      float* o = HL + i * hstride + r;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o[q * hstride] = rnntg_exact::tanhf_glibc(o[q * hstride]);
+    }
+    return;
+  }
+  for (int base = tid; base < total; base += 4 * nt) {
+    float a[4], b[4];
+    int rr[4], ii[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = base + u * nt;
+      rr[u] = idx < total ? idx / J : 0;
+      ii[u] = idx < total ? idx - rr[u] * J : 0;
+      a[u] = idx < total ? pe[row_pe[rr[u]] * J + ii[u]] : 0.0f;
+      b[u] = idx < total ? m.pd[static_cast<int64_t>(row_ctx[rr[u]]) * J + ii[u]] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (base + u * nt < total) HL[ii[u] * hstride + rr[u]] = fadd(fadd(a[u], b[u]), m.j_b[ii[u]]);
+  }
+  // Each thread reads back only the elements it wrote (idx = tid mod nt).
+  for (int idx = tid; idx < total; idx += nt) {
     const int r = idx / J, i = idx - r * J;
-    const float a = pe[row_pe[r] * J + i];
-    const float b = m.pd[static_cast<int64_t>(row_ctx[r]) * J + i];
-    HL[i * hstride + r] = rnntg_exact::tanhf_glibc(fadd(fadd(a, b), m.j_b[i]));
+    float& x = HL[i * hstride + r];
+    x = rnntg_exact::tanhf_glibc(x);
   }
 }
 
@@ -336,14 +391,7 @@ __device__ __forceinline__ void build_h(const ModelView& m, const float* pe,
                                         const int64_t* row_pe,
                                         const int32_t* row_ctx, int R,
                                         float* HL) {
-  const int J = m.J;
-  const int total = R * J;
-  for (int idx = threadIdx.x; idx < total; idx += kDecodeThreads) {
-    const int r = idx / J, i = idx - r * J;
-    const float a = pe[row_pe[r] * J + i];
-    const float b = m.pd[static_cast<int64_t>(row_ctx[r]) * J + i];
-    HL[i * kHStride + r] = rnntg_exact::tanhf_glibc(fadd(fadd(a, b), m.j_b[i]));
-  }
+  build_h_g(m, pe, row_pe, row_ctx, R, HL, kHStride, threadIdx.x, kDecodeThreads);
   __syncthreads();
 }
 
@@ -471,8 +519,8 @@ __device__ __forceinline__ void tc_gemm(const ModelView& m, const TcPipe& p, uin
   mbar_wait(p.done, frame & 1u);
   tc::fence_after_sync();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q = warp & 3, mt = warp >> 2;
-  if (mt < MT) {
+  const int q = warp & 3;
+  for (int mt = warp >> 2; mt < MT; mt += kWarps / 4) {
     const int v = mt * 128 + q * 32 + lane;
     const float bias = m.out_b[v];
     const uint32_t ta = p.tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(mt) * 32u;

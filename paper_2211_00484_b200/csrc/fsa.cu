@@ -38,6 +38,7 @@ constexpr int kHashCap = 256;    // hot-candidate hash entries per stream
 constexpr int kBins = 256;
 constexpr int kSurvHash = 128;
 constexpr int kMaxGroups = 4;    // streams per CTA
+constexpr int kMaxRaw = 32768;   // raw candidates per stream-frame (64 states x 511 arcs)
 constexpr uint64_t kEmptyKey = ~0ull;
 
 struct ArcRec {  // matches the host ArcRec in capi.cu
@@ -58,6 +59,9 @@ struct FsaStream {
   int32_t act_ctx[kMaxStates], act_state[kMaxStates], act_node[kMaxStates], act_row[kMaxStates];
   double act_score[kMaxStates];
   int32_t act_off[kMaxStates + 1];
+  int32_t act_abase[kMaxStates];  // first CSR arc of the tuple's graph state
+  double ub;                      // upper bound on the frame's best candidate
+  uint32_t mbits[kMaxRaw / 32];   // raw candidates that enter the lattice
   int32_t row_ctx[kMaxStates];
   int32_t bins[kBins];
   uint64_t hkey[kHashCap];
@@ -76,6 +80,7 @@ struct FsaSmem {
   int64_t row_pe[kRowCap];
   int32_t row_ctx[kRowCap];
   double row_lse[kRowCap];
+  double row_lpmax[kRowCap];  // max_k lp[k] of the row
   int32_t nrows;
 };
 
@@ -169,7 +174,7 @@ __device__ __forceinline__ Raw raw_cand(const FsaStream& S, int q, const ArcRec*
     r.label = 0;
     r.arc_score = static_cast<double>(Lr[0]) - lse;
   } else {
-    const ArcRec a = arcs[splits[S.act_state[lo]] + j - 1];
+    const ArcRec a = arcs[S.act_abase[lo] + j - 1];
     r.ctx = (S.act_ctx[lo] % V) * V + a.label;
     r.state = a.dst;
     r.label = a.label;
@@ -179,16 +184,66 @@ __device__ __forceinline__ Raw raw_cand(const FsaStream& S, int q, const ArcRec*
   return r;
 }
 
-__device__ __forceinline__ int bin_of(double best, double score, double floor, double scale) {
-  if (!(score >= floor)) return -1;
-  const double d = (best - score) * scale;
-  return d >= kBins - 1 ? kBins - 1 : static_cast<int>(d);
+// kU raw candidates q0, q0+stride, ... at once: all locations first, then
+// all (independent) 16-byte arc loads, then the arithmetic, so a thread has
+// kU L2 requests in flight instead of one.
+constexpr int kU = 4;
+__device__ __forceinline__ void raw_batch(const FsaStream& S, int q0, int stride, int nraw,
+                                          const ArcRec* __restrict__ arcs, const float* L,
+                                          const double* row_lse, int Vp, int V, Raw (&r)[kU],
+                                          bool (&ok)[kU]) {
+  int ii[kU], jj[kU];
+  ArcRec a[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int q = q0 + u * stride;
+    ok[u] = q < nraw;
+    int lo = 0, hi = S.n_act - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (S.act_off[mid] <= q) lo = mid;
+      else hi = mid - 1;
+    }
+    ii[u] = lo;
+    jj[u] = ok[u] ? q - S.act_off[lo] : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < kU; ++u)
+    if (jj[u] > 0) a[u] = arcs[S.act_abase[ii[u]] + jj[u] - 1];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int lo = ii[u];
+    const int row = S.row_base + S.act_row[lo];
+    const float* Lr = L + static_cast<int64_t>(row) * Vp;
+    const double lse = row_lse[row];
+    r[u].i = lo;
+    if (jj[u] == 0) {
+      r[u].ctx = S.act_ctx[lo];
+      r[u].state = S.act_state[lo];
+      r[u].label = 0;
+      r[u].arc_score = static_cast<double>(Lr[0]) - lse;
+    } else {
+      r[u].ctx = (S.act_ctx[lo] % V) * V + a[u].label;
+      r[u].state = a[u].dst;
+      r[u].label = a[u].label;
+      r[u].arc_score = a[u].w + (static_cast<double>(Lr[a[u].label]) - lse);
+    }
+    r[u].score = S.act_score[lo] + r[u].arc_score;
+  }
+}
+
+// Histogram bin of a candidate below the stream's upper bound `ub`
+// (monotone non-increasing in the score); kBins = beyond the binned range.
+__device__ __forceinline__ int ub_bin(double ub, double score, double scale) {
+  const double d = (ub - score) * scale;
+  return d < 0.0 ? 0 : (d < kBins ? static_cast<int>(d) : kBins);
 }
 
 __global__ void __launch_bounds__(kDecodeThreads, 1)
     fsa_kernel(ModelView m, const float* __restrict__ pe, const int32_t* __restrict__ frame_splits,
                int32_t B, int32_t G, const ArcRec* __restrict__ arcs,
-               const int32_t* __restrict__ gsplits, double beam, int32_t max_states,
+               const int32_t* __restrict__ gsplits, const double* __restrict__ gmaxw,
+               double beam, int32_t max_states,
                int32_t max_contexts, LatArc* __restrict__ lat, int64_t lat_cap,
                unsigned long long* __restrict__ lat_count, int4* __restrict__ finfo,
                double* __restrict__ nodebest, int32_t* __restrict__ tokens,
@@ -216,7 +271,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int K = min(max_states, kMaxStates);
   const int64_t fbase = static_cast<int64_t>(fs) + sidx;          // frame info base
   const int64_t nbase = static_cast<int64_t>(fs) * K + sidx;       // node-best base
-  const double scale = kBins / (beam < 8.0 ? (beam > 0.0 ? beam : 1.0) : 8.0);
+  // Histogram range below the upper bound: the beam (capped at 8 nats) plus
+  // 2 nats of slack for the gap between the bound and the true best.
+  const double scale = kBins / ((beam < 8.0 ? beam : 8.0) + 2.0);
   const int M = K + 32;  // hot-candidate target
 
   int32_t tmax = 0;
@@ -242,6 +299,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   }
   uint32_t gch = 0;
   unsigned long long rows_total = 0, raw_total = 0, lat_total = 0;
+  long long ph[3] = {0, 0, 0};  // thread 0: h build, joiner GEMM, lse + expand/prune
 
   for (int32_t t = 0; t < tmax; ++t) {
     const bool live = have && t < T;
@@ -279,13 +337,23 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     __syncthreads();
     const int R = C.nrows;
     rows_total += R;
+    const long long c0 = clock64();
     build_h(m, pe, C.row_pe, C.row_ctx, R, HL);
+    const long long c1 = clock64();
     joiner_gemm(m, pipe, gch, HL, R);
+    const long long c2 = clock64();
     {
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       for (int r = warp; r < R; r += kDecodeThreads / 32) {
-        const double lse = row_lse(HL + static_cast<int64_t>(r) * m.Vp, m.V);
-        if (lane == 0) C.row_lse[r] = lse;
+        const float* L = HL + static_cast<int64_t>(r) * m.Vp;
+        const double lse = row_lse(L, m.V);
+        float mx = -FLT_MAX;
+        for (int k = lane; k < m.V; k += 32) mx = fmaxf(mx, L[k]);
+        mx = warp_max_f(mx);
+        if (lane == 0) {
+          C.row_lse[r] = lse;
+          C.row_lpmax[r] = static_cast<double>(mx) - lse;
+        }
       }
     }
     __syncthreads();
@@ -293,78 +361,110 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     if (live) {
       // ---- expand_arcs ----
       if (grp.tid == 0) {
+        // Segment offsets of the raw candidates and an upper bound on the
+        // frame's best candidate: tuple i scores at most
+        // score_i + max(0, max arc weight of its state) + max_k lp_i[k].
         int off = 0;
+        double ub = -INFINITY;
         for (int i = 0; i < S.n_act; ++i) {
+          const int st = S.act_state[i];
           S.act_off[i] = off;
-          off += 1 + gsplits[S.act_state[i] + 1] - gsplits[S.act_state[i]];
+          S.act_abase[i] = gsplits[st];
+          off += 1 + gsplits[st + 1] - gsplits[st];
+          const double bound =
+              S.act_score[i] + fmax(0.0, gmaxw[st]) + C.row_lpmax[S.row_base + S.act_row[i]];
+          ub = fmax(ub, bound);
         }
         S.act_off[S.n_act] = off;
         S.n_raw = off;
+        S.ub = ub + 1e-9 * fabs(ub) + 1e-12;  // absorbs the rounding of the bound itself
+        if (off > kMaxRaw) atomicExch(error_flag, 6);
       }
       for (int b = grp.tid; b < kBins; b += nt) S.bins[b] = 0;
       for (int b = grp.tid; b < kHashCap; b += nt) {
         S.hkey[b] = kEmptyKey;
         S.hval[b] = 0ull;
       }
+      for (int w = grp.tid; w < kMaxRaw / 32; w += nt) S.mbits[w] = 0u;
       grp.sync();
-      const int nraw = S.n_raw;
+      const int nraw = min(S.n_raw, kMaxRaw);
+      const double ub = S.ub;
       raw_total += (grp.tid == 0) ? nraw : 0;
+      // Pass A: the stream's best candidate and a histogram below `ub`.
       double mx = -INFINITY;
-      for (int q = grp.tid; q < nraw; q += nt)
-        mx = fmax(mx, raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V).score);
+      for (int q0 = grp.tid; q0 < nraw; q0 += kU * nt) {
+        Raw rc[kU];
+        bool ok[kU];
+        raw_batch(S, q0, nt, nraw, arcs, HL, C.row_lse, m.Vp, m.V, rc, ok);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          if (!ok[u]) continue;
+          mx = fmax(mx, rc[u].score);
+          const int b = ub_bin(ub, rc[u].score, scale);
+          if (b < kBins) atomicAdd(&S.bins[b], 1);
+        }
+      }
       const double best = group_max(grp, S, mx);
       const double floor = best - beam;  // prune_streams 247-248
-      for (int q = grp.tid; q < nraw; q += nt) {
-        const int b = bin_of(best, raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V).score,
-                             floor, scale);
-        if (b >= 0) atomicAdd(&S.bins[b], 1);
-      }
-      grp.sync();
+      // Smallest prefix of bins lying wholly at or above the floor that holds
+      // M candidates; kBins = every candidate at or above the floor.
       if (grp.tid == 0) {
-        int cum = 0, b = 0;
-        for (; b < kBins; ++b) {
+        int cum = 0, bstar = kBins;
+        for (int b = 0; b < kBins; ++b) {
+          if (ub - (b + 1) / scale < floor) break;
           cum += S.bins[b];
-          if (cum >= M) break;
+          if (cum >= M) {
+            bstar = b;
+            break;
+          }
         }
-        S.bstar = min(b, kBins - 1);
+        S.bstar = bstar;
         S.n_hot = 0;
       }
       grp.sync();
-      // Hot candidates into the hash; widen the threshold if duplicates left
-      // fewer than K distinct keys.
+      // Pass B: hot candidates into the hash; widen the threshold if
+      // duplicates left fewer than K distinct keys.
       while (true) {
         const int bstar = S.bstar;
-        for (int q = grp.tid; q < nraw; q += nt) {
-          const Raw rc = raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V);
-          const int b = bin_of(best, rc.score, floor, scale);
-          if (b < 0 || b > bstar) continue;
-          const uint64_t k = key_of(rc.ctx, rc.state);
-          uint32_t slot = hash_slot(k, kHashCap);
-          for (int probe = 0; probe < kHashCap; ++probe) {
-            const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(&S.hkey[slot]),
-                                            static_cast<unsigned long long>(kEmptyKey),
-                                            static_cast<unsigned long long>(k));
-            if (prev == kEmptyKey) atomicAdd(&S.n_hot, 1);
-            if (prev == kEmptyKey || prev == k) {
-              atomicMax(&S.hval[slot], ord_of(rc.score));
-              break;
+        for (int q0 = grp.tid; q0 < nraw; q0 += kU * nt) {
+          Raw rc[kU];
+          bool ok[kU];
+          raw_batch(S, q0, nt, nraw, arcs, HL, C.row_lse, m.Vp, m.V, rc, ok);
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            if (!ok[u] || rc[u].score < floor) continue;
+            if (bstar < kBins && ub_bin(ub, rc[u].score, scale) > bstar) continue;
+            const uint64_t k = key_of(rc[u].ctx, rc[u].state);
+            uint32_t slot = hash_slot(k, kHashCap);
+            for (int probe = 0; probe < kHashCap; ++probe) {
+              const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(&S.hkey[slot]),
+                                              static_cast<unsigned long long>(kEmptyKey),
+                                              static_cast<unsigned long long>(k));
+              if (prev == kEmptyKey) atomicAdd(&S.n_hot, 1);
+              if (prev == kEmptyKey || prev == k) {
+                atomicMax(&S.hval[slot], ord_of(rc[u].score));
+                break;
+              }
+              slot = (slot + 1) & (kHashCap - 1);
+              if (probe == kHashCap - 1) atomicExch(error_flag, 3);
             }
-            slot = (slot + 1) & (kHashCap - 1);
-            if (probe == kHashCap - 1) atomicExch(error_flag, 3);
           }
         }
         grp.sync();
-        if (S.n_hot >= K || bstar >= kBins - 1) break;
+        if (S.n_hot >= K || bstar >= kBins) break;
         if (S.n_hot > kHashCap / 2) break;
         grp.sync();
-        if (grp.tid == 0) {  // next bin with entries
+        if (grp.tid == 0) {  // widen by another M candidates (max is idempotent)
           int b = bstar + 1, cum = 0;
-          for (; b < kBins - 1; ++b) {
+          for (; b < kBins; ++b) {
+            if (ub - (b + 1) / scale < floor) {
+              b = kBins;
+              break;
+            }
             cum += S.bins[b];
             if (cum >= M) break;
           }
-          S.bstar = b;
-          // entries already inserted are re-offered: max is idempotent.
+          S.bstar = min(b, kBins);
         }
         grp.sync();
       }
@@ -456,16 +556,33 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       }
       grp.sync();
       // ---- lattice arcs: raw candidates into survivors, generation order ----
-      int cnt = 0;
-      for (int q = grp.tid; q < nraw; q += nt) {
-        const Raw rc = raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V);
-        const uint64_t k = key_of(rc.ctx, rc.state);
-        uint32_t slot = hash_slot(k, kSurvHash);
-        while (S.shkey[slot] != kEmptyKey && S.shkey[slot] != k) slot = (slot + 1) & (kSurvHash - 1);
-        cnt += S.shkey[slot] == k ? 1 : 0;
+      // Pass C: one bit per raw candidate whose key survived.
+      for (int q0 = grp.tid; q0 < nraw; q0 += kU * nt) {
+        Raw rc[kU];
+        bool ok[kU];
+        raw_batch(S, q0, nt, nraw, arcs, HL, C.row_lse, m.Vp, m.V, rc, ok);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          if (!ok[u]) continue;
+          const uint64_t k = key_of(rc[u].ctx, rc[u].state);
+          uint32_t slot = hash_slot(k, kSurvHash);
+          while (S.shkey[slot] != kEmptyKey && S.shkey[slot] != k) slot = (slot + 1) & (kSurvHash - 1);
+          if (S.shkey[slot] == k) {
+            const int q = q0 + u * nt;
+            atomicOr(&S.mbits[q >> 5], 1u << (q & 31));
+          }
+        }
       }
+      grp.sync();
+      // Each thread owns a contiguous run of bit words, so the scan order is
+      // the generation order.
+      const int nwords = (nraw + 31) >> 5;
+      const int wpt = (nwords + nt - 1) / nt;
+      const int w0 = min(nwords, grp.tid * wpt), w1 = min(nwords, w0 + wpt);
+      int cnt = 0;
+      for (int w = w0; w < w1; ++w) cnt += __popc(S.mbits[w]);
       int total = 0;
-      group_scan(grp, S, cnt, &total);
+      const int my_pos = group_scan(grp, S, cnt, &total);
       if (grp.tid == 0) {
         const unsigned long long off = atomicAdd(lat_count, static_cast<unsigned long long>(total));
         if (static_cast<int64_t>(off + total) > lat_cap) {
@@ -479,33 +596,27 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       grp.sync();
       const int arc_off = S.arc_off;
       lat_total += grp.tid == 0 ? total : 0;
-      int written = 0;
-      for (int q0 = 0; q0 < nraw; q0 += nt) {
-        const int q = q0 + grp.tid;
-        int hit = 0, dst = -1;
-        Raw rc;
-        if (q < nraw) {
-          rc = raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V);
-          const uint64_t k = key_of(rc.ctx, rc.state);
-          uint32_t slot = hash_slot(k, kSurvHash);
-          while (S.shkey[slot] != kEmptyKey && S.shkey[slot] != k) slot = (slot + 1) & (kSurvHash - 1);
-          if (S.shkey[slot] == k) {
-            hit = 1;
-            dst = S.shnode[slot];
+      // Pass D: only the (few) hits are recomputed and written.
+      if (arc_off >= 0) {
+        int pos = my_pos;
+        for (int w = w0; w < w1; ++w) {
+          uint32_t bits = S.mbits[w];
+          while (bits) {
+            const int q = (w << 5) + __ffs(bits) - 1;
+            bits &= bits - 1;
+            const Raw rc = raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V);
+            const uint64_t k = key_of(rc.ctx, rc.state);
+            uint32_t slot = hash_slot(k, kSurvHash);
+            while (S.shkey[slot] != k) slot = (slot + 1) & (kSurvHash - 1);
+            LatArc a;
+            a.src = S.act_node[rc.i];
+            a.dst = S.shnode[slot];
+            a.label = rc.label;
+            a.pad = 0;
+            a.score = rc.arc_score;
+            lat[static_cast<int64_t>(arc_off) + pos++] = a;
           }
         }
-        int tot = 0;
-        const int pos = group_scan(grp, S, hit, &tot);
-        if (hit && arc_off >= 0) {
-          LatArc a;
-          a.src = S.act_node[rc.i];
-          a.dst = dst;
-          a.label = rc.label;
-          a.pad = 0;
-          a.score = rc.arc_score;
-          lat[static_cast<int64_t>(arc_off) + written + pos] = a;
-        }
-        written += tot;
       }
       grp.sync();
       // New active set, sorted by (ctx, state).
@@ -525,9 +636,16 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       grp.sync();
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long c4 = clock64();
+      ph[0] += c1 - c0;
+      ph[1] += c2 - c1;
+      ph[2] += c4 - c2;
+    }
   }
 
   // ---- lattice_to_best_seq(kMax) = best_path on the stream's lattice ----
+  const long long cb0 = clock64();
   if (have && grp.tid == 0) {
     double* nb = nodebest + nbase;
     const int32_t nn = S.num_nodes;
@@ -578,7 +696,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     lengths[sidx] = len;
     scores[sidx] = total;
   }
+  if (grp.tid == 0 && have) atomicAdd(&counters[11], static_cast<unsigned long long>(clock64() - cb0));
   if (threadIdx.x == 0) {
+    atomicAdd(&counters[8], static_cast<unsigned long long>(ph[0]));
+    atomicAdd(&counters[9], static_cast<unsigned long long>(ph[1]));
+    atomicAdd(&counters[10], static_cast<unsigned long long>(ph[2]));
     mbar_wait(&C.bar[gch & 1u], (gch >> 1) & 1u);
     mbar_wait(&C.bar[(gch + 1) & 1u], ((gch + 1) >> 1) & 1u);
     unsigned long long sf = 0;
@@ -606,7 +728,7 @@ cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s) {
   const int grid = (a.B + G - 1) / G;
   fsa_kernel<<<grid, kDecodeThreads, smem, s>>>(
       m, a.pe, a.frame_splits, a.B, G, static_cast<const ArcRec*>(a.graph_arcs), a.graph_splits,
-      a.fsa_beam, a.max_states, a.max_contexts, static_cast<LatArc*>(a.lattice), a.lattice_cap,
+      a.graph_maxw, a.fsa_beam, a.max_states, a.max_contexts, static_cast<LatArc*>(a.lattice), a.lattice_cap,
       a.lattice_count, reinterpret_cast<int4*>(a.lat_frame_info), a.node_best, a.tokens, a.lengths,
       a.scores, a.counters, a.error_flag);
   return cudaGetLastError();

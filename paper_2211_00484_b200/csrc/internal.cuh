@@ -15,7 +15,7 @@ constexpr int kMaxVocab = 512;      // joiner output row staged whole in smem
 constexpr int kMaxJoiner = 512;     // reference limit (model.hpp:287-288)
 constexpr int kMaxBeam = 8;         // hypotheses per stream (warp lanes)
 constexpr int kFsaMaxStates = 64;   // FSA active tuples per stream
-constexpr int kDecodeThreads = 512; // persistent decode CTA
+constexpr int kDecodeThreads = 512; // persistent decode CTA (16 warps)
 
 void set_error(const std::string& msg);
 
@@ -108,6 +108,7 @@ struct DecodeArgs {
   // fsa
   const void* graph_arcs;   // device int4-packed arcs
   const int32_t* graph_splits;
+  const double* graph_maxw;     // device [states]: max outgoing arc weight (-inf if none)
   int32_t graph_states;
   double fsa_beam;
   int32_t max_states, max_contexts;

@@ -54,6 +54,22 @@ int main() {
       std::printf("fsa mismatch %zu\n", i);
       ++bad;
     }
+  // Whole lattices through the reference-typed fsa_beam_search: same nodes,
+  // arcs and labels; scores to 1e-12 relative; same best sequences.
+  auto glats = gpu::fsa_beam_search(ctx, m, batch, graphs, fp);
+  for (size_t i = 0; i < batch.size(); ++i) {
+    const Fsa& a = glats[i];
+    const Fsa& b = lats[i];
+    bool same = a.num_states == b.num_states && a.arcs.size() == b.arcs.size() && a.finals == b.finals;
+    for (size_t k = 0; same && k < a.arcs.size(); ++k)
+      same = a.arcs[k].src == b.arcs[k].src && a.arcs[k].dst == b.arcs[k].dst &&
+             a.arcs[k].label == b.arcs[k].label &&
+             std::abs(a.arcs[k].score - b.arcs[k].score) <= 1e-12 * std::abs(b.arcs[k].score) + 1e-15;
+    if (!same || lattice_to_best_seq(a, MergeOp::kMax) != lattice_to_best_seq(b, MergeOp::kMax)) {
+      std::printf("lattice mismatch %zu\n", i);
+      ++bad;
+    }
+  }
   try {
     gpu::greedy_search_batch(ctx, m, batch, 2);
     ++bad;

@@ -71,6 +71,7 @@ def run(name, m, B, T, kind, params, graph=None, ref_graph=None, cpu_streams=Non
                decode_ms=st["decode_ms"], rows_per_sf=st["joiner_rows"] / max(1, st["stream_frames"]),
                arcs_per_sf=st["arcs_expanded"] / max(1, st["stream_frames"]),
                lattice_arcs_per_sf=st["lattice_arcs"] / max(1, st["stream_frames"]),
+               phase_cycles=st["phase_cycles"],
                note="fsa timed through host frames (includes H2D)" if kind == "fsa" else "frames resident in HBM")
     if cpu_streams:
         n = min(cpu_streams, len(splits_u) - 1)
