@@ -32,6 +32,9 @@ struct rnntg_model_s {
   // RNNTG_WS=1 selects the warp-specialised beam kernel (measured slower on
   // B200 at batch 1024: profiles/r01/README.md); default single-group kernel.
   bool warp_specialized = false;
+  // RNNTG_BEAM_IMPL: 0 = dual-residency 256-thread kernel (default), 1 = one
+  // 512-thread CTA per SM (beam_kernel / beam_ws_kernel).
+  int beam_impl = 0;
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
   Scratch finfo, nodebest, lattice, flag, feat, hid;
   int64_t lat_cap_hint = 0;
@@ -280,6 +283,7 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
   for (auto& e : h->ev) cudaEventCreate(&e);
   h->num_sms = rnntg::decode_num_sms(device);
   if (const char* ws = std::getenv("RNNTG_WS")) h->warp_specialized = std::atoi(ws) != 0;
+  if (const char* bi = std::getenv("RNNTG_BEAM_IMPL")) h->beam_impl = std::atoi(bi);
   rnntg::DeviceModel& d = h->d;
   d.V = V;
   d.D = D;
@@ -493,6 +497,9 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       a.backptr = h->bp.as<uint32_t>() + static_cast<int64_t>(b0) * rnntg::kMaxBeam;
       a.joiner_bf16 = h->joiner_mode == RNNTG_JOINER_BF16;
       a.warp_specialized = ws;
+      a.beam_impl = h->beam_impl;
+      // a chunk of the host-frame pipeline fills its share of the CTA slots
+      a.cta_slots = static_cast<int32_t>((2LL * h->num_sms * (b1 - b0) + B - 1) / B);
       return rnntg::launch_decode_beam(a, cs);
     });
     if (st) return st;

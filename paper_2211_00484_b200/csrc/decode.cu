@@ -707,7 +707,134 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Dual-residency beam kernel: 256 threads, two CTAs per SM (decode_common.cuh
+// "Dual-residency exact joiner").  Same phases, arithmetic and decisions as
+// beam_kernel; CTA i owns streams [i*q + min(i, rem), +q + (i < rem)) of the
+// launch (q = B / NC, rem = B % NC), so per-SM stream counts differ by at
+// most one.
+// ---------------------------------------------------------------------------
+struct DualSmem {
+  uint64_t full[kStages2];
+  uint32_t empty_cnt[kStages2];
+  int64_t row_pe[kRowCap2];
+  int32_t row_ctx[kRowCap2];
+  double row_lse[kRowCap2];
+  float row_l0[kRowCap2];
+  float row_tl[kRowCap2][kMaxBeam];
+  int32_t row_tk[kRowCap2][kMaxBeam];
+  int32_t nrows;
+};
+
+template <int BCAP>
+__global__ void __launch_bounds__(kDualThreads, 2)
+    beam_dual_kernel(ModelView m, const float* __restrict__ pe,
+                     const int32_t* __restrict__ frame_splits, int32_t B, int32_t NC,
+                     int32_t beam, int32_t merge_log, int32_t length_norm,
+                     int32_t max_total, uint32_t* __restrict__ backptr,
+                     int32_t* __restrict__ tokens, int32_t* __restrict__ lengths,
+                     double* __restrict__ scores,
+                     unsigned long long* __restrict__ counters) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* HL = reinterpret_cast<float*>(smem_raw);
+  const int hl_floats = max(m.J * kHStride2, kRowCap2 * m.Vp);
+  float* W0 = HL + hl_floats;
+  DualSmem& S = *reinterpret_cast<DualSmem*>(W0 + kStages2 * kBK2 * m.Vp);
+  Hyps* H = reinterpret_cast<Hyps*>(&S + 1);
+  constexpr int kCandPerStream = BCAP * BCAP + 2 * BCAP;
+
+  const int q = B / NC, rem = B % NC;
+  const int s0 = blockIdx.x * q + min(static_cast<int>(blockIdx.x), rem);
+  const int ns = q + (static_cast<int>(blockIdx.x) < rem ? 1 : 0);
+  if (ns <= 0) return;
+  BeamCand* C = reinterpret_cast<BeamCand*>(H + ns);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const DualPipe pipe{smem_u32(W0), static_cast<uint32_t>(kBK2 * m.Vp * 4), S.full, S.empty_cnt,
+                      (m.J + kBK2 - 1) / kBK2};
+
+  int32_t tmax = 0;
+  for (int i = 0; i < ns; ++i) tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
+  for (int i = threadIdx.x; i < ns; i += kDualThreads) {
+    Hyps& h = H[i];
+    h.nh = 1;
+    h.score[0] = 0.0;
+    h.ctx[0] = 0;
+    h.len[0] = 0;
+    h.last[0] = -1;
+    h.h1[0] = 0x243f6a8885a308d3ull;
+    h.h2[0] = 0x13198a2e03707344ull;
+    h.p1[0] = h.p2[0] = 0;
+  }
+  if (threadIdx.x == 0) dual_pipe_init(pipe, m);
+  __syncthreads();
+  if (threadIdx.x == 0) dual_pipe_prime(pipe, m);
+  uint32_t g = 0;
+  unsigned long long rows_total = 0, ties = 0;
+  long long ph_h = 0, ph_gemm = 0, ph_epi = 0, ph_step = 0;  // phase cycles (thread 0)
+
+  for (int32_t t = 0; t < tmax; ++t) {
+    if (warp == 0) {  // A. rows: distinct contexts per live stream (lane = stream)
+      const int R0 = beam_rows(H, ns, frame_splits + s0, t, S.row_pe, S.row_ctx);
+      if (lane == 0) S.nrows = R0;
+    }
+    __syncthreads();
+    const int R = S.nrows;
+    rows_total += R;
+    const long long c0 = clock64();
+    build_h_g(m, pe, S.row_pe, S.row_ctx, R, HL, kHStride2, threadIdx.x, kDualThreads);
+    __syncthreads();
+    const long long c1 = clock64();
+    dual_gemm(m, pipe, g, HL, R);
+    const long long c2 = clock64();
+    const RowRes rr{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
+    for (int r = warp; r < R; r += kDualWarps)
+      beam_row_reduce<BCAP>(HL + static_cast<int64_t>(r) * m.Vp, m.V, beam, r, rr);
+    __syncthreads();
+    const long long c3 = clock64();
+    for (int i = warp; i < ns; i += kDualWarps) {
+      const int32_t fs = frame_splits[s0 + i];
+      const int32_t T = frame_splits[s0 + i + 1] - fs;
+      if (t >= T) continue;
+      beam_stream_step<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
+                             backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs, beam,
+                             merge_log, length_norm, max_total, rr, tokens, lengths + s0 + i,
+                             scores + s0 + i, &ties);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long c4 = clock64();
+      ph_h += c1 - c0;
+      ph_gemm += c2 - c1;
+      ph_epi += c3 - c2;
+      ph_step += c4 - c3;
+    }
+  }
+  for (int i = threadIdx.x; i < ns; i += kDualThreads)
+    if (frame_splits[s0 + i + 1] == frame_splits[s0 + i]) {
+      lengths[s0 + i] = 0;
+      scores[s0 + i] = 0.0;
+    }
+  atomicAdd(&counters[4], ties);
+  if (threadIdx.x == 0) {
+    dual_pipe_drain(pipe, g);
+    atomicAdd(&counters[8], static_cast<unsigned long long>(ph_h));
+    atomicAdd(&counters[9], static_cast<unsigned long long>(ph_gemm));
+    atomicAdd(&counters[10], static_cast<unsigned long long>(ph_epi));
+    atomicAdd(&counters[11], static_cast<unsigned long long>(ph_step));
+    unsigned long long sf = 0;
+    for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
+    atomicAdd(&counters[0], sf);
+    atomicAdd(&counters[1], rows_total);
+  }
+}
+
 }  // namespace
+
+int decode_num_sms_current() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return decode_num_sms(dev);
+}
 
 int decode_num_sms(int device) {
   int n = 0;
@@ -929,8 +1056,32 @@ cudaError_t launch_beam_cap(const DecodeArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int BCAP>
+cudaError_t launch_beam_dual(const DecodeArgs& a, cudaStream_t s) {
+  const ModelView m = view_of(*a.m);
+  const int gmax = std::max(1, kRowCap2 / std::max(1, a.beam_size));
+  const int slots = a.cta_slots > 0 ? a.cta_slots : 2 * decode_num_sms_current();
+  const int NC = std::max((a.B + gmax - 1) / gmax, std::min(a.B, slots));
+  const int ns_max = (a.B + NC - 1) / NC;
+  const size_t smem = smem_dual(m) + sizeof(DualSmem) + sizeof(Hyps) * ns_max +
+                      sizeof(BeamCand) * ns_max * (BCAP * BCAP + 2 * BCAP);
+  cudaError_t e = cudaFuncSetAttribute(beam_dual_kernel<BCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  beam_dual_kernel<BCAP><<<NC, kDualThreads, smem, s>>>(
+      m, a.pe, a.frame_splits, a.B, NC, a.beam_size, a.merge_op, a.length_norm, a.max_total,
+      a.backptr, a.tokens, a.lengths, a.scores, a.counters);
+  return cudaGetLastError();
+}
+
 template <bool TC>
 cudaError_t launch_beam_mode(const DecodeArgs& a, cudaStream_t s) {
+  if (!TC && a.beam_impl == 0) {  // exact joiner, dual-residency kernel (default)
+    if (a.beam_size <= 1) return launch_beam_dual<1>(a, s);
+    if (a.beam_size <= 2) return launch_beam_dual<2>(a, s);
+    if (a.beam_size <= 4) return launch_beam_dual<4>(a, s);
+    return launch_beam_dual<8>(a, s);
+  }
   if (!TC && a.warp_specialized) {  // exact joiner, >= 2 streams per CTA
     if (a.beam_size <= 1) return launch_beam_ws<1>(a, s);
     if (a.beam_size <= 2) return launch_beam_ws<2>(a, s);

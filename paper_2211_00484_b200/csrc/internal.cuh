@@ -104,6 +104,8 @@ struct DecodeArgs {
   int32_t beam_size, merge_op, length_norm, max_total;
   int32_t joiner_bf16;      // 1: tcgen05 bf16 joiner variant (not token-exact)
   int32_t warp_specialized; // 1: beam_ws_kernel (GEMM / POST warp groups)
+  int32_t beam_impl;        // 0: dual-residency kernel (default); 1: single 512-thread CTA per SM
+  int32_t cta_slots;        // dual kernel: CTA slots this launch may fill (0: 2 x SMs)
   uint32_t* backptr;        // device [(sum T + B) * kMaxBeam]
   // fsa
   const void* graph_arcs;   // device int4-packed arcs
@@ -124,6 +126,7 @@ cudaError_t launch_decode_greedy(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s);
 int decode_num_sms(int device);
+int decode_num_sms_current();
 
 cudaError_t launch_tanhf_hash(int32_t first_chunk, int32_t num_chunks,
                               unsigned long long* d_hashes, cudaStream_t s);

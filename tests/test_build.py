@@ -52,7 +52,7 @@ def _functions(sass):
 def test_no_ffma_outside_division(lib):
     sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
     funcs = _functions(sass)
-    exact = [f for f in funcs if re.search(r"gemm_exact|beam_kernel|greedy_kernel|fsa_kernel|joiner_rows", f)]
+    exact = [f for f in funcs if re.search(r"gemm_exact|beam_(dual_|ws_)?kernel|greedy_kernel|fsa_kernel|joiner_rows", f)]
     assert len(exact) >= 6
     for f in exact:
         ins = funcs[f]
@@ -60,8 +60,13 @@ def test_no_ffma_outside_division(lib):
         last_exit = max(i for i, s in enumerate(ins) if s.endswith("EXIT") or " EXIT" in s or s == "EXIT")
         for i, s in enumerate(ins[: last_exit + 1]):
             if re.search(r"\bFFMA2?\b", s):
-                # fp32 division (FCHK-guarded Newton steps) and the fp64
+                # fp32 division (FCHK-guarded Newton steps, or the unchecked
+                # reciprocal + Newton + residual sequence of
+                # exact_math.h:fdiv_nochk after MUFU.RCP) and the fp64
                 # division's range check (FFMA ..., RZ, ... after DFMA steps)
-                # are correctly rounded library sequences.
+                # are correctly rounded sequences, not dot-product math.
                 window = ins[max(0, i - 10) : i]
-                assert any("FCHK" in w or "DFMA" in w for w in window), f"{f}: FFMA outside division: {s}"
+                rcp_window = ins[max(0, i - 32) : i]
+                assert any("FCHK" in w or "DFMA" in w for w in window) or any(
+                    "MUFU.RCP" in w for w in rcp_window
+                ), f"{f}: FFMA outside division: {s}"

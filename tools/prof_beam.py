@@ -1,0 +1,32 @@
+"""Beam-search timing on the bench workload (reference-encoder frames in HBM),
+for A/B comparisons of the decode kernels (RNNTG_BEAM_IMPL / RNNTG_WS) and
+for ncu captures.  Usage: python tools/prof_beam.py [B] [T] [reps]"""
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+from paper_2211_00484_b200.api import BeamParams, Decoder, ModelWeights  # noqa: E402
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+T = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+w = bench.synthetic_weights()
+dec = Decoder(ModelWeights.from_dict(w))
+dec.set_encoder(w)
+d_enc, splits = bench.synthetic_frames(dec, B, T, seed=100, device="cuda:0")
+tok = torch.zeros(B * T, dtype=torch.int32, device="cuda")
+sc = torch.zeros(B, dtype=torch.float64, device="cuda")
+out = []
+for r in range(reps):
+    osp, otok, osc = dec.beam_search_batch(d_enc, splits, BeamParams(4), tok, sc)
+    st = dec.stats()
+    out.append(st["decode_ms"])
+ph = st["phase_cycles"]
+tot = sum(ph) or 1
+print(json.dumps(dict(B=B, T=T, decode_ms=out, gpu_ms=st["gpu_ms"], fps_decode=B * T / (min(out) * 1e-3),
+                      rows_per_sf=st["joiner_rows"] / st["stream_frames"], ties=st["tie_breaks"],
+                      phase_share=[round(x / tot, 3) for x in ph],
+                      tokens=int(osp[-1]), checksum=float(osc.sum()))))
