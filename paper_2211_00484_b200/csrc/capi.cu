@@ -32,9 +32,10 @@ struct rnntg_model_s {
   // RNNTG_WS=1 selects the warp-specialised beam kernel (measured slower on
   // B200 at batch 1024: profiles/r01/README.md); default single-group kernel.
   bool warp_specialized = false;
-  // RNNTG_BEAM_IMPL: 0 = dual-residency 256-thread kernel (default), 1 = one
-  // 512-thread CTA per SM (beam_kernel / beam_ws_kernel).
-  int beam_impl = 0;
+  // RNNTG_BEAM_IMPL: 1 = one 512-thread CTA per SM (beam_kernel /
+  // beam_ws_kernel; default), 0 = dual-residency 256-thread kernel (two CTAs
+  // per SM; measured slower, profiles/r01).
+  int beam_impl = 1;
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
   Scratch finfo, nodebest, lattice, flag, feat, hid;
   int64_t lat_cap_hint = 0;

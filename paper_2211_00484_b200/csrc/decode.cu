@@ -1076,7 +1076,7 @@ cudaError_t launch_beam_dual(const DecodeArgs& a, cudaStream_t s) {
 
 template <bool TC>
 cudaError_t launch_beam_mode(const DecodeArgs& a, cudaStream_t s) {
-  if (!TC && a.beam_impl == 0) {  // exact joiner, dual-residency kernel (default)
+  if (!TC && a.beam_impl == 0) {  // exact joiner, dual-residency kernel (opt-in)
     if (a.beam_size <= 1) return launch_beam_dual<1>(a, s);
     if (a.beam_size <= 2) return launch_beam_dual<2>(a, s);
     if (a.beam_size <= 4) return launch_beam_dual<4>(a, s);

@@ -196,8 +196,101 @@ __device__ __forceinline__ void gemm_pass(const ModelView& m, const WPipe& p,
   __syncthreads();
 }
 
+// One out_w chunk of a work item: 4 rows x 32*TN columns (lane columns
+// col[0..TN)), accumulated into acc[.][0..TN).
+template <int TN>
+__device__ __forceinline__ void gemm_chunk(const ModelView& m, uint32_t ws, const float* hp, int kk_end,
+                                           const int* col, float (&acc)[4][8]) {
+#pragma unroll 4
+  for (int kk = 0; kk < kk_end; ++kk) {
+    const float4 h4 = *reinterpret_cast<const float4*>(hp + kk * kHStride);
+    const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
+    float wv[TN];
+    const uint32_t wr = ws + static_cast<uint32_t>(kk * m.Vp) * 4u;
+    const float4 wa = lds128(wr + col[0] * 4u);
+    wv[0] = wa.x; wv[1] = wa.y; wv[2] = wa.z; wv[3] = wa.w;
+    if constexpr (TN == 8) {
+      const float4 wb = lds128(wr + col[4] * 4u);
+      wv[4] = wb.x; wv[5] = wb.y; wv[6] = wb.z; wv[7] = wb.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+        acc[i][j] = fadd(acc[i][j], fmul(wv[j], hv[i]));
+  }
+}
+
+// C for Vp = 512, balanced over the four SM sub-partitions (a warp's SMSP is
+// warp % 4, and the FMUL/FADD stream is issue-bound per SMSP).  With rgs =
+// ceil(R/4) row groups: every full pair of row groups gives 4 "heavy" items
+// (4 rows x 256 columns, TN = 8) on 4 consecutive warps; an odd last row
+// group is cut into 4 "light" items (4 rows x 128 columns, TN = 4), again on
+// 4 consecutive warps — so every SMSP gets the same work for any R.  (A
+// plain 2-items-per-row-group split leaves SMSPs 3:3:2:2 loaded at R = 20:
+// tools/probes/gemm_tiling.cu measured 1.23e13 vs 1.47e13 MAC/s.)
+__device__ __forceinline__ void gemm_pass_bal(const ModelView& m, const WPipe& p, uint32_t& g,
+                                              float* HL, int R) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rgs = (R + 3) >> 2;
+  const int heavy = 2 * (rgs & ~1);
+  const int light = (rgs & 1) ? 4 : 0;
+  int tn = 0, rg = 0, cbase = 0;
+  if (warp < heavy) {
+    tn = 8;
+    rg = warp >> 1;
+    cbase = (warp & 1) * 256;
+  } else if (warp < heavy + light) {
+    tn = 4;
+    rg = rgs - 1;
+    cbase = (warp - heavy) * 128;
+  }
+  int col[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) col[j] = cbase + (j < 4 ? lane * 4 + j : 128 + lane * 4 + (j - 4));
+  float acc[4][8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float b = (tn == 8 || (tn == 4 && j < 4)) ? m.out_b[col[j]] : 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][j] = b;
+  }
+  for (int32_t c = 0; c < p.nc; ++c, ++g) {
+    const uint32_t st = g & 1u;
+    // Idle warps go straight to the barrier (bar.sync does not issue) rather
+    // than spinning on the mbarrier.  Warp 0 always waits: it refills the
+    // stage.
+    if (tn != 0 || warp == 0) mbar_wait(p.bar + st, (g >> 1) & 1u);
+    const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(kBK * m.Vp * 4);
+    const int kk_end = min(kBK, m.J - c * kBK);
+    const float* hp = HL + static_cast<int64_t>(c * kBK) * kHStride + rg * 4;
+    if (tn == 8) gemm_chunk<8>(m, ws, hp, kk_end, col, acc);
+    else if (tn == 4) gemm_chunk<4>(m, ws, hp, kk_end, col, acc);
+    __syncthreads();  // every warp is done with this stage
+    if (threadIdx.x == 0) wpipe_issue(p, m, g + 2);
+  }
+  // The last __syncthreads above also retired every read of the h tile.
+  if (tn != 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = rg * 4 + i;
+      if (r < R) {
+        float* lr = HL + static_cast<int64_t>(r) * m.Vp;
+        *reinterpret_cast<float4*>(lr + col[0]) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        if (tn == 8)
+          *reinterpret_cast<float4*>(lr + col[4]) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+      }
+    }
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void joiner_gemm(const ModelView& m, const WPipe& p,
                                             uint32_t& g, float* HL, int R) {
+  if (m.Vp == 512 && R > 4) {
+    gemm_pass_bal(m, p, g, HL, R);
+    return;
+  }
   const int rg = (R + 3) >> 2;
   const int nb256 = m.Vp >> 8, nb128 = m.Vp >> 7, nb64 = m.Vp >> 6;
   constexpr int W = kDecodeThreads / 32;

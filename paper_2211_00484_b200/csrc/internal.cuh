@@ -104,7 +104,7 @@ struct DecodeArgs {
   int32_t beam_size, merge_op, length_norm, max_total;
   int32_t joiner_bf16;      // 1: tcgen05 bf16 joiner variant (not token-exact)
   int32_t warp_specialized; // 1: beam_ws_kernel (GEMM / POST warp groups)
-  int32_t beam_impl;        // 0: dual-residency kernel (default); 1: single 512-thread CTA per SM
+  int32_t beam_impl;        // 1: single 512-thread CTA per SM (default); 0: dual-residency kernel
   int32_t cta_slots;        // dual kernel: CTA slots this launch may fill (0: 2 x SMs)
   uint32_t* backptr;        // device [(sum T + B) * kMaxBeam]
   // fsa
