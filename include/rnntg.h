@@ -116,6 +116,8 @@ typedef struct {
   float decode_ms;        /* device time of the persistent decode kernel */
   int64_t phase_cycles[4];/* beam kernel, summed over CTAs: h build, joiner
                              GEMM, row reduction, search step (SM cycles) */
+  int64_t joiner_rows_computed; /* beam kernel: rows the GEMM tiles computed
+                                   (row groups of 4, padding included) */
 } rnntg_stats;
 
 const char* rnntg_last_error(void);

@@ -88,6 +88,7 @@ class _Stats(C.Structure):
         ("gpu_ms", C.c_float),
         ("decode_ms", C.c_float),
         ("phase_cycles", C.c_int64 * 4),
+        ("joiner_rows_computed", C.c_int64),
     ]
 
 

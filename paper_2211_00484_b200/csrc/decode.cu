@@ -373,6 +373,83 @@ __device__ __forceinline__ void beam_row_reduce(const float* L, int V, int beam,
   }
 }
 
+// D for NR rows per warp (rows r0 + 16 j), their dependency chains
+// interleaved.  Per row: each lane keeps a sorted top-BCAP of its columns
+// k >= 1 (k = lane + 32 i) as 64-bit keys (ordered logit << 32 | ~k: key
+// order is (logit desc, token asc)) by branch-free compare-exchange; `beam`
+// pops take the warp maximum with two redux.sync each; the row max M is the
+// larger of the first pop and the blank logit; then lse = M + log(sum of
+// exp(double(l) - M)) in row_lse's order.  Same results as beam_row_reduce.
+__device__ __forceinline__ uint64_t tok_key(float v, int k) {
+  return (static_cast<uint64_t>(ord_key(v + 0.0f)) << 32) | static_cast<uint32_t>(~k);  // -0 -> +0
+}
+
+template <int BCAP, int NR>
+__device__ __forceinline__ void beam_row_reduce_n(const float* HL, int Vp, int V, int beam, int r0,
+                                                  int R, RowRes rr) {
+  const int lane = threadIdx.x & 31;
+  uint64_t t[NR][BCAP];
+  const float* L[NR];
+  bool live[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    live[j] = r0 + 16 * j < R;
+    L[j] = HL + static_cast<int64_t>(live[j] ? r0 + 16 * j : r0) * Vp;
+#pragma unroll
+    for (int q = 0; q < BCAP; ++q) t[j][q] = 0;
+  }
+  for (int k = lane; k < V; k += 32) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      uint64_t c = k >= 1 ? tok_key(L[j][k], k) : 0;
+#pragma unroll
+      for (int q = 0; q < BCAP; ++q) {
+        const uint64_t hi = max(t[j][q], c);
+        c = min(t[j][q], c);
+        t[j][q] = hi;
+      }
+    }
+  }
+  float M[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) M[j] = L[j][0];
+  for (int q = 0; q < beam; ++q) {
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const uint32_t H = __reduce_max_sync(0xffffffffu, static_cast<uint32_t>(t[j][0] >> 32));
+      const uint32_t Lo = __reduce_max_sync(
+          0xffffffffu, static_cast<uint32_t>(t[j][0] >> 32) == H ? static_cast<uint32_t>(t[j][0]) : 0u);
+      const float v = H != 0 ? ord_val(H) : -FLT_MAX;
+      const int k = H != 0 ? static_cast<int>(~Lo) : 0x7fffffff;
+      if (q == 0 && H != 0) M[j] = fmaxf(M[j], v);
+      if (lane == 0 && live[j]) {
+        rr.tl[r0 + 16 * j][q] = v;
+        rr.tk[r0 + 16 * j][q] = k;
+      }
+      if (H != 0 && t[j][0] == ((static_cast<uint64_t>(H) << 32) | Lo)) {
+#pragma unroll
+        for (int z = 0; z < BCAP - 1; ++z) t[j][z] = t[j][z + 1];
+        t[j][BCAP - 1] = 0;
+      }
+    }
+  }
+  double s[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) s[j] = 0.0;
+#pragma unroll 4
+  for (int k = lane; k < V; k += 32)
+#pragma unroll
+    for (int j = 0; j < NR; ++j) s[j] += exp_lse(static_cast<double>(L[j][k]) - static_cast<double>(M[j]));
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    s[j] = warp_sum_d(s[j]);
+    if (lane == 0 && live[j]) {
+      rr.lse[r0 + 16 * j] = static_cast<double>(M[j]) + log(s[j]);
+      rr.l0[r0 + 16 * j] = L[j][0];
+    }
+  }
+}
+
 // E. one stream's frame (one warp).  Reference order (search.hpp:223-259 at
 // S = 1): the extensions are cut to the beam first (prune_to_beam of
 // next_level), then merged with the blank continuations by full-sequence
@@ -616,7 +693,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     wpipe_issue(pipe, m, 1);
   }
   uint32_t g = 0;
-  unsigned long long rows_total = 0, ties = 0;
+  unsigned long long rows_total = 0, ties = 0, rows_padded = 0;
   long long ph_h = 0, ph_gemm = 0, ph_epi = 0, ph_step = 0;  // phase cycles (thread 0)
 
   for (int32_t t = 0; t < tmax; ++t) {
@@ -628,6 +705,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     __syncthreads();
     const int R = S.nrows;
     rows_total += R;
+    rows_padded += (R + 3) & ~3;
     long long c0 = clock64();
     if constexpr (TC)
       build_h_tc(m, pe, S.row_pe, S.row_ctx, R, R <= 16 ? 16 : 32, hb);
@@ -644,8 +722,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     // token asc).  Each lane keeps a sorted local top-kMaxBeam, then `beam`
     // warp-wide pops.
     const RowRes rr{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
-    for (int r = warp; r < R; r += kWarps)
-      beam_row_reduce<BCAP>(HL + static_cast<int64_t>(r) * m.Vp, m.V, beam, r, rr);
+    if (R <= kWarps) {
+      if (warp < R) beam_row_reduce_n<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr);
+    } else if (warp < R - kWarps || warp < kWarps) {
+      beam_row_reduce_n<BCAP, 2>(HL, m.Vp, m.V, beam, warp, R, rr);
+    }
     __syncthreads();
 
     long long c3 = clock64();
@@ -683,6 +764,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     atomicAdd(&counters[9], static_cast<unsigned long long>(ph_gemm));
     atomicAdd(&counters[10], static_cast<unsigned long long>(ph_epi));
     atomicAdd(&counters[11], static_cast<unsigned long long>(ph_step));
+    atomicAdd(&counters[5], rows_padded);
   }
   if constexpr (TC) {
     // Chunks g .. g+kTcStages-2 were prefetched for a frame that never came.
@@ -769,7 +851,7 @@ __global__ void __launch_bounds__(kDualThreads, 2)
   __syncthreads();
   if (threadIdx.x == 0) dual_pipe_prime(pipe, m);
   uint32_t g = 0;
-  unsigned long long rows_total = 0, ties = 0;
+  unsigned long long rows_total = 0, ties = 0, rows_padded = 0;
   long long ph_h = 0, ph_gemm = 0, ph_epi = 0, ph_step = 0;  // phase cycles (thread 0)
 
   for (int32_t t = 0; t < tmax; ++t) {

@@ -498,6 +498,16 @@ __device__ __forceinline__ void build_h(const ModelView& m, const float* pe,
   __syncthreads();
 }
 
+// Order-preserving uint32 key of a float (larger float -> larger key; every
+// float but -NaN maps above 0, so 0 can mean "none") and its inverse.
+__device__ __forceinline__ uint32_t ord_key(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord_val(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
 __device__ __forceinline__ float warp_max_f(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -507,6 +517,39 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// exp(x) for the log-softmax sums, x = double(l) - double(max) <= 0: n =
+// rint(x / ln2), r = x - n ln2 (two-part ln2, |r| <= ln2/2), e^r by its
+// degree-13 Taylor polynomial in Horner form (truncation < 5e-18 relative),
+// times 2^n by an exponent add.  ~1-2 ulp, branch-free, ~22 instructions
+// against ~90 for the libdevice exp (whose range checks also split it into
+// basic blocks, so consecutive evaluations cannot interleave).  x < -700
+// gives 0 (e^-700 is far below an ulp of any sum it joins: the sum holds
+// e^0 = 1).
+__device__ __forceinline__ double exp_lse(double x) {
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
+  const double t = __fma_rn(x, 1.4426950408889634, kMagic);
+  const double nd = t - kMagic;
+  const int n = __double2loint(t);
+  double r = __fma_rn(-nd, 6.93147180369123816490e-01, x);  // ln2 hi (n*hi exact for |n| < 2^20)
+  r = __fma_rn(-nd, 1.90821492927058770002e-10, r);          // ln2 lo
+  double p = 1.6059043836821614599e-10;                       // 1/13!
+  p = __fma_rn(p, r, 2.0876756987868098979e-09);              // 1/12!
+  p = __fma_rn(p, r, 2.5052108385441718775e-08);              // 1/11!
+  p = __fma_rn(p, r, 2.7557319223985890653e-07);              // 1/10!
+  p = __fma_rn(p, r, 2.7557319223985890653e-06);              // 1/9!
+  p = __fma_rn(p, r, 2.4801587301587301566e-05);              // 1/8!
+  p = __fma_rn(p, r, 1.9841269841269841253e-04);              // 1/7!
+  p = __fma_rn(p, r, 1.3888888888888889419e-03);              // 1/6!
+  p = __fma_rn(p, r, 8.3333333333333332177e-03);              // 1/5!
+  p = __fma_rn(p, r, 4.1666666666666664354e-02);              // 1/4!
+  p = __fma_rn(p, r, 1.6666666666666665741e-01);              // 1/3!
+  p = __fma_rn(p, r, 0.5);
+  p = __fma_rn(p, r, 1.0);
+  p = __fma_rn(p, r, 1.0);
+  const double y = __hiloint2double(__double2hiint(p) + (n << 20), __double2loint(p));
+  return x < -700.0 ? 0.0 : y;
 }
 
 // Log-softmax normaliser of one logits row (model.hpp:115-125): float max,
@@ -519,7 +562,8 @@ __device__ __forceinline__ double row_lse(const float* L, int V) {
   for (int k = lane; k < V; k += 32) mx = fmaxf(mx, L[k]);
   mx = warp_max_f(mx);
   double s = 0.0;
-  for (int k = lane; k < V; k += 32) s += exp(static_cast<double>(L[k]) - static_cast<double>(mx));
+#pragma unroll 4
+  for (int k = lane; k < V; k += 32) s += exp_lse(static_cast<double>(L[k]) - static_cast<double>(mx));
   s = warp_sum_d(s);
   return static_cast<double>(mx) + log(s);
 }
