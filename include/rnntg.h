@@ -118,6 +118,8 @@ typedef struct {
                              GEMM, row reduction, search step (SM cycles) */
   int64_t joiner_rows_computed; /* beam kernel: rows the GEMM tiles computed
                                    (row groups of 4, padding included) */
+  int64_t gather_cycles;  /* beam kernel: cycles of the h build spent gathering
+                             pe / pd rows (thread 0, summed over CTAs) */
 } rnntg_stats;
 
 const char* rnntg_last_error(void);

@@ -89,6 +89,7 @@ class _Stats(C.Structure):
         ("decode_ms", C.c_float),
         ("phase_cycles", C.c_int64 * 4),
         ("joiner_rows_computed", C.c_int64),
+        ("gather_cycles", C.c_int64),
     ]
 
 

@@ -694,6 +694,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   }
   uint32_t g = 0;
   unsigned long long rows_total = 0, ties = 0, rows_padded = 0;
+  long long tsplit = 0, ph_gather = 0;
   long long ph_h = 0, ph_gemm = 0, ph_epi = 0, ph_step = 0;  // phase cycles (thread 0)
 
   for (int32_t t = 0; t < tmax; ++t) {
@@ -710,8 +711,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     if constexpr (TC)
       build_h_tc(m, pe, S.row_pe, S.row_ctx, R, R <= 16 ? 16 : 32, hb);
     else
-      build_h(m, pe, S.row_pe, S.row_ctx, R, HL);
+      build_h(m, pe, S.row_pe, S.row_ctx, R, HL, &tsplit);
     long long c1 = clock64();
+    if (threadIdx.x == 0) ph_gather += tsplit - c0;
     if constexpr (TC)
       tc_gemm(m, tp, g, static_cast<uint32_t>(t), HL, R);
     else
@@ -765,6 +767,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     atomicAdd(&counters[10], static_cast<unsigned long long>(ph_epi));
     atomicAdd(&counters[11], static_cast<unsigned long long>(ph_step));
     atomicAdd(&counters[5], rows_padded);
+    atomicAdd(&counters[6], static_cast<unsigned long long>(ph_gather));
   }
   if constexpr (TC) {
     // Chunks g .. g+kTcStages-2 were prefetched for a frame that never came.
@@ -852,6 +855,7 @@ __global__ void __launch_bounds__(kDualThreads, 2)
   if (threadIdx.x == 0) dual_pipe_prime(pipe, m);
   uint32_t g = 0;
   unsigned long long rows_total = 0, ties = 0, rows_padded = 0;
+  long long tsplit = 0, ph_gather = 0;
   long long ph_h = 0, ph_gemm = 0, ph_epi = 0, ph_step = 0;  // phase cycles (thread 0)
 
   for (int32_t t = 0; t < tmax; ++t) {

@@ -414,7 +414,7 @@ __device__ __forceinline__ void joiner_gemm_g(const ModelView& m, const WPipe& p
 // h tile for a thread group of nt threads (tid in [0, nt)), k-major stride.
 __device__ __forceinline__ void build_h_g(const ModelView& m, const float* pe, const int64_t* row_pe,
                                           const int32_t* row_ctx, int R, float* HL, int hstride,
-                                          int tid, int nt) {
+                                          int tid, int nt, long long* tsplit = nullptr) {
   const int J = m.J;
   const int total = R * J;
   // Pass 1: gather (pe + pd) + j_b with many independent global loads in
@@ -447,6 +447,7 @@ __device__ __forceinline__ void build_h_g(const ModelView& m, const float* pe, c
         o[3 * hstride] = fadd(fadd(a[u].w, b[u].w), jb[3]);
       }
     }
+    if (tsplit && tid == 0) tsplit[0] = clock64();
     // Pass 2 over the same units (each thread reads back what it wrote).
     // Four independent branch-free tanhf chains per unit; the rare special
     // inputs are fixed up afterwards so the main paths interleave.
@@ -493,8 +494,8 @@ __device__ __forceinline__ void build_h_g(const ModelView& m, const float* pe, c
 __device__ __forceinline__ void build_h(const ModelView& m, const float* pe,
                                         const int64_t* row_pe,
                                         const int32_t* row_ctx, int R,
-                                        float* HL) {
-  build_h_g(m, pe, row_pe, row_ctx, R, HL, kHStride, threadIdx.x, kDecodeThreads);
+                                        float* HL, long long* tsplit = nullptr) {
+  build_h_g(m, pe, row_pe, row_ctx, R, HL, kHStride, threadIdx.x, kDecodeThreads, tsplit);
   __syncthreads();
 }
 
