@@ -421,7 +421,9 @@ __device__ __forceinline__ void build_h_g(const ModelView& m, const float* pe, c
   // flight per thread; pass 2: tanhf in place.  Splitting the passes keeps
   // the glibc-tanhf dependency chains from serialising the HBM/L2 latency.
   if ((J & 3) == 0) {
-    // 16-byte loads: unit = 4 consecutive i of one row.
+    // 16-byte loads: unit = 4 consecutive i of one row; units are numbered
+    // row-fastest, so a warp's k-major h writes (i * hstride + r) hit
+    // consecutive banks (column-fastest units were a 16-way conflict).
     const int J4 = J >> 2, units = R * J4;
     for (int base = tid; base < units; base += 4 * nt) {
       float4 a[4], b[4];
@@ -430,8 +432,8 @@ __device__ __forceinline__ void build_h_g(const ModelView& m, const float* pe, c
       for (int u = 0; u < 4; ++u) {
         const int x = base + u * nt;
         const bool ok = x < units;
-        rr[u] = ok ? x / J4 : 0;
-        ii[u] = ok ? (x - rr[u] * J4) * 4 : 0;
+        ii[u] = ok ? (x / R) * 4 : 0;  // row-fastest units: a warp's lanes take
+        rr[u] = ok ? x - (ii[u] >> 2) * R : 0;  // consecutive rows -> conflict-free h writes
         a[u] = ok ? *reinterpret_cast<const float4*>(pe + row_pe[rr[u]] * J + ii[u]) : make_float4(0, 0, 0, 0);
         b[u] = ok ? *reinterpret_cast<const float4*>(m.pd + static_cast<int64_t>(row_ctx[rr[u]]) * J + ii[u])
                   : make_float4(0, 0, 0, 0);
@@ -452,7 +454,7 @@ __device__ __forceinline__ void build_h_g(const ModelView& m, const float* pe, c
     // Four independent branch-free tanhf chains per unit; the rare special
     // inputs are fixed up afterwards so the main paths interleave.
     for (int x = tid; x < units; x += nt) {
-      const int r = x / J4, i = (x - r * J4) * 4;
+      const int i = (x / R) * 4, r = x - (i >> 2) * R;
       float* o = HL + i * hstride + r;
       float v[4], z[4];
 #pragma unroll
