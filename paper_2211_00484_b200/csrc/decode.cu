@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     __syncthreads();
     const int R = S.nrows;
     rows_total += R;
-    rows_padded += (R + 3) & ~3;
+    rows_padded += (m.Vp == 512 && R > 4 && R < 28) ? R : ((R + 3) & ~3);
     long long c0 = clock64();
     if constexpr (TC)
       build_h_tc(m, pe, S.row_pe, S.row_ctx, R, R <= 16 ? 16 : 32, hb);

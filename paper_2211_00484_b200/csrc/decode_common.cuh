@@ -196,9 +196,9 @@ __device__ __forceinline__ void gemm_pass(const ModelView& m, const WPipe& p,
   __syncthreads();
 }
 
-// One out_w chunk of a work item: 4 rows x 32*TN columns (lane columns
-// col[0..TN)), accumulated into acc[.][0..TN).
-template <int TN>
+// One out_w chunk of a work item: NR <= 4 rows x 32*TN columns (lane
+// columns col[0..TN)), accumulated into acc[0..NR)[0..TN).
+template <int TN, int NR>
 __device__ __forceinline__ void gemm_chunk(const ModelView& m, uint32_t ws, const float* hp, int kk_end,
                                            const int* col, float (&acc)[4][8]) {
 #pragma unroll 4
@@ -214,7 +214,7 @@ __device__ __forceinline__ void gemm_chunk(const ModelView& m, uint32_t ws, cons
       wv[4] = wb.x; wv[5] = wb.y; wv[6] = wb.z; wv[7] = wb.w;
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < NR; ++i)
 #pragma unroll
       for (int j = 0; j < TN; ++j)
         acc[i][j] = fadd(acc[i][j], fmul(wv[j], hv[i]));
@@ -222,28 +222,39 @@ __device__ __forceinline__ void gemm_chunk(const ModelView& m, uint32_t ws, cons
 }
 
 // C for Vp = 512, balanced over the four SM sub-partitions (a warp's SMSP is
-// warp % 4, and the FMUL/FADD stream is issue-bound per SMSP).  With rgs =
-// ceil(R/4) row groups: every full pair of row groups gives 4 "heavy" items
-// (4 rows x 256 columns, TN = 8) on 4 consecutive warps; an odd last row
-// group is cut into 4 "light" items (4 rows x 128 columns, TN = 4), again on
-// 4 consecutive warps — so every SMSP gets the same work for any R.  (A
-// plain 2-items-per-row-group split leaves SMSPs 3:3:2:2 loaded at R = 20:
-// tools/probes/gemm_tiling.cu measured 1.23e13 vs 1.47e13 MAC/s.)
+// warp % 4, and the FMUL/FADD stream is issue-bound per SMSP).  R = 4 full +
+// rem rows.  Every pair of full row groups gives 4 "heavy" items (4 rows x
+// 256 columns, TN = 8) on 4 consecutive warps; an odd full group gives 4
+// "light" items (4 rows x 128 columns); the rem-row partial group gives 4
+// light items of rem rows — each on 4 consecutive warps, so every SMSP gets
+// the same work for any R and no padding row is computed (up to R = 27;
+// beyond, the partial group is padded to 4 rows).  A plain 2-items-per-row-
+// group split leaves SMSPs 3:3:2:2 loaded at R = 20 (tools/probes/
+// gemm_tiling.cu: 1.23e13 vs 1.47e13 MAC/s).
 __device__ __forceinline__ void gemm_pass_bal(const ModelView& m, const WPipe& p, uint32_t& g,
                                               float* HL, int R) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rgs = (R + 3) >> 2;
-  const int heavy = 2 * (rgs & ~1);
-  const int light = (rgs & 1) ? 4 : 0;
-  int tn = 0, rg = 0, cbase = 0;
+  int full = R >> 2, rem = R & 3;
+  if (rem != 0 && 2 * (full & ~1) + 4 * (full & 1) + 4 > kWarps) {  // pad the partial group
+    ++full;
+    rem = 0;
+  }
+  const int heavy = 2 * (full & ~1);
+  const int lfull = (full & 1) ? 4 : 0;
+  int tn = 0, nr = 4, rg = 0, cbase = 0;
   if (warp < heavy) {
     tn = 8;
     rg = warp >> 1;
     cbase = (warp & 1) * 256;
-  } else if (warp < heavy + light) {
+  } else if (warp < heavy + lfull) {
     tn = 4;
-    rg = rgs - 1;
+    rg = full - 1;
     cbase = (warp - heavy) * 128;
+  } else if (rem != 0 && warp < heavy + lfull + 4) {
+    tn = 4;
+    nr = rem;
+    rg = full;
+    cbase = (warp - heavy - lfull) * 128;
   }
   int col[8];
 #pragma unroll
@@ -264,8 +275,11 @@ __device__ __forceinline__ void gemm_pass_bal(const ModelView& m, const WPipe& p
     const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(kBK * m.Vp * 4);
     const int kk_end = min(kBK, m.J - c * kBK);
     const float* hp = HL + static_cast<int64_t>(c * kBK) * kHStride + rg * 4;
-    if (tn == 8) gemm_chunk<8>(m, ws, hp, kk_end, col, acc);
-    else if (tn == 4) gemm_chunk<4>(m, ws, hp, kk_end, col, acc);
+    if (tn == 8) gemm_chunk<8, 4>(m, ws, hp, kk_end, col, acc);
+    else if (tn == 4 && nr == 4) gemm_chunk<4, 4>(m, ws, hp, kk_end, col, acc);
+    else if (tn == 4 && nr == 3) gemm_chunk<4, 3>(m, ws, hp, kk_end, col, acc);
+    else if (tn == 4 && nr == 2) gemm_chunk<4, 2>(m, ws, hp, kk_end, col, acc);
+    else if (tn == 4) gemm_chunk<4, 1>(m, ws, hp, kk_end, col, acc);
     __syncthreads();  // every warp is done with this stage
     if (threadIdx.x == 0) wpipe_issue(p, m, g + 2);
   }
