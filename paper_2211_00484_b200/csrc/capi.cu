@@ -1,5 +1,6 @@
 // C ABI of librnntg.so (include/rnntg.h): argument validation mirroring the
 // reference's checks, device model construction, and the decode drivers.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -36,6 +37,13 @@ struct rnntg_model_s {
   // beam_ws_kernel; default), 0 = dual-residency 256-thread kernel (two CTAs
   // per SM; measured slower, profiles/r01).
   int beam_impl = 1;
+  // Fused encoder projection in the beam kernel (no separate K1 launch; host
+  // frames stream in per time slice).  RNNTG_FUSED_PE: 1 = host frames of
+  // uniform length (default; the copy engine streams while the SMs decode),
+  // 2 = also device frames (measured slower there than K1 + decode:
+  // profiles/r01), 0 = never.
+  int fused_pe = 1;
+  Scratch ready;
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
   Scratch finfo, nodebest, lattice, flag, feat, hid;
   int64_t lat_cap_hint = 0;
@@ -108,6 +116,84 @@ rnntg_status prepare(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem)
   RNNTG_CUDA_TRY(h->score.ensure(sizeof(double) * std::max(1, B)));
   RNNTG_CUDA_TRY(h->counters.ensure(sizeof(unsigned long long) * 16));
   RNNTG_CUDA_TRY(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long) * 16, h->stream));
+  return RNNTG_OK;
+}
+
+// cuStreamWriteValue32 through the runtime's driver entry-point lookup (no
+// link-time libcuda dependency): a stream-ordered 32-bit store with no
+// kernel, so it lands while the decode kernel holds every SM.
+using StreamWrite32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+StreamWrite32 stream_write32() {
+  // Resolved once and proven with a real write + read-back before any kernel
+  // relies on it (a kernel waiting for a write that never lands would hang).
+  static StreamWrite32 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return static_cast<StreamWrite32>(nullptr);
+    auto w = reinterpret_cast<StreamWrite32>(f);
+    int32_t* d = nullptr;
+    cudaStream_t st = nullptr;
+    int32_t got = 0;
+    bool ok = cudaMalloc(reinterpret_cast<void**>(&d), sizeof(int32_t)) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaMemsetAsync(d, 0, sizeof(int32_t), st) == cudaSuccess &&
+              w(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(d), 0x5a5a5a5au,
+                CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS &&
+              cudaMemcpyAsync(&got, d, sizeof(int32_t), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+              cudaStreamSynchronize(st) == cudaSuccess && got == 0x5a5a5a5a;
+    if (st) cudaStreamDestroy(st);
+    if (d) cudaFree(d);
+    cudaGetLastError();
+    return ok ? w : static_cast<StreamWrite32>(nullptr);
+  }();
+  return fn;
+}
+
+// Frames -> decode with the encoder projection fused into the beam kernel.
+// Device frames: one launch.  Host frames (every stream T frames): the
+// kernel is launched first and polls a device counter of landed time slices;
+// a copy stream moves slice s = frames [s*S, (s+1)*S) of all streams with one
+// pitched cudaMemcpy2DAsync and then bumps the counter with a stream-ordered
+// write, so the copy engine streams frames in while the SMs decode.
+template <typename Launch>
+rnntg_status run_fused(rnntg_model_t h, const float* enc, const int32_t* fs, int32_t B, int32_t mem,
+                       int64_t* launches, Launch&& launch) {
+  constexpr int32_t kSlice = 32;
+  const int32_t D = h->d.D;
+  RNNTG_CUDA_TRY(h->ready.ensure(sizeof(int32_t)));
+  int32_t* ready = h->ready.as<int32_t>();
+  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
+  const float* d_enc = mem == RNNTG_MEM_HOST ? h->enc.as<float>() : enc;
+  RNNTG_CUDA_TRY(cudaMemsetAsync(ready, mem == RNNTG_MEM_HOST ? 0x00 : 0x7f, sizeof(int32_t), h->stream));
+  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+  RNNTG_CUDA_TRY(launch(d_enc, ready, kSlice, h->stream));
+  ++*launches;
+  if (mem == RNNTG_MEM_HOST && fs[B] > 0) {
+    if (!h->cstream[0]) RNNTG_CUDA_TRY(cudaStreamCreateWithFlags(&h->cstream[0], cudaStreamNonBlocking));
+    cudaStream_t cs = h->cstream[0];
+    RNNTG_CUDA_TRY(cudaStreamWaitEvent(cs, h->ev[1], 0));
+    const int32_t T = fs[1] - fs[0];
+    const size_t pitch = sizeof(float) * static_cast<size_t>(T) * D;
+    StreamWrite32 w32 = stream_write32();
+    for (int32_t s = 0; s * kSlice < T; ++s) {
+      const int32_t f0 = s * kSlice, nf = std::min(kSlice, T - f0);
+      RNNTG_CUDA_TRY(cudaMemcpy2DAsync(h->enc.as<float>() + static_cast<int64_t>(f0) * D, pitch,
+                                       enc + static_cast<int64_t>(f0) * D, pitch,
+                                       sizeof(float) * static_cast<size_t>(nf) * D, B,
+                                       cudaMemcpyHostToDevice, cs));
+      if (w32(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(ready),
+              static_cast<cuuint32_t>(s + 1), CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+        set_error("cuStreamWriteValue32 failed");
+        return RNNTG_CUDA_ERROR;
+      }
+    }
+    if (!h->done[0]) RNNTG_CUDA_TRY(cudaEventCreateWithFlags(&h->done[0], cudaEventDisableTiming));
+    RNNTG_CUDA_TRY(cudaEventRecord(h->done[0], cs));
+    RNNTG_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->done[0], 0));
+  }
+  h->pipelined = false;
   return RNNTG_OK;
 }
 
@@ -287,6 +373,7 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
   h->num_sms = rnntg::decode_num_sms(device);
   if (const char* ws = std::getenv("RNNTG_WS")) h->warp_specialized = std::atoi(ws) != 0;
   if (const char* bi = std::getenv("RNNTG_BEAM_IMPL")) h->beam_impl = std::atoi(bi);
+  if (const char* fp = std::getenv("RNNTG_FUSED_PE")) h->fused_pe = std::atoi(fp);
   rnntg::DeviceModel& d = h->d;
   d.V = V;
   d.D = D;
@@ -308,6 +395,7 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
     std::vector<float> ob(d.Vp, 0.0f);
     std::copy(desc->out_b, desc->out_b + V, ob.begin());
     if ((st = upload(h, &d.out_b, ob))) return fail(st);
+    if ((st = upload(h, &d.zeros, std::vector<float>(std::max(d.Vp, d.Jp), 0.0f)))) return fail(st);
   }
   if (J % 16 == 0) {
     // bf16 out_w for the tcgen05 variant, pre-arranged chunk by chunk (16
@@ -481,6 +569,49 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
     const int gmax = std::max(1, exact ? 2 * (16 / p->beam_size) : 32 / p->beam_size);
     const int G = std::min(gmax, std::max(1, (B + h->num_sms - 1) / h->num_sms));
     const bool ws = exact && G >= 2 && h->warp_specialized;
+    // Fused encoder projection: exact single-CTA kernel, out_w^T and j_we^T
+    // chunks of one shape, frames of uniform length when they come from the
+    // host (time slices), and a working stream-ordered write.
+    bool uniform = true;
+    for (int32_t i = 1; i < B; ++i) uniform = uniform && fs[i + 1] - fs[i] == fs[1] - fs[0];
+    const bool fused = exact && !ws && h->beam_impl == 1 && h->fused_pe > 0 && h->d.Jp == h->d.Vp &&
+                       h->d.D % 4 == 0 && h->d.D <= rnntg::kMaxJoiner &&
+                       ((mem == RNNTG_MEM_DEVICE && h->fused_pe > 1) ||
+                        (mem == RNNTG_MEM_HOST && uniform && stream_write32() != nullptr));
+    auto args = [&](int32_t b0, int32_t b1) {
+      rnntg::DecodeArgs a{};
+      a.m = &h->d;
+      a.pe = h->pe.as<float>();
+      a.frame_splits = h->splits.as<int32_t>() + b0;
+      a.B = b1 - b0;
+      a.streams_per_cta = G;
+      a.tokens = h->tok.as<int32_t>();
+      a.lengths = h->len.as<int32_t>() + b0;
+      a.scores = h->score.as<double>() + b0;
+      a.counters = h->counters.as<unsigned long long>();
+      a.beam_size = p->beam_size;
+      a.merge_op = p->merge_op;
+      a.length_norm = p->length_norm;
+      a.max_total = p->max_total_symbols;
+      a.backptr = h->bp.as<uint32_t>() + static_cast<int64_t>(b0) * rnntg::kMaxBeam;
+      a.joiner_bf16 = h->joiner_mode == RNNTG_JOINER_BF16;
+      a.warp_specialized = ws;
+      a.beam_impl = h->beam_impl;
+      return a;
+    };
+    if (fused) {
+      st = run_fused(h, enc, fs, B, mem, &launches, [&](const float* d_enc, const int32_t* rdy, int32_t S,
+                                                       cudaStream_t cs) {
+        rnntg::DecodeArgs a = args(0, B);
+        a.fused_enc = d_enc;
+        a.fused_pe = h->pe.as<float>();
+        a.ready = rdy;
+        a.slice_frames = S;
+        return rnntg::launch_decode_beam(a, cs);
+      });
+      if (st) return st;
+      return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+    }
     st = run_pipeline(h, enc, fs, B, mem, G, &launches, [&](int32_t b0, int32_t b1, cudaStream_t cs) {
       rnntg::DecodeArgs a{};
       a.m = &h->d;

@@ -37,6 +37,7 @@ using namespace dec;
 // ---------------------------------------------------------------------------
 struct GreedySmem {
   uint64_t bar[2];
+  uint32_t wcur[2];
   int64_t row_pe[kRowCap];
   int32_t row_ctx[kRowCap];
   int32_t row_stream[kRowCap];
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int s0 = blockIdx.x * G;
   const int ns = min(G, B - s0);
   if (ns <= 0) return;
-  WPipe pipe{{W0, W1}, S.bar, (m.J + kBK - 1) / kBK};
+  WPipe pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
 
   int32_t tmax = 0;
   for (int i = 0; i < ns; ++i)
@@ -183,7 +184,10 @@ struct BeamCand {  // stage-1 extension or stage-2 merged entry
 };
 
 struct BeamSmem {
+  int64_t pe_src[kRowCap];  // fused encoder projection: frame rows of this pass
+  int32_t pe_rows;
   uint64_t bar[2];
+  uint32_t wcur[2];
   int64_t row_pe[kRowCap];
   int32_t row_ctx[kRowCap];
   double row_lse[kRowCap];
@@ -621,7 +625,81 @@ __device__ void beam_stream_step(const ModelView& m, Hyps& h, BeamCand* cand, ui
   }
 }
 
-template <int BCAP, bool TC>
+// Fused encoder projection (joiner_project_enc, model.hpp:263-271):
+// pe[row] = j_we . enc[row], sequential in k from 0.0f, for up to kRowCap
+// frame rows of the CTA's streams (F consecutive frames each), through the
+// same balanced exact GEMM and chunk pipeline as the joiner (the pipeline's
+// A matrix).  The frame rows are staged k-major in the h tile (row-fastest
+// units: conflict-free), the results are written to the global pe buffer the
+// h build reads.  With host frames streamed in time slices the pass first
+// waits until the slice holding its last frame has landed.
+struct FusedPe {
+  const float* enc;
+  float* pe;
+  const int32_t* ready;
+  int32_t slice_frames;
+  int32_t D;
+  const float* j_wet;
+  const float* zeros;
+};
+
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename Smem>
+__device__ __forceinline__ void fused_pe_pass(const ModelView& m, const FusedPe& fp, const WPipe& pipe,
+                                              uint32_t& g, float* HL, Smem& S,
+                                              const int32_t* __restrict__ frame_splits, int s0,
+                                              int ns, int t, int F) {
+  if (threadIdx.x == 0) {
+    int R = 0, last = t;
+    for (int f = 0; f < F; ++f)
+      for (int i = 0; i < ns; ++i) {
+        const int32_t fs = frame_splits[s0 + i], T = frame_splits[s0 + i + 1] - fs;
+        if (t + f < T) {
+          S.pe_src[R++] = fs + t + f;
+          last = t + f;
+        }
+      }
+    S.pe_rows = R;
+    const int32_t need = last / fp.slice_frames;
+    const long long t0 = clock64();
+    while (ld_acquire(fp.ready) <= need) {
+      __nanosleep(500);
+      if (clock64() - t0 > (1ll << 36)) __trap();  // ~35 s: a slice never landed; fail, don't hang
+    }
+  }
+  __syncthreads();
+  const int R = S.pe_rows;
+  const int D = fp.D, D4 = D >> 2, units = R * D4;
+  for (int x = threadIdx.x; x < units; x += blockDim.x) {  // row-fastest: conflict-free
+    const int i = (x / R) * 4, r = x - (i >> 2) * R;
+    const float4 v = *reinterpret_cast<const float4*>(fp.enc + S.pe_src[r] * D + i);
+    float* o = HL + i * kHStride + r;
+    o[0] = v.x;
+    o[kHStride] = v.y;
+    o[2 * kHStride] = v.z;
+    o[3 * kHStride] = v.w;
+  }
+  __syncthreads();
+  ModelView mp = m;
+  mp.J = D;          // contraction length
+  mp.out_wt = fp.j_wet;
+  mp.out_b = fp.zeros;  // acc starts from 0.0f
+  joiner_gemm(mp, pipe, g, HL, R);  // rows land in HL as [R][Vp] (Vp == Jp)
+  const int J = m.J, J4 = J >> 2;
+  for (int x = threadIdx.x; x < R * J4; x += blockDim.x) {
+    const int r = x / J4, j = (x - r * J4) * 4;
+    *reinterpret_cast<float4*>(fp.pe + S.pe_src[r] * J + j) =
+        *reinterpret_cast<const float4*>(HL + static_cast<int64_t>(r) * m.Vp + j);
+  }
+  __syncthreads();
+}
+
+template <int BCAP, bool TC, bool FPE>
 __global__ void __launch_bounds__(kDecodeThreads, 1)
     beam_kernel(ModelView m, const float* __restrict__ pe,
                 const int32_t* __restrict__ frame_splits, int32_t B, int32_t G,
@@ -629,10 +707,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
                 int32_t max_total, uint32_t* __restrict__ backptr,
                 int32_t* __restrict__ tokens, int32_t* __restrict__ lengths,
                 double* __restrict__ scores,
-                unsigned long long* __restrict__ counters) {
+                unsigned long long* __restrict__ counters, FusedPe fp) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* HL = reinterpret_cast<float*>(smem_raw);
-  const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
+  const int hl_floats = max(max(m.J, fp.D) * kHStride, kRowCap * m.Vp);
   float* W0 = HL + hl_floats;
   float* W1 = W0 + kBK * m.Vp;
   BeamSmem& S = *reinterpret_cast<BeamSmem*>(W1 + kBK * m.Vp);
@@ -648,7 +726,16 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int ns = min(G, B - s0);
   if (ns <= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WPipe pipe{{W0, W1}, S.bar, (m.J + kBK - 1) / kBK};
+  WPipe pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
+  // fused encoder projection: one A pass (j_we) per F frames, F frames x ns
+  // streams <= kRowCap rows
+  const int F = FPE ? max(1, min(4, kRowCap / ns)) : 1;
+  if constexpr (FPE) {
+    pipe.a_ptr = fp.j_wet;
+    pipe.a_K = fp.D;
+    pipe.a_nc = (fp.D + kBK - 1) / kBK;
+    pipe.period = F;
+  }
   TcPipe tp{smem_u32(W0), tb->full, tb->empty, &tb->done, smem_u32(hb), 0u, m.J / kTcBK};
 
   int32_t tmax = 0;
@@ -698,6 +785,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   long long ph_h = 0, ph_gemm = 0, ph_epi = 0, ph_step = 0;  // phase cycles (thread 0)
 
   for (int32_t t = 0; t < tmax; ++t) {
+    if constexpr (FPE) {
+      if (t % F == 0) fused_pe_pass(m, fp, pipe, g, HL, S, frame_splits, s0, ns, t, F);
+    }
     // A. rows: distinct contexts per live stream (lane = stream, G <= 32).
     if (warp == 0) {
       const int R0 = beam_rows(H, ns, frame_splits + s0, t, S.row_pe, S.row_ctx);
@@ -974,6 +1064,7 @@ struct WsHalf {
 
 struct WsSmem {
   uint64_t bar[2];
+  uint32_t wcur[2];
   WsHalf half[2];
 };
 
@@ -1005,7 +1096,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int ns = min(G, B - s0);
   if (ns <= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WPipe pipe{{W0, W1}, S.bar, (m.J + kBK - 1) / kBK};
+  WPipe pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
   const int nA = (ns + 1) >> 1;
   const int hfirst[2] = {0, nA}, hcount[2] = {nA, ns - nA};
   float* const HLh[2] = {HL0, HL1};
@@ -1125,21 +1216,31 @@ cudaError_t launch_beam_ws(const DecodeArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int BCAP, bool TC>
-cudaError_t launch_beam_cap(const DecodeArgs& a, cudaStream_t s) {
+template <int BCAP, bool TC, bool FPE>
+cudaError_t launch_beam_cap3(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);
   const int G = a.streams_per_cta;
-  size_t smem = smem_common(m) + sizeof(BeamSmem) + sizeof(Hyps) * G +
+  FusedPe fp{a.fused_enc, a.fused_pe, a.ready, a.slice_frames, FPE ? a.m->D : 0, a.m->j_wet, a.m->zeros};
+  const size_t hl = static_cast<size_t>(max(max(m.J, fp.D) * kHStride, kRowCap * m.Vp)) * 4;
+  size_t smem = hl + static_cast<size_t>(2) * kBK * m.Vp * 4 + sizeof(BeamSmem) + sizeof(Hyps) * G +
                 sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
   if (TC) smem += 1024 + static_cast<size_t>(kRowCap) * m.J * 2 + sizeof(TcBars);
-  cudaError_t e = cudaFuncSetAttribute(beam_kernel<BCAP, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = cudaFuncSetAttribute(beam_kernel<BCAP, TC, FPE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int grid = (a.B + G - 1) / G;
-  beam_kernel<BCAP, TC><<<grid, kDecodeThreads, smem, s>>>(
+  beam_kernel<BCAP, TC, FPE><<<grid, kDecodeThreads, smem, s>>>(
       m, a.pe, a.frame_splits, a.B, G, a.beam_size, a.merge_op, a.length_norm, a.max_total,
-      a.backptr, a.tokens, a.lengths, a.scores, a.counters);
+      a.backptr, a.tokens, a.lengths, a.scores, a.counters, fp);
   return cudaGetLastError();
+}
+
+template <int BCAP, bool TC>
+cudaError_t launch_beam_cap(const DecodeArgs& a, cudaStream_t s) {
+  if constexpr (!TC) {
+    if (a.fused_enc) return launch_beam_cap3<BCAP, false, true>(a, s);
+  }
+  return launch_beam_cap3<BCAP, TC, false>(a, s);
 }
 
 template <int BCAP>

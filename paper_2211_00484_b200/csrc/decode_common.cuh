@@ -88,25 +88,57 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------------------
-// out_w chunk pipeline.  Chunk g (a running sequence number across frames)
-// holds k-rows [(g % nc) * kBK, ...) of out_wt and lives in stage g & 1.
+// Weight chunk pipeline.  Chunk g (a running sequence number across frames)
+// lives in stage g & 1.  The sequence is data independent and periodic:
+// optionally a_nc chunks of matrix A (the fused encoder projection j_we^T,
+// once per `period` frames), then `period` passes of nc chunks of matrix B
+// (out_w^T, once per frame).  Each chunk is kBK k-rows of a k-major [K][N]
+// matrix; both matrices share the stage size (N_A == N_B).
 // ---------------------------------------------------------------------------
 struct WPipe {
   float* stage[2];
   uint64_t* bar;  // [2]
-  int32_t nc;     // chunks per frame
+  uint32_t* cur;  // [2] smem issue cursor (thread 0): position in the period, B chunk index
+  int32_t nc;     // chunks per B pass
+  const float* b_ptr;
+  int32_t b_K, b_N;
+  const float* a_ptr;  // nullptr: no A passes
+  int32_t a_nc, a_K;
+  int32_t period;      // B passes per A pass
 };
 
-__device__ __forceinline__ void wpipe_issue(const WPipe& p, const ModelView& m,
-                                            uint32_t g) {
-  const int32_t c = static_cast<int32_t>(g % static_cast<uint32_t>(p.nc));
-  const int32_t rows = min(kBK, m.J - c * kBK);
-  const uint32_t bytes = static_cast<uint32_t>(rows) * m.Vp * 4u;
+__device__ __forceinline__ WPipe make_wpipe(float* W0, float* W1, uint64_t* bar, uint32_t* cur,
+                                            const ModelView& m) {
+  return WPipe{{W0, W1}, bar, cur, (m.J + kBK - 1) / kBK, m.out_wt, m.J, m.Vp, nullptr, 0, 0, 1};
+}
+
+// Issues chunk g (thread 0; chunks are issued strictly in sequence, so the
+// schedule position advances by a cursor — no division on the issuing
+// warp's path).
+__device__ __forceinline__ void wpipe_issue(const WPipe& p, const ModelView& /*m*/, uint32_t g) {
+  if (g == 0) {
+    p.cur[0] = 0;
+    p.cur[1] = 0;
+  }
+  const int32_t q = static_cast<int32_t>(p.cur[0]);
+  const int32_t per = p.a_nc + p.period * p.nc;
+  p.cur[0] = q + 1 == per ? 0u : static_cast<uint32_t>(q + 1);
+  const float* src;
+  int32_t rows;
+  if (q < p.a_nc) {
+    rows = min(kBK, p.a_K - q * kBK);
+    src = p.a_ptr + static_cast<int64_t>(q) * kBK * p.b_N;
+  } else {
+    const int32_t c = static_cast<int32_t>(p.cur[1]);
+    p.cur[1] = c + 1 == p.nc ? 0u : static_cast<uint32_t>(c + 1);
+    rows = min(kBK, p.b_K - c * kBK);
+    src = p.b_ptr + static_cast<int64_t>(c) * kBK * p.b_N;
+  }
+  const uint32_t bytes = static_cast<uint32_t>(rows) * p.b_N * 4u;
   uint64_t* bar = p.bar + (g & 1u);
   fence_proxy_async();
   mbar_expect_tx(bar, bytes);
-  bulk_g2s(p.stage[g & 1u], m.out_wt + static_cast<int64_t>(c) * kBK * m.Vp,
-           bytes, bar);
+  bulk_g2s(p.stage[g & 1u], src, bytes, bar);
 }
 
 // C. logits[r][n] = out_b[n] + sum_k out_w[n][k] * h[r][k], sequential in k.

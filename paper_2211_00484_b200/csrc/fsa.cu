@@ -77,6 +77,7 @@ struct FsaStream {
 
 struct FsaSmem {
   uint64_t bar[2];
+  uint32_t wcur[2];
   int64_t row_pe[kRowCap];
   int32_t row_ctx[kRowCap];
   double row_lse[kRowCap];
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int s0 = blockIdx.x * G;
   const int ns = min(G, B - s0);
   if (ns <= 0) return;
-  WPipe pipe{{W0, W1}, C.bar, (m.J + kBK - 1) / kBK};
+  WPipe pipe = make_wpipe(W0, W1, C.bar, C.wcur, m);
   const int nt = kDecodeThreads / G;
   const Group grp{static_cast<int>(threadIdx.x) / nt, static_cast<int>(threadIdx.x) % nt, nt};
   const bool have = grp.id < ns;

@@ -40,6 +40,7 @@ struct DeviceModel {
   float* j_b = nullptr;    // [J]
   float* out_wt = nullptr; // [J][Vp]   (transposed out_w, zero-padded)
   float* out_b = nullptr;  // [Vp]
+  float* zeros = nullptr;  // [max(Vp, Jp)] zero bias (encoder projection starts from 0.0f)
   float* pd_table = nullptr; // [V*V][J]: decoder-side joiner projection of
                              // every packed context (K0)
   uint16_t* out_w_bf16 = nullptr; // bf16 out_w, UMMA chunk layout (tcgen05 variant)
@@ -107,6 +108,11 @@ struct DecodeArgs {
   int32_t beam_impl;        // 1: single 512-thread CTA per SM (default); 0: dual-residency kernel
   int32_t cta_slots;        // dual kernel: CTA slots this launch may fill (0: 2 x SMs)
   uint32_t* backptr;        // device [(sum T + B) * kMaxBeam]
+  // beam, fused encoder projection (pe computed inside the decode kernel):
+  const float* fused_enc;   // device [sum T][D] frames, or nullptr (pe precomputed by K1)
+  float* fused_pe;          // device [sum T][J] written by the kernel (== pe)
+  const int32_t* ready;     // device: number of frame slices of fused_enc that have landed
+  int32_t slice_frames;     // frames per slice (slice s = frames [s*slice_frames, ...) of every stream)
   // fsa
   const void* graph_arcs;   // device int4-packed arcs
   const int32_t* graph_splits;
