@@ -120,6 +120,11 @@ typedef struct {
                                    (row groups of 4, padding included) */
   int64_t gather_cycles;  /* beam kernel: cycles of the h build spent gathering
                              pe / pd rows (thread 0, summed over CTAs) */
+  int64_t gemm_wait_cycles; /* beam kernel: joiner GEMM cycles thread 0 waited
+                               for weight chunks (pipeline starvation) */
+  int64_t fused_pe_cycles[4]; /* beam kernel, fused encoder projection (thread 0,
+                                 summed over CTAs): row list + slice wait, frame
+                                 staging, GEMM, pe write-back */
 } rnntg_stats;
 
 const char* rnntg_last_error(void);

@@ -90,6 +90,8 @@ class _Stats(C.Structure):
         ("phase_cycles", C.c_int64 * 4),
         ("joiner_rows_computed", C.c_int64),
         ("gather_cycles", C.c_int64),
+        ("gemm_wait_cycles", C.c_int64),
+        ("fused_pe_cycles", C.c_int64 * 4),
     ]
 
 
@@ -326,6 +328,7 @@ class Decoder:
         _check(self._lib.rnntg_get_stats(self.h, C.byref(s)))
         d = {f: getattr(s, f) for f, _ in _Stats._fields_}
         d["phase_cycles"] = list(d["phase_cycles"])
+        d["fused_pe_cycles"] = list(d["fused_pe_cycles"])
         return d
 
     # ---- searches ----

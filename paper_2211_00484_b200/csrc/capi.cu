@@ -319,6 +319,8 @@ rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
   for (int i = 0; i < 4; ++i) h->stats.phase_cycles[i] = static_cast<int64_t>(cnt[8 + i]);
   h->stats.joiner_rows_computed = static_cast<int64_t>(cnt[5]);
   h->stats.gather_cycles = static_cast<int64_t>(cnt[6]);
+  h->stats.gemm_wait_cycles = static_cast<int64_t>(cnt[7]);
+  for (int i = 0; i < 4; ++i) h->stats.fused_pe_cycles[i] = static_cast<int64_t>(cnt[12 + i]);
   h->stats.gpu_ms = ms_all;
   h->stats.decode_ms = ms_dec;
   return RNNTG_OK;

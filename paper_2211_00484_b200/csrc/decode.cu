@@ -24,6 +24,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "decode_common.cuh"
 
@@ -184,6 +185,8 @@ struct BeamCand {  // stage-1 extension or stage-2 merged entry
 };
 
 struct BeamSmem {
+  unsigned long long stat[16];  // per-CTA counters (layout of DecodeArgs::counters)
+  WPipe pipe;
   int64_t pe_src[kRowCap];  // fused encoder projection: frame rows of this pass
   int32_t pe_rows;
   uint64_t bar[2];
@@ -641,6 +644,7 @@ struct FusedPe {
   int32_t D;
   const float* j_wet;
   const float* zeros;
+  int32_t dbg_force_r;  // development: GEMM over this many rows every frame (0 = off)
 };
 
 __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
@@ -653,43 +657,70 @@ template <typename Smem>
 __device__ __forceinline__ void fused_pe_pass(const ModelView& m, const FusedPe& fp, const WPipe& pipe,
                                               uint32_t& g, float* HL, Smem& S,
                                               const int32_t* __restrict__ frame_splits, int s0,
-                                              int ns, int t, int F) {
-  if (threadIdx.x == 0) {
+                                              int ns, int t, int F, long long* ph) {
+  const long long q0 = clock64();
+  if (threadIdx.x < 32) {  // warp 0: rows in (frame, stream) order, lane = stream
+    const int lane = threadIdx.x;
+    int32_t fs = 0, T = 0;
+    if (lane < ns) {
+      fs = frame_splits[s0 + lane];
+      T = frame_splits[s0 + lane + 1] - fs;
+    }
     int R = 0, last = t;
-    for (int f = 0; f < F; ++f)
-      for (int i = 0; i < ns; ++i) {
-        const int32_t fs = frame_splits[s0 + i], T = frame_splits[s0 + i + 1] - fs;
-        if (t + f < T) {
-          S.pe_src[R++] = fs + t + f;
-          last = t + f;
-        }
+    for (int f = 0; f < F; ++f) {
+      const bool ok = lane < ns && t + f < T;
+      const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+      if (ok) S.pe_src[R + __popc(bal & ((1u << lane) - 1u))] = fs + t + f;
+      if (bal) last = t + f;
+      R += __popc(bal);
+    }
+    if (lane == 0) {
+      S.pe_rows = R;
+      const int32_t need = last / fp.slice_frames;
+      const long long t0 = clock64();
+      while (ld_acquire(fp.ready) <= need) {
+        __nanosleep(500);
+        if (clock64() - t0 > (1ll << 36)) __trap();  // ~35 s: a slice never landed; fail, don't hang
       }
-    S.pe_rows = R;
-    const int32_t need = last / fp.slice_frames;
-    const long long t0 = clock64();
-    while (ld_acquire(fp.ready) <= need) {
-      __nanosleep(500);
-      if (clock64() - t0 > (1ll << 36)) __trap();  // ~35 s: a slice never landed; fail, don't hang
     }
   }
   __syncthreads();
+  const long long q1 = clock64();
   const int R = S.pe_rows;
   const int D = fp.D, D4 = D >> 2, units = R * D4;
-  for (int x = threadIdx.x; x < units; x += blockDim.x) {  // row-fastest: conflict-free
-    const int i = (x / R) * 4, r = x - (i >> 2) * R;
-    const float4 v = *reinterpret_cast<const float4*>(fp.enc + S.pe_src[r] * D + i);
-    float* o = HL + i * kHStride + r;
-    o[0] = v.x;
-    o[kHStride] = v.y;
-    o[2 * kHStride] = v.z;
-    o[3 * kHStride] = v.w;
+  // Row-fastest units (conflict-free k-major stores); eight loads in flight
+  // per thread before any store.
+  for (int base = threadIdx.x; base < units; base += 8 * blockDim.x) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int x = base + u * blockDim.x;
+      if (x < units) {
+        const int i = (x / R) * 4, r = x - (i >> 2) * R;
+        v[u] = *reinterpret_cast<const float4*>(fp.enc + S.pe_src[r] * D + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int x = base + u * blockDim.x;
+      if (x < units) {
+        const int i = (x / R) * 4, r = x - (i >> 2) * R;
+        float* o = HL + i * kHStride + r;
+        o[0] = v[u].x;
+        o[kHStride] = v[u].y;
+        o[2 * kHStride] = v[u].z;
+        o[3 * kHStride] = v[u].w;
+      }
+    }
   }
   __syncthreads();
+  const long long q2 = clock64();
   ModelView mp = m;
   mp.J = D;          // contraction length
   mp.out_wt = fp.j_wet;
   mp.out_b = fp.zeros;  // acc starts from 0.0f
   joiner_gemm(mp, pipe, g, HL, R);  // rows land in HL as [R][Vp] (Vp == Jp)
+  const long long q3 = clock64();
   const int J = m.J, J4 = J >> 2;
   for (int x = threadIdx.x; x < R * J4; x += blockDim.x) {
     const int r = x / J4, j = (x - r * J4) * 4;
@@ -697,6 +728,12 @@ __device__ __forceinline__ void fused_pe_pass(const ModelView& m, const FusedPe&
         *reinterpret_cast<const float4*>(HL + static_cast<int64_t>(r) * m.Vp + j);
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    ph[0] += q1 - q0;
+    ph[1] += q2 - q1;
+    ph[2] += q3 - q2;
+    ph[3] += clock64() - q3;
+  }
 }
 
 template <int BCAP, bool TC, bool FPE>
@@ -726,15 +763,21 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int ns = min(G, B - s0);
   if (ns <= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WPipe pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
+  // The pipe descriptor lives in shared memory: its fields are read where a
+  // chunk is waited for or issued instead of pinning ~14 registers across
+  // every phase (register pressure here costs the GEMM its LDS prefetch).
+  const WPipe& pipe = S.pipe;
   // fused encoder projection: one A pass (j_we) per F frames, F frames x ns
   // streams <= kRowCap rows
   const int F = FPE ? max(1, min(4, kRowCap / ns)) : 1;
-  if constexpr (FPE) {
-    pipe.a_ptr = fp.j_wet;
-    pipe.a_K = fp.D;
-    pipe.a_nc = (fp.D + kBK - 1) / kBK;
-    pipe.period = F;
+  if (threadIdx.x == 0) {
+    S.pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
+    if constexpr (FPE) {
+      S.pipe.a_ptr = fp.j_wet;
+      S.pipe.a_K = fp.D;
+      S.pipe.a_nc = (fp.D + kBK - 1) / kBK;
+      S.pipe.period = F;
+    }
   }
   TcPipe tp{smem_u32(W0), tb->full, tb->empty, &tb->done, smem_u32(hb), 0u, m.J / kTcBK};
 
@@ -752,6 +795,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     h.h2[0] = 0x13198a2e03707344ull;
     h.p1[0] = h.p2[0] = 0;
   }
+  if (threadIdx.x < 16) S.stat[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     if constexpr (TC) {
       for (int i = 0; i < kTcStages; ++i) {
@@ -780,13 +824,14 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     wpipe_issue(pipe, m, 1);
   }
   uint32_t g = 0;
-  unsigned long long rows_total = 0, ties = 0, rows_padded = 0;
-  long long tsplit = 0, ph_gather = 0;
-  long long ph_h = 0, ph_gemm = 0, ph_epi = 0, ph_step = 0;  // phase cycles (thread 0)
+  // Per-CTA counters live in shared memory (thread 0 accumulates; ties by
+  // shared atomics) so no register is held across the GEMM for them.
+  unsigned long long* st = S.stat;
+  long long* pst = reinterpret_cast<long long*>(S.stat);
 
   for (int32_t t = 0; t < tmax; ++t) {
     if constexpr (FPE) {
-      if (t % F == 0) fused_pe_pass(m, fp, pipe, g, HL, S, frame_splits, s0, ns, t, F);
+      if (t % F == 0) fused_pe_pass(m, fp, pipe, g, HL, S, frame_splits, s0, ns, t, F, pst + 12);
     }
     // A. rows: distinct contexts per live stream (lane = stream, G <= 32).
     if (warp == 0) {
@@ -795,19 +840,21 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     }
     __syncthreads();
     const int R = S.nrows;
-    rows_total += R;
-    rows_padded += (m.Vp == 512 && R > 4 && R < 28) ? R : ((R + 3) & ~3);
+    if (threadIdx.x == 0) {
+      st[1] += R;
+      st[5] += (m.Vp == 512 && R > 4 && R < 28) ? R : ((R + 3) & ~3);
+    }
     long long c0 = clock64();
     if constexpr (TC)
       build_h_tc(m, pe, S.row_pe, S.row_ctx, R, R <= 16 ? 16 : 32, hb);
     else
-      build_h(m, pe, S.row_pe, S.row_ctx, R, HL, &tsplit);
+      build_h(m, pe, S.row_pe, S.row_ctx, R, HL, pst + 2);
     long long c1 = clock64();
-    if (threadIdx.x == 0) ph_gather += tsplit - c0;
+    if (threadIdx.x == 0) pst[6] += pst[2] - c0;
     if constexpr (TC)
       tc_gemm(m, tp, g, static_cast<uint32_t>(t), HL, R);
     else
-      joiner_gemm(m, pipe, g, HL, R);
+      joiner_gemm(m, pipe, g, HL, fp.dbg_force_r > 0 ? fp.dbg_force_r : R, pst + 7);
     long long c2 = clock64();
 
     // D. per row: lse, blank logit, top-`beam` tokens k >= 1 by (logit desc,
@@ -833,15 +880,15 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       beam_stream_step<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
                              backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs, beam,
                              merge_log, length_norm, max_total, rr, tokens, lengths + s0 + i,
-                             scores + s0 + i, &ties);
+                             scores + s0 + i, &st[4]);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       const long long c4 = clock64();
-      ph_h += c1 - c0;
-      ph_gemm += c2 - c1;
-      ph_epi += c3 - c2;
-      ph_step += c4 - c3;
+      pst[8] += c1 - c0;
+      pst[9] += c2 - c1;
+      pst[10] += c3 - c2;
+      pst[11] += c4 - c3;
     }
   }
   // Zero-frame streams: empty result, score 0.
@@ -850,15 +897,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       lengths[s0 + i] = 0;
       scores[s0 + i] = 0.0;
     }
-  atomicAdd(&counters[4], ties);
-  if (threadIdx.x == 0) {
-    atomicAdd(&counters[8], static_cast<unsigned long long>(ph_h));
-    atomicAdd(&counters[9], static_cast<unsigned long long>(ph_gemm));
-    atomicAdd(&counters[10], static_cast<unsigned long long>(ph_epi));
-    atomicAdd(&counters[11], static_cast<unsigned long long>(ph_step));
-    atomicAdd(&counters[5], rows_padded);
-    atomicAdd(&counters[6], static_cast<unsigned long long>(ph_gather));
-  }
+  __syncthreads();
+  if (threadIdx.x < 16 && threadIdx.x != 0 && threadIdx.x != 2 && st[threadIdx.x] != 0)
+    atomicAdd(&counters[threadIdx.x], st[threadIdx.x]);
   if constexpr (TC) {
     // Chunks g .. g+kTcStages-2 were prefetched for a frame that never came.
     if (threadIdx.x == 0)
@@ -878,7 +919,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     unsigned long long sf = 0;
     for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
     atomicAdd(&counters[0], sf);
-    atomicAdd(&counters[1], rows_total);
   }
 }
 
@@ -945,7 +985,7 @@ __global__ void __launch_bounds__(kDualThreads, 2)
   if (threadIdx.x == 0) dual_pipe_prime(pipe, m);
   uint32_t g = 0;
   unsigned long long rows_total = 0, ties = 0, rows_padded = 0;
-  long long tsplit = 0, ph_gather = 0;
+  long long tsplit = 0, ph_gather = 0, ph_pe[4] = {0, 0, 0, 0}, wcyc[2] = {0, 0};
   long long ph_h = 0, ph_gemm = 0, ph_epi = 0, ph_step = 0;  // phase cycles (thread 0)
 
   for (int32_t t = 0; t < tmax; ++t) {
@@ -1000,7 +1040,6 @@ __global__ void __launch_bounds__(kDualThreads, 2)
     unsigned long long sf = 0;
     for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
     atomicAdd(&counters[0], sf);
-    atomicAdd(&counters[1], rows_total);
   }
 }
 
@@ -1220,7 +1259,11 @@ template <int BCAP, bool TC, bool FPE>
 cudaError_t launch_beam_cap3(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);
   const int G = a.streams_per_cta;
-  FusedPe fp{a.fused_enc, a.fused_pe, a.ready, a.slice_frames, FPE ? a.m->D : 0, a.m->j_wet, a.m->zeros};
+  static const int force_r = [] {
+    const char* e = std::getenv("RNNTG_DBG_FORCE_R");
+    return e ? std::atoi(e) : 0;
+  }();
+  FusedPe fp{a.fused_enc, a.fused_pe, a.ready, a.slice_frames, FPE ? a.m->D : 0, a.m->j_wet, a.m->zeros, force_r};
   const size_t hl = static_cast<size_t>(max(max(m.J, fp.D) * kHStride, kRowCap * m.Vp)) * 4;
   size_t smem = hl + static_cast<size_t>(2) * kBK * m.Vp * 4 + sizeof(BeamSmem) + sizeof(Hyps) * G +
                 sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);

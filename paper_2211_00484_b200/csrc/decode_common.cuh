@@ -264,7 +264,7 @@ __device__ __forceinline__ void gemm_chunk(const ModelView& m, uint32_t ws, cons
 // group split leaves SMSPs 3:3:2:2 loaded at R = 20 (tools/probes/
 // gemm_tiling.cu: 1.23e13 vs 1.47e13 MAC/s).
 __device__ __forceinline__ void gemm_pass_bal(const ModelView& m, const WPipe& p, uint32_t& g,
-                                              float* HL, int R) {
+                                              float* HL, int R, long long* g_wait_cycles = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int full = R >> 2, rem = R & 3;
   if (rem != 0 && 2 * (full & ~1) + 4 * (full & 1) + 4 > kWarps) {  // pad the partial group
@@ -303,7 +303,9 @@ __device__ __forceinline__ void gemm_pass_bal(const ModelView& m, const WPipe& p
     // Idle warps go straight to the barrier (bar.sync does not issue) rather
     // than spinning on the mbarrier.  Warp 0 always waits: it refills the
     // stage.
+    const long long w0 = clock64();
     if (tn != 0 || warp == 0) mbar_wait(p.bar + st, (g >> 1) & 1u);
+    if (threadIdx.x == 0 && g_wait_cycles) *g_wait_cycles += clock64() - w0;
     const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(kBK * m.Vp * 4);
     const int kk_end = min(kBK, m.J - c * kBK);
     const float* hp = HL + static_cast<int64_t>(c * kBK) * kHStride + rg * 4;
@@ -312,8 +314,12 @@ __device__ __forceinline__ void gemm_pass_bal(const ModelView& m, const WPipe& p
     else if (tn == 4 && nr == 3) gemm_chunk<4, 3>(m, ws, hp, kk_end, col, acc);
     else if (tn == 4 && nr == 2) gemm_chunk<4, 2>(m, ws, hp, kk_end, col, acc);
     else if (tn == 4) gemm_chunk<4, 1>(m, ws, hp, kk_end, col, acc);
+    const long long b0 = clock64();
     __syncthreads();  // every warp is done with this stage
-    if (threadIdx.x == 0) wpipe_issue(p, m, g + 2);
+    if (threadIdx.x == 0 && g_wait_cycles) g_wait_cycles[1] += clock64() - b0;
+    // The refill is issued by the last warp: idle or light for every R, so
+    // the issue latency never delays a heavy warp into the next barrier.
+    if (threadIdx.x == kDecodeThreads - 32) wpipe_issue(p, m, g + 2);
   }
   // The last __syncthreads above also retired every read of the h tile.
   if (tn != 0) {
@@ -332,9 +338,9 @@ __device__ __forceinline__ void gemm_pass_bal(const ModelView& m, const WPipe& p
 }
 
 __device__ __forceinline__ void joiner_gemm(const ModelView& m, const WPipe& p,
-                                            uint32_t& g, float* HL, int R) {
+                                            uint32_t& g, float* HL, int R, long long* wc = nullptr) {
   if (m.Vp == 512 && R > 4) {
-    gemm_pass_bal(m, p, g, HL, R);
+    gemm_pass_bal(m, p, g, HL, R, wc);
     return;
   }
   const int rg = (R + 3) >> 2;

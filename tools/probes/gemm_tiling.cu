@@ -241,7 +241,9 @@ int main() {
     printf("\"B256x2_NG4_TC2(R16/CTA)\": %.3e", m);
   }
   {
-    float* wg; cudaMalloc(&wg, J * Vp * 4); cudaMemset(wg, 0, J * Vp * 4);
+    float* wg; cudaMalloc(&wg, J * Vp * 4);
+    { float* hw = (float*)malloc(J * Vp * 4); unsigned st = 7; for (int i = 0; i < J * Vp; ++i) { st = st * 1664525u + 1013904223u; hw[i] = ((st >> 8) * (1.0f / 16777216.0f) - 0.5f) * 0.088f; }
+      cudaMemcpy(wg, hw, J * Vp * 4, cudaMemcpyHostToDevice); free(hw); }
     for (int v = 0; v < 4; ++v) {
       for (int R : {16, 24}) {
         const int KS = v < 2 ? 2 : 3;

@@ -29,6 +29,9 @@ tot = sum(ph) or 1
 print(json.dumps(dict(B=B, T=T, decode_ms=out, gpu_ms=st["gpu_ms"], fps_decode=B * T / (min(out) * 1e-3),
                       rows_per_sf=st["joiner_rows"] / st["stream_frames"], ties=st["tie_breaks"],
                       gather_share=round(st["gather_cycles"] / tot, 3),
+                      gemm_wait_share=round(st["gemm_wait_cycles"] / tot, 4),
+                      gemm_bar_share=round(st["lattice_arcs"] / tot, 4),
+                      fused_pe_share=[round(x / tot, 4) for x in st["fused_pe_cycles"]],
                       padded_per_row=st["joiner_rows_computed"] / max(1, st["joiner_rows"]),
                       gemm_mac_per_s_per_sm=st["joiner_rows_computed"] * 512 * 512 /
                       (st["phase_cycles"][1] / 1.965e9),
