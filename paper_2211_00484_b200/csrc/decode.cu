@@ -654,7 +654,7 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
 }
 
 template <typename Smem>
-__device__ __forceinline__ void fused_pe_pass(const ModelView& m, const FusedPe& fp, const WPipe& pipe,
+__device__ __noinline__ void fused_pe_pass(const ModelView& m, const FusedPe& fp, const WPipe& pipe,
                                               uint32_t& g, float* HL, Smem& S,
                                               const int32_t* __restrict__ frame_splits, int s0,
                                               int ns, int t, int F, long long* ph) {
