@@ -568,8 +568,13 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
     // Streams per CTA: enough to give every SM work, capped by the 32-row
     // joiner tile (and, for the warp-specialised kernel, 16 rows per half).
     const bool exact = h->joiner_mode == RNNTG_JOINER_EXACT;
+    // Batches beyond one wave (num_sms * gmax streams) run in whole waves of
+    // equal CTAs: G = ceil(B / (waves * num_sms)), not gmax with a ragged
+    // last wave (B = 2048: 2 x 148 CTAs of 7 streams, not 148 + 108 of 8).
     const int gmax = std::max(1, exact ? 2 * (16 / p->beam_size) : 32 / p->beam_size);
-    const int G = std::min(gmax, std::max(1, (B + h->num_sms - 1) / h->num_sms));
+    const int64_t waves = (static_cast<int64_t>(B) + static_cast<int64_t>(h->num_sms) * gmax - 1) /
+                          (static_cast<int64_t>(h->num_sms) * gmax);
+    const int G = std::min<int64_t>(gmax, std::max<int64_t>(1, (B + waves * h->num_sms - 1) / (waves * h->num_sms)));
     const bool ws = exact && G >= 2 && h->warp_specialized;
     // Fused encoder projection: exact single-CTA kernel, out_w^T and j_we^T
     // chunks of one shape, frames of uniform length when they come from the
