@@ -748,9 +748,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* HL = reinterpret_cast<float*>(smem_raw);
   const int hl_floats = max(max(m.J, fp.D) * kHStride, kRowCap * m.Vp);
+  // weight stages: two kBK-row fp32 chunks, or (bf16 variant) kTcStages
+  // 16 KB bf16 chunks = the area of two 16-row fp32 chunks
+  const int wst = TC ? 16 * m.Vp : kBK * m.Vp;
   float* W0 = HL + hl_floats;
-  float* W1 = W0 + kBK * m.Vp;
-  BeamSmem& S = *reinterpret_cast<BeamSmem*>(W1 + kBK * m.Vp);
+  float* W1 = W0 + wst;
+  BeamSmem& S = *reinterpret_cast<BeamSmem*>(W1 + wst);
   Hyps* H = reinterpret_cast<Hyps*>(&S + 1);          // [G]
   BeamCand* C = reinterpret_cast<BeamCand*>(H + G);   // [G][BCAP*BCAP + 2*BCAP]
   constexpr int kCandPerStream = BCAP * BCAP + 2 * BCAP;
@@ -775,7 +778,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     if constexpr (FPE) {
       S.pipe.a_ptr = fp.j_wet;
       S.pipe.a_K = fp.D;
-      S.pipe.a_nc = (fp.D + kBK - 1) / kBK;
+      S.pipe.a_nc = (fp.D + kBK - 1) / kBK;  // (bk == kBK for this kernel)
       S.pipe.period = F;
     }
   }
@@ -1124,8 +1127,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   float* HL0 = reinterpret_cast<float*>(smem_raw);
   float* HL1 = HL0 + hl;
   float* W0 = HL1 + hl;
-  float* W1 = W0 + kBK * m.Vp;
-  WsSmem& S = *reinterpret_cast<WsSmem*>(W1 + kBK * m.Vp);
+  float* W1 = W0 + kBKSmall * m.Vp;
+  WsSmem& S = *reinterpret_cast<WsSmem*>(W1 + kBKSmall * m.Vp);
   Hyps* H = reinterpret_cast<Hyps*>(&S + 1);         // [G]
   BeamCand* C = reinterpret_cast<BeamCand*>(H + G);  // [G][BCAP*BCAP + 2*BCAP]
   constexpr int kCandPerStream = BCAP * BCAP + 2 * BCAP;
@@ -1135,7 +1138,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int ns = min(G, B - s0);
   if (ns <= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WPipe pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
+  WPipe pipe = make_wpipe(W0, W1, S.bar, S.wcur, m, kBKSmall);
   const int nA = (ns + 1) >> 1;
   const int hfirst[2] = {0, nA}, hcount[2] = {nA, ns - nA};
   float* const HLh[2] = {HL0, HL1};
@@ -1243,7 +1246,7 @@ cudaError_t launch_beam_ws(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);
   const int G = a.streams_per_cta;
   const size_t hl = static_cast<size_t>(std::max(m.J * kWsHStride, kWsHalfRows * m.Vp)) * 4;
-  const size_t smem = 2 * hl + static_cast<size_t>(2) * kBK * m.Vp * 4 + sizeof(WsSmem) +
+  const size_t smem = 2 * hl + static_cast<size_t>(2) * kBKSmall * m.Vp * 4 + sizeof(WsSmem) +
                       sizeof(Hyps) * G + sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
   cudaError_t e = cudaFuncSetAttribute(beam_ws_kernel<BCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -1265,7 +1268,7 @@ cudaError_t launch_beam_cap3(const DecodeArgs& a, cudaStream_t s) {
   }();
   FusedPe fp{a.fused_enc, a.fused_pe, a.ready, a.slice_frames, FPE ? a.m->D : 0, a.m->j_wet, a.m->zeros, force_r};
   const size_t hl = static_cast<size_t>(max(max(m.J, fp.D) * kHStride, kRowCap * m.Vp)) * 4;
-  size_t smem = hl + static_cast<size_t>(2) * kBK * m.Vp * 4 + sizeof(BeamSmem) + sizeof(Hyps) * G +
+  size_t smem = hl + static_cast<size_t>(2) * (TC ? 16 : kBK) * m.Vp * 4 + sizeof(BeamSmem) + sizeof(Hyps) * G +
                 sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
   if (TC) smem += 1024 + static_cast<size_t>(kRowCap) * m.J * 2 + sizeof(TcBars);
   cudaError_t e = cudaFuncSetAttribute(beam_kernel<BCAP, TC, FPE>,

@@ -17,7 +17,8 @@ using rnntg_exact::fadd;
 using rnntg_exact::fmul;
 
 constexpr int kWarps = kDecodeThreads / 32;  // 16
-constexpr int kBK = 16;                      // k rows per out_w chunk
+constexpr int kBK = 32;                      // k rows per weight chunk (greedy / beam)
+constexpr int kBKSmall = 16;                 // ... where shared memory is tighter (FSA, warp-specialised)
 constexpr int kRowCap = 32;                  // joiner rows per CTA per frame
 constexpr int kHStride = kRowCap + 4;        // padded k-major h tile stride
 
@@ -99,6 +100,7 @@ struct WPipe {
   float* stage[2];
   uint64_t* bar;  // [2]
   uint32_t* cur;  // [2] smem issue cursor (thread 0): position in the period, B chunk index
+  int32_t bk;     // k rows per chunk
   int32_t nc;     // chunks per B pass
   const float* b_ptr;
   int32_t b_K, b_N;
@@ -108,8 +110,8 @@ struct WPipe {
 };
 
 __device__ __forceinline__ WPipe make_wpipe(float* W0, float* W1, uint64_t* bar, uint32_t* cur,
-                                            const ModelView& m) {
-  return WPipe{{W0, W1}, bar, cur, (m.J + kBK - 1) / kBK, m.out_wt, m.J, m.Vp, nullptr, 0, 0, 1};
+                                            const ModelView& m, int bk = kBK) {
+  return WPipe{{W0, W1}, bar, cur, bk, (m.J + bk - 1) / bk, m.out_wt, m.J, m.Vp, nullptr, 0, 0, 1};
 }
 
 // Issues chunk g (thread 0; chunks are issued strictly in sequence, so the
@@ -126,13 +128,13 @@ __device__ __forceinline__ void wpipe_issue(const WPipe& p, const ModelView& /*m
   const float* src;
   int32_t rows;
   if (q < p.a_nc) {
-    rows = min(kBK, p.a_K - q * kBK);
-    src = p.a_ptr + static_cast<int64_t>(q) * kBK * p.b_N;
+    rows = min(p.bk, p.a_K - q * p.bk);
+    src = p.a_ptr + static_cast<int64_t>(q) * p.bk * p.b_N;
   } else {
     const int32_t c = static_cast<int32_t>(p.cur[1]);
     p.cur[1] = c + 1 == p.nc ? 0u : static_cast<uint32_t>(c + 1);
-    rows = min(kBK, p.b_K - c * kBK);
-    src = p.b_ptr + static_cast<int64_t>(c) * kBK * p.b_N;
+    rows = min(p.bk, p.b_K - c * p.bk);
+    src = p.b_ptr + static_cast<int64_t>(c) * p.bk * p.b_N;
   }
   const uint32_t bytes = static_cast<uint32_t>(rows) * p.b_N * 4u;
   uint64_t* bar = p.bar + (g & 1u);
@@ -175,9 +177,9 @@ __device__ __forceinline__ void gemm_pass(const ModelView& m, const WPipe& p,
     const uint32_t st = g & 1u;
     mbar_wait(p.bar + st, (g >> 1) & 1u);
     if (active) {
-      const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(kBK * m.Vp * 4);
-      const int kk_end = min(kBK, m.J - c * kBK);
-      const float* hp = HL + static_cast<int64_t>(c * kBK) * kHStride + rg * 4;
+      const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(p.bk * m.Vp * 4);
+      const int kk_end = min(p.bk, m.J - c * p.bk);
+      const float* hp = HL + static_cast<int64_t>(c * p.bk) * kHStride + rg * 4;
 #pragma unroll 4
       for (int kk = 0; kk < kk_end; ++kk) {
         const float4 h4 = *reinterpret_cast<const float4*>(hp + kk * kHStride);
@@ -306,9 +308,9 @@ __device__ __forceinline__ void gemm_pass_bal(const ModelView& m, const WPipe& p
     const long long w0 = clock64();
     if (tn != 0 || warp == 0) mbar_wait(p.bar + st, (g >> 1) & 1u);
     if (threadIdx.x == 0 && g_wait_cycles) *g_wait_cycles += clock64() - w0;
-    const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(kBK * m.Vp * 4);
-    const int kk_end = min(kBK, m.J - c * kBK);
-    const float* hp = HL + static_cast<int64_t>(c * kBK) * kHStride + rg * 4;
+    const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(p.bk * m.Vp * 4);
+    const int kk_end = min(p.bk, m.J - c * p.bk);
+    const float* hp = HL + static_cast<int64_t>(c * p.bk) * kHStride + rg * 4;
     if (tn == 8) gemm_chunk<8, 4>(m, ws, hp, kk_end, col, acc);
     else if (tn == 4 && nr == 4) gemm_chunk<4, 4>(m, ws, hp, kk_end, col, acc);
     else if (tn == 4 && nr == 3) gemm_chunk<4, 3>(m, ws, hp, kk_end, col, acc);
@@ -397,9 +399,9 @@ __device__ __forceinline__ void gemm_pass_g(const ModelView& m, const WPipe& p, 
     const uint32_t st = g & 1u;
     mbar_wait(p.bar + st, (g >> 1) & 1u);
     if (active) {
-      const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(kBK * m.Vp * 4);
-      const int kk_end = min(kBK, m.J - c * kBK);
-      const float* hp = HL + static_cast<int64_t>(c * kBK) * hstride + rg * 4;
+      const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(p.bk * m.Vp * 4);
+      const int kk_end = min(p.bk, m.J - c * p.bk);
+      const float* hp = HL + static_cast<int64_t>(c * p.bk) * hstride + rg * 4;
 #pragma unroll 4
       for (int kk = 0; kk < kk_end; ++kk) {
         const float4 h4 = *reinterpret_cast<const float4*>(hp + kk * hstride);
@@ -742,9 +744,9 @@ __device__ __forceinline__ void tc_gemm(const ModelView& m, const TcPipe& p, uin
   __syncthreads();
 }
 
-inline size_t smem_common(const ModelView& m) {
+inline size_t smem_common(const ModelView& m, int bk = kBK) {
   const size_t hl = static_cast<size_t>(max(m.J * kHStride, kRowCap * m.Vp)) * 4;
-  return hl + static_cast<size_t>(2) * kBK * m.Vp * 4;
+  return hl + static_cast<size_t>(2) * bk * m.Vp * 4;
 }
 
 // ---------------------------------------------------------------------------

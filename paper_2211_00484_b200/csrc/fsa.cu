@@ -254,14 +254,14 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   float* HL = reinterpret_cast<float*>(smem_raw);
   const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
   float* W0 = HL + hl_floats;
-  float* W1 = W0 + kBK * m.Vp;
-  FsaSmem& C = *reinterpret_cast<FsaSmem*>(W1 + kBK * m.Vp);
+  float* W1 = W0 + kBKSmall * m.Vp;
+  FsaSmem& C = *reinterpret_cast<FsaSmem*>(W1 + kBKSmall * m.Vp);
   FsaStream* SS = reinterpret_cast<FsaStream*>(&C + 1);
 
   const int s0 = blockIdx.x * G;
   const int ns = min(G, B - s0);
   if (ns <= 0) return;
-  WPipe pipe = make_wpipe(W0, W1, C.bar, C.wcur, m);
+  WPipe pipe = make_wpipe(W0, W1, C.bar, C.wcur, m, kBKSmall);
   const int nt = kDecodeThreads / G;
   const Group grp{static_cast<int>(threadIdx.x) / nt, static_cast<int>(threadIdx.x) % nt, nt};
   const bool have = grp.id < ns;
@@ -722,7 +722,7 @@ size_t fsa_stream_smem() { return sizeof(FsaStream); }
 cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);
   const int G = a.streams_per_cta;
-  const size_t smem = smem_common(m) + sizeof(FsaSmem) + sizeof(FsaStream) * G;
+  const size_t smem = smem_common(m, kBKSmall) + sizeof(FsaSmem) + sizeof(FsaStream) * G;
   cudaError_t e = cudaFuncSetAttribute(fsa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
