@@ -393,15 +393,15 @@ __device__ __forceinline__ uint64_t tok_key(float v, int k) {
 
 template <int BCAP, int NR>
 __device__ __forceinline__ void beam_row_reduce_n(const float* HL, int Vp, int V, int beam, int r0,
-                                                  int R, RowRes rr) {
+                                                  int R, RowRes rr, int rs = 16) {
   const int lane = threadIdx.x & 31;
   uint64_t t[NR][BCAP];
   const float* L[NR];
   bool live[NR];
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
-    live[j] = r0 + 16 * j < R;
-    L[j] = HL + static_cast<int64_t>(live[j] ? r0 + 16 * j : r0) * Vp;
+    live[j] = r0 + rs * j < R;
+    L[j] = HL + static_cast<int64_t>(live[j] ? r0 + rs * j : r0) * Vp;
 #pragma unroll
     for (int q = 0; q < BCAP; ++q) t[j][q] = 0;
   }
@@ -430,8 +430,8 @@ __device__ __forceinline__ void beam_row_reduce_n(const float* HL, int Vp, int V
       const int k = H != 0 ? static_cast<int>(~Lo) : 0x7fffffff;
       if (q == 0 && H != 0) M[j] = fmaxf(M[j], v);
       if (lane == 0 && live[j]) {
-        rr.tl[r0 + 16 * j][q] = v;
-        rr.tk[r0 + 16 * j][q] = k;
+        rr.tl[r0 + rs * j][q] = v;
+        rr.tk[r0 + rs * j][q] = k;
       }
       if (H != 0 && t[j][0] == ((static_cast<uint64_t>(H) << 32) | Lo)) {
 #pragma unroll
@@ -451,8 +451,8 @@ __device__ __forceinline__ void beam_row_reduce_n(const float* HL, int Vp, int V
   for (int j = 0; j < NR; ++j) {
     s[j] = warp_sum_d(s[j]);
     if (lane == 0 && live[j]) {
-      rr.lse[r0 + 16 * j] = static_cast<double>(M[j]) + log(s[j]);
-      rr.l0[r0 + 16 * j] = L[j][0];
+      rr.lse[r0 + rs * j] = static_cast<double>(M[j]) + log(s[j]);
+      rr.l0[r0 + rs * j] = L[j][0];
     }
   }
 }
@@ -1077,16 +1077,19 @@ cudaError_t launch_decode_greedy(const DecodeArgs& a, cudaStream_t s) {
 namespace {
 // ---------------------------------------------------------------------------
 // Warp-specialised exact beam kernel.  The CTA's streams are split into two
-// halves with their own h/logits tiles.  Warps 0-11 (GEMM group) run the
-// exact joiner for half 0 then half 1 of each frame; warps 12-15 (POST
-// group) reduce the rows, step the beams and build the next frame's rows and
-// h tile of one half while the GEMM group computes the other half, so the
-// non-GEMM phases hide behind the dense contraction.  Hand-offs are named
-// barriers (bar.arrive by the producer group, bar.sync by the consumer):
+// halves with their own h/logits tiles.  Warps 0-11 (GEMM group) run only
+// the exact joiner contraction, half 0 then half 1 of each frame; warps
+// 12-15 (POST group, one per SM sub-partition) reduce the rows, step the
+// beams and build the next frame's rows and h tile (gather + tanhf) of one
+// half while the GEMM group computes the other half, so the latency-bound
+// phases hide behind the FMUL/FADD stream.  Hand-offs are named barriers
+// (bar.arrive by the producer group, bar.sync by the consumer):
 //   1+h  h tile of half h ready      (POST -> GEMM)
 //   3+h  logits of half h ready      (GEMM -> POST)
-//   5    GEMM group stage hand-off, 6 POST group internal.
-// Arithmetic and decisions are identical to beam_kernel.
+//   5    GEMM group chunk hand-off, 6 POST group internal.
+// The GEMM is the SMSP-balanced tiling of gemm_pass_bal over the 12 GEMM
+// warps (<= 16 rows per half: at most 12 items).  Arithmetic and decisions
+// are identical to beam_kernel.
 // ---------------------------------------------------------------------------
 constexpr int kWsGemmWarps = 12;
 constexpr int kWsPostWarps = 4;
@@ -1105,6 +1108,8 @@ struct WsHalf {
 };
 
 struct WsSmem {
+  unsigned long long stat[16];
+  WPipe pipe;
   uint64_t bar[2];
   uint32_t wcur[2];
   WsHalf half[2];
@@ -1114,8 +1119,73 @@ __device__ __forceinline__ int ws_hl_floats(const ModelView& m) {
   return max(m.J * kWsHStride, kWsHalfRows * m.Vp);
 }
 
+// Balanced exact GEMM for the 12-warp GEMM group (gemm_pass_bal's items;
+// chunk hand-off on named barrier 5; the last GEMM warp refills).
+__device__ __forceinline__ void ws_gemm(const ModelView& m, const WPipe& p, uint32_t& g, float* HL,
+                                        int R) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int full = R >> 2, rem = R & 3;
+  if (rem != 0 && 2 * (full & ~1) + 4 * (full & 1) + 4 > kWsGemmWarps) {
+    ++full;
+    rem = 0;
+  }
+  const int heavy = 2 * (full & ~1);
+  const int lfull = (full & 1) ? 4 : 0;
+  int tn = 0, nr = 4, rg = 0, cbase = 0;
+  if (warp < heavy) {
+    tn = 8;
+    rg = warp >> 1;
+    cbase = (warp & 1) * 256;
+  } else if (warp < heavy + lfull) {
+    tn = 4;
+    rg = full - 1;
+    cbase = (warp - heavy) * 128;
+  } else if (rem != 0 && warp < heavy + lfull + 4) {
+    tn = 4;
+    nr = rem;
+    rg = full;
+    cbase = (warp - heavy - lfull) * 128;
+  }
+  int col[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) col[j] = cbase + (j < 4 ? lane * 4 + j : 128 + lane * 4 + (j - 4));
+  float acc[4][8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float b = (tn == 8 || (tn == 4 && j < 4)) ? m.out_b[col[j]] : 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][j] = b;
+  }
+  for (int32_t c = 0; c < p.nc; ++c, ++g) {
+    const uint32_t st = g & 1u;
+    if (tn != 0 || warp == 0) mbar_wait(p.bar + st, (g >> 1) & 1u);
+    const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(p.bk * m.Vp * 4);
+    const int kk_end = min(p.bk, m.J - c * p.bk);
+    const float* hp = HL + static_cast<int64_t>(c * p.bk) * kWsHStride + rg * 4;
+    if (tn == 8) gemm_chunk<8, 4, kWsHStride>(m, ws, hp, kk_end, col, acc);
+    else if (tn == 4 && nr == 4) gemm_chunk<4, 4, kWsHStride>(m, ws, hp, kk_end, col, acc);
+    else if (tn == 4 && nr == 3) gemm_chunk<4, 3, kWsHStride>(m, ws, hp, kk_end, col, acc);
+    else if (tn == 4 && nr == 2) gemm_chunk<4, 2, kWsHStride>(m, ws, hp, kk_end, col, acc);
+    else if (tn == 4) gemm_chunk<4, 1, kWsHStride>(m, ws, hp, kk_end, col, acc);
+    nbar_sync(5, kWsGemmWarps * 32);  // the GEMM group is done with this stage (and with h)
+    if (threadIdx.x == (kWsGemmWarps - 1) * 32) wpipe_issue(p, m, g + 2);
+  }
+  if (tn != 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = rg * 4 + i;
+      if (r < R) {
+        float* lr = HL + static_cast<int64_t>(r) * m.Vp;
+        *reinterpret_cast<float4*>(lr + col[0]) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        if (tn == 8)
+          *reinterpret_cast<float4*>(lr + col[4]) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+      }
+    }
+  }
+}
+
 template <int BCAP>
-__global__ void __launch_bounds__(kDecodeThreads, 1)
+__global__ void __launch_bounds__(kWsThreads, 1)
     beam_ws_kernel(ModelView m, const float* __restrict__ pe,
                    const int32_t* __restrict__ frame_splits, int32_t B, int32_t G, int32_t beam,
                    int32_t merge_log, int32_t length_norm, int32_t max_total,
@@ -1127,8 +1197,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   float* HL0 = reinterpret_cast<float*>(smem_raw);
   float* HL1 = HL0 + hl;
   float* W0 = HL1 + hl;
-  float* W1 = W0 + kBKSmall * m.Vp;
-  WsSmem& S = *reinterpret_cast<WsSmem*>(W1 + kBKSmall * m.Vp);
+  float* W1 = W0 + kBK * m.Vp;
+  WsSmem& S = *reinterpret_cast<WsSmem*>(W1 + kBK * m.Vp);
   Hyps* H = reinterpret_cast<Hyps*>(&S + 1);         // [G]
   BeamCand* C = reinterpret_cast<BeamCand*>(H + G);  // [G][BCAP*BCAP + 2*BCAP]
   constexpr int kCandPerStream = BCAP * BCAP + 2 * BCAP;
@@ -1138,10 +1208,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int ns = min(G, B - s0);
   if (ns <= 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WPipe pipe = make_wpipe(W0, W1, S.bar, S.wcur, m, kBKSmall);
+  const WPipe& pipe = S.pipe;
   const int nA = (ns + 1) >> 1;
-  const int hfirst[2] = {0, nA}, hcount[2] = {nA, ns - nA};
-  float* const HLh[2] = {HL0, HL1};
 
   int32_t tmax = 0;
   for (int i = 0; i < ns; ++i) tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
@@ -1156,16 +1224,17 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     h.h2[0] = 0x13198a2e03707344ull;
     h.p1[0] = h.p2[0] = 0;
   }
+  if (threadIdx.x < 16) S.stat[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
+    S.pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  unsigned long long ties = 0, rows_total = 0;
 
   if (warp < kWsGemmWarps) {
-    // ---- GEMM group ----
+    // ---- GEMM group: nothing but the joiner contraction ----
     if (threadIdx.x == 0) {
       wpipe_issue(pipe, m, 0);
       wpipe_issue(pipe, m, 1);
@@ -1173,57 +1242,62 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     uint32_t g = 0;
     for (int32_t t = 0; t < tmax; ++t)
       for (int hh = 0; hh < 2; ++hh) {
-        nbar_sync(1 + hh, kAll);  // rows of half hh ready (POST group)
-        WsHalf& X = S.half[hh];
-        const int R = X.nrows;
-        build_h_g(m, pe, X.row_pe, X.row_ctx, R, HLh[hh], kWsHStride, threadIdx.x, kWsGemmWarps * 32);
-        nbar_sync(5, kWsGemmWarps * 32);
-        if (R > 0) joiner_gemm_g(m, pipe, g, HLh[hh], kWsHStride, R, kWsGemmWarps, warp, 5);
-        nbar_arrive(3 + hh, kAll);
+        nbar_sync(1 + hh, kAll);  // h tile of half hh ready (POST group)
+        const int R = S.half[hh].nrows;
+        if (R > 0) ws_gemm(m, pipe, g, hh ? HL1 : HL0, R);
+        nbar_arrive(3 + hh, kAll);  // logits of half hh ready
       }
     if (threadIdx.x == 0) {
       mbar_wait(&S.bar[g & 1u], (g >> 1) & 1u);
       mbar_wait(&S.bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);
     }
   } else {
-    // ---- POST group ----
+    // ---- POST group: rows, h tile, row reduction, beam step ----
     const int pw = warp - kWsGemmWarps, ptid = threadIdx.x - kWsGemmWarps * 32;
     constexpr int kPost = kWsPostWarps * 32;
-    auto prepare = [&](int hh, int t) {  // joiner rows of half hh for frame t
-      WsHalf& X = S.half[hh];
-      if (pw == 0) {
-        const int R = beam_rows(H + hfirst[hh], hcount[hh], frame_splits + s0 + hfirst[hh], t,
-                                X.row_pe, X.row_ctx);
-        if (lane == 0) {
-          X.nrows = R;
-          rows_total += R;
-        }
-      }
-      nbar_arrive(1 + hh, kAll);
-    };
-    prepare(0, 0);
-    prepare(1, 0);
-    for (int32_t t = 0; t < tmax; ++t)
+    for (int32_t t = -1; t < tmax; ++t)
       for (int hh = 0; hh < 2; ++hh) {
-        nbar_sync(3 + hh, kAll);
+        const int first = hh ? nA : 0, count = hh ? ns - nA : nA;
         WsHalf& X = S.half[hh];
-        const int R = X.nrows;
-        const RowRes rr{X.row_lse, X.row_l0, X.row_tl, X.row_tk};
-        for (int r = pw; r < R; r += kWsPostWarps)
-          beam_row_reduce<BCAP>(HLh[hh] + static_cast<int64_t>(r) * m.Vp, m.V, beam, r, rr);
-        nbar_sync(6, kPost);
-        for (int k = pw; k < hcount[hh]; k += kWsPostWarps) {
-          const int i = hfirst[hh] + k;
-          const int32_t fs = frame_splits[s0 + i];
-          const int32_t T = frame_splits[s0 + i + 1] - fs;
-          if (t >= T) continue;
-          beam_stream_step<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
-                                 backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs,
-                                 beam, merge_log, length_norm, max_total, rr, tokens,
-                                 lengths + s0 + i, scores + s0 + i, &ties);
+        float* HLh = hh ? HL1 : HL0;
+        if (t >= 0) {
+          nbar_sync(3 + hh, kAll);  // logits of half hh (frame t)
+          const int R = X.nrows;
+          const RowRes rr{X.row_lse, X.row_l0, X.row_tl, X.row_tk};
+          // rows pw, pw + 4, pw + 8, pw + 12 of this warp, chains interleaved
+          if (R > 8) {
+            if (pw < R) beam_row_reduce_n<BCAP, 4>(HLh, m.Vp, m.V, beam, pw, R, rr, kWsPostWarps);
+          } else if (R > 4) {
+            if (pw < R) beam_row_reduce_n<BCAP, 2>(HLh, m.Vp, m.V, beam, pw, R, rr, kWsPostWarps);
+          } else if (pw < R) {
+            beam_row_reduce_n<BCAP, 1>(HLh, m.Vp, m.V, beam, pw, R, rr, kWsPostWarps);
+          }
+          nbar_sync(6, kPost);
+          for (int k = pw; k < count; k += kWsPostWarps) {
+            const int i = first + k;
+            const int32_t fs = frame_splits[s0 + i];
+            const int32_t T = frame_splits[s0 + i + 1] - fs;
+            if (t >= T) continue;
+            beam_stream_step<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
+                                   backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs,
+                                   beam, merge_log, length_norm, max_total, rr, tokens,
+                                   lengths + s0 + i, scores + s0 + i, &S.stat[4]);
+          }
+          nbar_sync(6, kPost);  // hypotheses of half hh stepped, its logits consumed
         }
-        nbar_sync(6, kPost);
-        if (t + 1 < tmax) prepare(hh, t + 1);
+        if (t + 1 < tmax) {  // rows + h tile of half hh for frame t + 1
+          if (pw == 0) {
+            const int R = beam_rows(H + first, count, frame_splits + s0 + first, t + 1, X.row_pe, X.row_ctx);
+            if (lane == 0) {
+              X.nrows = R;
+              S.stat[1] += R;
+            }
+          }
+          nbar_sync(6, kPost);
+          build_h_g(m, pe, X.row_pe, X.row_ctx, X.nrows, HLh, kWsHStride, ptid, kPost);
+          nbar_arrive(1 + hh, kAll);  // each POST thread releases its h writes
+        }
+
       }
   }
   __syncthreads();
@@ -1232,8 +1306,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       lengths[s0 + i] = 0;
       scores[s0 + i] = 0.0;
     }
-  atomicAdd(&counters[4], ties);
-  if (threadIdx.x == kWsGemmWarps * 32) atomicAdd(&counters[1], rows_total);
+  if (threadIdx.x < 16 && threadIdx.x != 0 && S.stat[threadIdx.x] != 0)
+    atomicAdd(&counters[threadIdx.x], S.stat[threadIdx.x]);
   if (threadIdx.x == 0) {
     unsigned long long sf = 0;
     for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
@@ -1246,7 +1320,7 @@ cudaError_t launch_beam_ws(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);
   const int G = a.streams_per_cta;
   const size_t hl = static_cast<size_t>(std::max(m.J * kWsHStride, kWsHalfRows * m.Vp)) * 4;
-  const size_t smem = 2 * hl + static_cast<size_t>(2) * kBKSmall * m.Vp * 4 + sizeof(WsSmem) +
+  const size_t smem = 2 * hl + static_cast<size_t>(2) * kBK * m.Vp * 4 + sizeof(WsSmem) +
                       sizeof(Hyps) * G + sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
   cudaError_t e = cudaFuncSetAttribute(beam_ws_kernel<BCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));

@@ -232,12 +232,12 @@ __device__ __forceinline__ void gemm_pass(const ModelView& m, const WPipe& p,
 
 // One out_w chunk of a work item: NR <= 4 rows x 32*TN columns (lane
 // columns col[0..TN)), accumulated into acc[0..NR)[0..TN).
-template <int TN, int NR>
+template <int TN, int NR, int HS = kHStride>
 __device__ __forceinline__ void gemm_chunk(const ModelView& m, uint32_t ws, const float* hp, int kk_end,
                                            const int* col, float (&acc)[4][8]) {
 #pragma unroll 4
   for (int kk = 0; kk < kk_end; ++kk) {
-    const float4 h4 = *reinterpret_cast<const float4*>(hp + kk * kHStride);
+    const float4 h4 = *reinterpret_cast<const float4*>(hp + kk * HS);
     const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
     float wv[TN];
     const uint32_t wr = ws + static_cast<uint32_t>(kk * m.Vp) * 4u;

@@ -34,6 +34,6 @@ print(json.dumps(dict(B=B, T=T, decode_ms=out, gpu_ms=st["gpu_ms"], fps_decode=B
                       fused_pe_share=[round(x / tot, 4) for x in st["fused_pe_cycles"]],
                       padded_per_row=st["joiner_rows_computed"] / max(1, st["joiner_rows"]),
                       gemm_mac_per_s_per_sm=st["joiner_rows_computed"] * 512 * 512 /
-                      (st["phase_cycles"][1] / 1.965e9),
+                      max(1e-9, st["phase_cycles"][1] / 1.965e9),
                       phase_share=[round(x / tot, 3) for x in ph],
                       tokens=int(osp[-1]), checksum=float(osc.sum()))))
