@@ -69,6 +69,16 @@ int main() {
       std::printf("lattice mismatch %zu\n", i);
       ++bad;
     }
+    // Log-add best sequence: the reference's own
+    // lattice_to_best_seq(kLogAdd) — n-best sampling, blank-strip dedup,
+    // per-sequence totals — on the GPU lattice, as the CLI calls it
+    // (rnnt_main.cpp:302: nbest 100, the run seed).
+    for (uint64_t seed : {0ull, 7ull})
+      if (lattice_to_best_seq(a, MergeOp::kLogAdd, 100, seed) !=
+          lattice_to_best_seq(b, MergeOp::kLogAdd, 100, seed)) {
+        std::printf("log-add mismatch %zu seed %llu\n", i, static_cast<unsigned long long>(seed));
+        ++bad;
+      }
   }
   try {
     gpu::greedy_search_batch(ctx, m, batch, 2);
