@@ -832,10 +832,14 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   unsigned long long* st = S.stat;
   long long* pst = reinterpret_cast<long long*>(S.stat);
 
-  for (int32_t t = 0; t < tmax; ++t) {
-    if constexpr (FPE) {
-      if (t % F == 0) fused_pe_pass(m, fp, pipe, g, HL, S, frame_splits, s0, ns, t, F, pst + 12);
-    }
+  // Frame blocks of F frames: the fused encoder projection runs once per
+  // block, outside the per-frame loop (keeps that loop's register allocation
+  // identical to the unfused kernel's).
+  const int32_t TB = FPE ? F : max(1, tmax);
+  for (int32_t tb = 0; tb < tmax; tb += TB) {
+  if constexpr (FPE) fused_pe_pass(m, fp, pipe, g, HL, S, frame_splits, s0, ns, tb, F, pst + 12);
+  const int32_t te = min(tb + TB, tmax);
+  for (int32_t t = tb; t < te; ++t) {
     // A. rows: distinct contexts per live stream (lane = stream, G <= 32).
     if (warp == 0) {
       const int R0 = beam_rows(H, ns, frame_splits + s0, t, S.row_pe, S.row_ctx);
@@ -893,6 +897,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       pst[10] += c3 - c2;
       pst[11] += c4 - c3;
     }
+  }
   }
   // Zero-frame streams: empty result, score 0.
   for (int i = threadIdx.x; i < ns; i += kDecodeThreads)
