@@ -52,6 +52,7 @@ struct LatArc {  // one lattice arc
 };
 
 struct FsaStream {
+  unsigned long long raw_total, lat_total;  // counters (group thread 0)
   int32_t n_act, num_nodes, nrows, row_base;
   int32_t n_raw, n_hot, n_sort, n_surv;
   int32_t bstar, arc_count, arc_off, flag;
@@ -76,6 +77,9 @@ struct FsaStream {
 };
 
 struct FsaSmem {
+  WPipe pipe;                    // in smem: no registers pinned across the frame loop
+  unsigned long long rows_total;
+  long long ph[3];               // thread 0: h build, joiner GEMM, lse + expand/prune
   uint64_t bar[2];
   uint32_t wcur[2];
   int64_t row_pe[kRowCap];
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int s0 = blockIdx.x * G;
   const int ns = min(G, B - s0);
   if (ns <= 0) return;
-  WPipe pipe = make_wpipe(W0, W1, C.bar, C.wcur, m, kBKSmall);
+  const WPipe& pipe = C.pipe;
   const int nt = kDecodeThreads / G;
   const Group grp{static_cast<int>(threadIdx.x) / nt, static_cast<int>(threadIdx.x) % nt, nt};
   const bool have = grp.id < ns;
@@ -289,18 +293,20 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     S.flag = 0;
   }
   if (threadIdx.x == 0) {
+    C.pipe = make_wpipe(W0, W1, C.bar, C.wcur, m, kBKSmall);
+    C.rows_total = 0;
+    C.ph[0] = C.ph[1] = C.ph[2] = 0;
     mbar_init(&C.bar[0], 1);
     mbar_init(&C.bar[1], 1);
     fence_mbar_init();
   }
+  if (have && grp.tid == 0) S.raw_total = S.lat_total = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
     wpipe_issue(pipe, m, 0);
     wpipe_issue(pipe, m, 1);
   }
   uint32_t gch = 0;
-  unsigned long long rows_total = 0, raw_total = 0, lat_total = 0;
-  long long ph[3] = {0, 0, 0};  // thread 0: h build, joiner GEMM, lse + expand/prune
 
   for (int32_t t = 0; t < tmax; ++t) {
     const bool live = have && t < T;
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     }
     __syncthreads();
     const int R = C.nrows;
-    rows_total += R;
+    if (threadIdx.x == 0) C.rows_total += R;
     const long long c0 = clock64();
     build_h(m, pe, C.row_pe, C.row_ctx, R, HL);
     const long long c1 = clock64();
@@ -390,7 +396,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       grp.sync();
       const int nraw = min(S.n_raw, kMaxRaw);
       const double ub = S.ub;
-      raw_total += (grp.tid == 0) ? nraw : 0;
+      if (grp.tid == 0) S.raw_total += nraw;
       // Pass A: the stream's best candidate and a histogram below `ub`.
       double mx = -INFINITY;
       for (int q0 = grp.tid; q0 < nraw; q0 += kU * nt) {
@@ -596,7 +602,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       }
       grp.sync();
       const int arc_off = S.arc_off;
-      lat_total += grp.tid == 0 ? total : 0;
+      if (grp.tid == 0) S.lat_total += total;
       // Pass D: only the (few) hits are recomputed and written.
       if (arc_off >= 0) {
         int pos = my_pos;
@@ -639,9 +645,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     __syncthreads();
     if (threadIdx.x == 0) {
       const long long c4 = clock64();
-      ph[0] += c1 - c0;
-      ph[1] += c2 - c1;
-      ph[2] += c4 - c2;
+      C.ph[0] += c1 - c0;
+      C.ph[1] += c2 - c1;
+      C.ph[2] += c4 - c2;
     }
   }
 
@@ -699,19 +705,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   }
   if (grp.tid == 0 && have) atomicAdd(&counters[11], static_cast<unsigned long long>(clock64() - cb0));
   if (threadIdx.x == 0) {
-    atomicAdd(&counters[8], static_cast<unsigned long long>(ph[0]));
-    atomicAdd(&counters[9], static_cast<unsigned long long>(ph[1]));
-    atomicAdd(&counters[10], static_cast<unsigned long long>(ph[2]));
+    atomicAdd(&counters[8], static_cast<unsigned long long>(C.ph[0]));
+    atomicAdd(&counters[9], static_cast<unsigned long long>(C.ph[1]));
+    atomicAdd(&counters[10], static_cast<unsigned long long>(C.ph[2]));
     mbar_wait(&C.bar[gch & 1u], (gch >> 1) & 1u);
     mbar_wait(&C.bar[(gch + 1) & 1u], ((gch + 1) >> 1) & 1u);
     unsigned long long sf = 0;
     for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
     atomicAdd(&counters[0], sf);
-    atomicAdd(&counters[1], rows_total);
+    atomicAdd(&counters[1], C.rows_total);
   }
   if (have && grp.tid == 0) {
-    atomicAdd(&counters[2], raw_total);
-    atomicAdd(&counters[3], lat_total);
+    atomicAdd(&counters[2], S.raw_total);
+    atomicAdd(&counters[3], S.lat_total);
   }
 }
 
