@@ -246,7 +246,7 @@ __device__ __forceinline__ int ub_bin(double ub, double score, double scale) {
 
 __global__ void __launch_bounds__(kDecodeThreads, 1)
     fsa_kernel(ModelView m, const float* __restrict__ pe, const int32_t* __restrict__ frame_splits,
-               int32_t B, int32_t G, const ArcRec* __restrict__ arcs,
+               int32_t B, int32_t G, int32_t bk, const ArcRec* __restrict__ arcs,
                const int32_t* __restrict__ gsplits, const double* __restrict__ gmaxw,
                double beam, int32_t max_states,
                int32_t max_contexts, LatArc* __restrict__ lat, int64_t lat_cap,
@@ -258,8 +258,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   float* HL = reinterpret_cast<float*>(smem_raw);
   const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
   float* W0 = HL + hl_floats;
-  float* W1 = W0 + kBKSmall * m.Vp;
-  FsaSmem& C = *reinterpret_cast<FsaSmem*>(W1 + kBKSmall * m.Vp);
+  float* W1 = W0 + bk * m.Vp;
+  FsaSmem& C = *reinterpret_cast<FsaSmem*>(W1 + bk * m.Vp);
   FsaStream* SS = reinterpret_cast<FsaStream*>(&C + 1);
 
   const int s0 = blockIdx.x * G;
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     S.flag = 0;
   }
   if (threadIdx.x == 0) {
-    C.pipe = make_wpipe(W0, W1, C.bar, C.wcur, m, kBKSmall);
+    C.pipe = make_wpipe(W0, W1, C.bar, C.wcur, m, bk);
     C.rows_total = 0;
     C.ph[0] = C.ph[1] = C.ph[2] = 0;
     mbar_init(&C.bar[0], 1);
@@ -728,13 +728,19 @@ size_t fsa_stream_smem() { return sizeof(FsaStream); }
 cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);
   const int G = a.streams_per_cta;
-  const size_t smem = smem_common(m, kBKSmall) + sizeof(FsaSmem) + sizeof(FsaStream) * G;
+  // 32-row weight chunks when they fit beside G stream states, else 16.
+  int max_smem = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t rest = sizeof(FsaSmem) + sizeof(FsaStream) * G;
+  const int bk = smem_common(m, kBK) + rest <= static_cast<size_t>(max_smem) ? kBK : kBKSmall;
+  const size_t smem = smem_common(m, bk) + rest;
   cudaError_t e = cudaFuncSetAttribute(fsa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int grid = (a.B + G - 1) / G;
   fsa_kernel<<<grid, kDecodeThreads, smem, s>>>(
-      m, a.pe, a.frame_splits, a.B, G, static_cast<const ArcRec*>(a.graph_arcs), a.graph_splits,
+      m, a.pe, a.frame_splits, a.B, G, bk, static_cast<const ArcRec*>(a.graph_arcs), a.graph_splits,
       a.graph_maxw, a.fsa_beam, a.max_states, a.max_contexts, static_cast<LatArc*>(a.lattice), a.lattice_cap,
       a.lattice_count, reinterpret_cast<int4*>(a.lat_frame_info), a.node_best, a.tokens, a.lengths,
       a.scores, a.counters, a.error_flag);
