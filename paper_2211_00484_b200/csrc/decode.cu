@@ -541,17 +541,25 @@ __device__ void beam_stream_step(const ModelView& m, Hyps& h, BeamCand* cand, ui
   // merge_into (search.hpp:180-187): an extension ys_g+k equals the blank
   // continuation of hypothesis j iff |ys_j| = |ys_g|+1, last(ys_j) = k and
   // prefix(ys_j) = ys_g.
+  // Each blank continuation j can equal at most one extension (extensions
+  // are distinct sequences, and two extensions never merge with each other:
+  // the reference compares them with the existing entries only), so lane q
+  // merges extension q on its own; misses are appended in q order.
   int nm = nh;
-  if (lane == 0) {
-    for (int q = 0; q < nsel; ++q) {
-      const BeamCand& e = cand[q];
-      int hit = -1;
+  {
+    int hit = -1;
+    BeamCand e;
+    if (lane < nsel) {
+      e = cand[lane];
       for (int j = 0; j < nh; ++j)
         if (merged[j].last == e.tok && merged[j].len == e.len && merged[j].p1 == e.p1 &&
             merged[j].p2 == e.p2) {
           hit = j;
           break;
         }
+    }
+    const unsigned miss = __ballot_sync(0xffffffffu, lane < nsel && hit < 0);
+    if (lane < nsel) {
       if (hit >= 0) {
         double& sc = merged[hit].score;
         if (merge_log) {  // log_add, common.hpp:48-54
@@ -566,11 +574,11 @@ __device__ void beam_stream_step(const ModelView& m, Hyps& h, BeamCand* cand, ui
           sc = sc > e.score ? sc : e.score;
         }
       } else {
-        merged[nm++] = e;
+        merged[nh + __popc(miss & ((1u << lane) - 1u))] = e;
       }
     }
+    nm = nh + __popc(miss);
   }
-  nm = __shfl_sync(0xffffffffu, nm, 0);
   __syncwarp();
   // prune_to_beam of the frame set by hyp_better.
   int myrank = 0x7fffffff;
@@ -858,6 +866,17 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       build_h(m, pe, S.row_pe, S.row_ctx, R, HL, pst + 2);
     long long c1 = clock64();
     if (threadIdx.x == 0) pst[6] += pst[2] - c0;
+    // Next frame's encoder projections into L2 while the GEMM runs (each
+    // stream's pe row is 2 KB of HBM read once; the h build then hits L2).
+    if constexpr (!FPE) {
+      const int lines = (m.J * 4 + 127) >> 7;
+      for (int x = threadIdx.x; x < ns * lines; x += kDecodeThreads) {
+        const int i = x / lines, l = x - i * lines;
+        const int32_t f = frame_splits[s0 + i];
+        if (t + 1 < frame_splits[s0 + i + 1] - f)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pe + static_cast<int64_t>(f + t + 1) * m.J + l * 32));
+      }
+    }
     if constexpr (TC)
       tc_gemm(m, tp, g, static_cast<uint32_t>(t), HL, R);
     else
