@@ -113,6 +113,29 @@ inline std::vector<std::vector<int32_t>> greedy_search_batch(
   return detail::unpack(splits, toks);
 }
 
+// greedy_search (search.hpp:76-100) with the reference's signature, any S
+// (kNoSymbolLimit = unlimited, 10 per frame at most), and its batched form.
+inline std::vector<std::vector<int32_t>> greedy_search_batched(
+    Context& ctx, const ToyTransducer& m, const std::vector<Mat<float>>& batch,
+    int32_t max_symbols, int64_t* capped_frames = nullptr) {
+  if (max_symbols < 1) throw ValidationError("max_symbols must be >= 1");
+  detail::Frames f = detail::encode(m, batch);
+  const int32_t B = static_cast<int32_t>(batch.size());
+  const int64_t cap = max_symbols == kNoSymbolLimit ? kMaxSymbolsPerFrameSafety : max_symbols;
+  std::vector<int32_t> splits(B + 1), toks(std::max<int64_t>(1, f.splits.back() * cap));
+  int64_t capped = 0;
+  check(rnntg_greedy_search(ctx.handle(), f.enc.data(), f.splits.data(), B, max_symbols,
+                            RNNTG_MEM_HOST, splits.data(), toks.data(), &capped));
+  if (capped_frames) *capped_frames = capped;
+  return detail::unpack(splits, toks);
+}
+
+inline std::vector<int32_t> greedy_search(Context& ctx, const ToyTransducer& m,
+                                          const Mat<float>& features, int32_t max_symbols,
+                                          int64_t* capped_frames = nullptr) {
+  return greedy_search_batched(ctx, m, {features}, max_symbols, capped_frames)[0];
+}
+
 inline std::vector<std::vector<int32_t>> beam_search_batch(
     Context& ctx, const ToyTransducer& m, const std::vector<Mat<float>>& batch,
     const SearchParams& params, std::vector<double>* scores = nullptr) {

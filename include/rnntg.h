@@ -11,6 +11,8 @@
  *                                  (model.hpp:61-90, 129-169; weights in
  *                                  param_views naming, model.hpp:75-82)
  *   rnntg_greedy_search_batch   <- greedy_search_batch   (search.hpp:107-167)
+ *   rnntg_greedy_search         <- greedy_search, any S  (search.hpp:76-100),
+ *                                  batched over utterances
  *   rnntg_beam_search_batch     <- beam_search, S = 1    (search.hpp:206-277),
  *                                  batched over utterances like the CLI's
  *                                  parallel_for (tools/rnnt_main.cpp:274-287)
@@ -122,6 +124,8 @@ typedef struct {
                              pe / pd rows (thread 0, summed over CTAs) */
   int64_t gemm_wait_cycles; /* beam kernel: joiner GEMM cycles thread 0 waited
                                for weight chunks (pipeline starvation) */
+  int64_t capped_frames;  /* greedy_search with S unlimited: frames stopped by
+                             the 10-symbol safety cap (search.hpp:31-34) */
   int64_t fused_pe_cycles[4]; /* beam kernel, fused encoder projection (thread 0,
                                  summed over CTAs): row list + slice wait, frame
                                  staging, GEMM, pe write-back */
@@ -154,6 +158,19 @@ rnntg_status rnntg_greedy_search_batch(rnntg_model_t model, const float* enc,
                                        int32_t max_symbols, int32_t mem,
                                        int32_t* out_splits,
                                        int32_t* out_tokens);
+
+/* greedy_search (search.hpp:76-100) for every stream of the batch: up to
+ * max_symbols emissions per frame (RNNTG_NO_SYMBOL_LIMIT = unlimited, capped
+ * at 10 per frame as the reference's kMaxSymbolsPerFrameSafety; the frames
+ * that hit that cap are counted in *capped_frames, may be NULL).
+ * out_tokens must hold frame_splits[B] * cap int32, cap = max_symbols, or 10
+ * when unlimited. */
+#define RNNTG_NO_SYMBOL_LIMIT 2147483647
+rnntg_status rnntg_greedy_search(rnntg_model_t model, const float* enc,
+                                 const int32_t* frame_splits, int32_t B,
+                                 int32_t max_symbols, int32_t mem,
+                                 int32_t* out_splits, int32_t* out_tokens,
+                                 int64_t* capped_frames);
 
 rnntg_status rnntg_beam_search_batch(rnntg_model_t model, const float* enc,
                                      const int32_t* frame_splits, int32_t B,

@@ -318,6 +318,7 @@ class Reference:
         L.ref_joiner_logits.argtypes = [C.c_void_p, _f32p, _i32p, C.c_int32, _f32p]
         L.ref_log_softmax.argtypes = [_f32p, C.c_int32, _f64p]
         L.ref_greedy_search_batch.argtypes = [C.c_void_p, _f32p, _i32p, C.c_int32, C.c_int32, C.c_int, _i32p, _i32p]
+        L.ref_greedy_search.argtypes = [C.c_void_p, _f32p, _i32p, C.c_int32, C.c_int32, C.c_int, _i32p, _i32p, C.POINTER(C.c_int64)]
         L.ref_beam_search_batch.argtypes = [C.c_void_p, _f32p, _i32p, C.c_int32] + [C.c_int32] * 5 + [
             C.c_int,
             _i32p,
@@ -503,6 +504,23 @@ class RefModel:
             )
         )
         return unragged(osp, otk)
+
+    def greedy_multi(self, feats, splits, max_symbols, threads=8):
+        """Reference greedy_search (any S) per utterance: (token lists, capped frames)."""
+        feats = np.ascontiguousarray(feats, np.float32)
+        splits = np.ascontiguousarray(splits, np.int32)
+        B = len(splits) - 1
+        cap = 10 if max_symbols == 2147483647 else max_symbols
+        osp = np.zeros(B + 1, np.int32)
+        otk = np.zeros(max(1, int(splits[-1]) * cap), np.int32)
+        capped = C.c_int64(0)
+        self.ref._check(
+            self.ref.lib.ref_greedy_search(
+                self.h, _p(feats, _f32p), _p(splits, _i32p), B, max_symbols, threads, _p(osp, _i32p),
+                _p(otk, _i32p), C.byref(capped)
+            )
+        )
+        return unragged(osp, otk), int(capped.value)
 
     def beam(self, feats, splits, beam=4, merge_op=0, length_norm=0, max_total=0, threads=8, max_symbols=1):
         feats = np.ascontiguousarray(feats, np.float32)

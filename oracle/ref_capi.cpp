@@ -234,6 +234,30 @@ int ref_greedy_search_batch(void* mp, const float* feats,
   }
 }
 
+// greedy_search (search.hpp:76-100, any S) per utterance under parallel_for;
+// capped_frames summed over utterances.
+int ref_greedy_search(void* mp, const float* feats, const int32_t* splits, int32_t B,
+                      int32_t max_symbols, int threads, int32_t* out_splits,
+                      int32_t* out_tokens, int64_t* capped_frames) {
+  try {
+    auto* m = static_cast<rnnt::ToyTransducer*>(mp);
+    auto batch = split_frames(feats, splits, B, m->cfg.feat_dim);
+    std::vector<std::vector<int32_t>> ys(B);
+    std::vector<int64_t> capped(B, 0);
+    parallel_for(B, std::max(1, threads), [&](int64_t i) {
+      ys[i] = rnnt::greedy_search(*m, batch[i], max_symbols, &capped[i]);
+    });
+    write_ragged(ys, out_splits, out_tokens);
+    if (capped_frames) {
+      *capped_frames = 0;
+      for (int64_t c : capped) *capped_frames += c;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // beam_search per utterance under parallel_for (rnnt_main.cpp:274-287).
 int ref_beam_search_batch(void* mp, const float* feats, const int32_t* splits,
                           int32_t B, int32_t beam_size, int32_t max_symbols,

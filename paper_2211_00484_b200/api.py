@@ -28,6 +28,7 @@ PARAM_NAMES = ("emb", "ctx_w", "ctx_b", "j_we", "j_wd", "j_b", "out_w", "out_b")
 
 OK, INVALID_ARGUMENT, INTERNAL, CUDA_ERROR, UNSUPPORTED = range(5)
 MEM_HOST, MEM_DEVICE = 0, 1
+NO_SYMBOL_LIMIT = 2147483647  # RNNTG_NO_SYMBOL_LIMIT (search.hpp:30 kNoSymbolLimit)
 MERGE_MAX, MERGE_LOG_ADD = 0, 1
 
 
@@ -91,6 +92,7 @@ class _Stats(C.Structure):
         ("joiner_rows_computed", C.c_int64),
         ("gather_cycles", C.c_int64),
         ("gemm_wait_cycles", C.c_int64),
+        ("capped_frames", C.c_int64),
         ("fused_pe_cycles", C.c_int64 * 4),
     ]
 
@@ -115,6 +117,7 @@ def _load():
     lib.rnntg_set_joiner_mode.argtypes = [vp, i32]
     lib.rnntg_get_stats.argtypes = [vp, C.POINTER(_Stats)]
     lib.rnntg_greedy_search_batch.argtypes = [vp, f32p, i32p, i32, i32, i32, i32p, vp]
+    lib.rnntg_greedy_search.argtypes = [vp, f32p, i32p, i32, i32, i32, i32p, vp, C.POINTER(C.c_int64)]
     lib.rnntg_beam_search_batch.argtypes = [vp, f32p, i32p, i32, C.POINTER(_BeamParams), i32, i32p, vp, f64p]
     lib.rnntg_graph_create.argtypes = [vp, i32, i32p, i32, i32p, i32p, f64p, C.POINTER(vp)]
     lib.rnntg_graph_destroy.argtypes = [vp]
@@ -345,6 +348,22 @@ class Decoder:
         if mem == MEM_DEVICE:
             return osp, tok
         return _ragged(osp, tok)
+
+    def greedy_search(self, enc, frame_splits, max_symbols=1):
+        """greedy_search (search.hpp:76-100) for every stream, any S
+        (NO_SYMBOL_LIMIT = unlimited, capped at 10 per frame).  Returns
+        (token lists, frames stopped by the cap)."""
+        p, mem, splits, keep = _frames(enc, frame_splits)
+        B = len(splits) - 1
+        cap = 10 if max_symbols == NO_SYMBOL_LIMIT else max_symbols
+        osp = np.zeros(B + 1, np.int32)
+        tok = np.zeros(max(1, int(splits[-1]) * max(1, cap)), np.int32)
+        capped = C.c_int64(0)
+        if mem == MEM_DEVICE:
+            raise ValueError("greedy_search: host frames only in this binding")
+        _check(self._lib.rnntg_greedy_search(self.h, p, _i32p(splits), B, max_symbols, mem, _i32p(osp), _ptr(tok),
+                                             C.byref(capped)))
+        return _ragged(osp, tok), int(capped.value)
 
     def beam_search_batch(self, enc, frame_splits, params: BeamParams = BeamParams(), out_tokens=None, out_scores=None):
         p, mem, splits, keep = _frames(enc, frame_splits)

@@ -44,6 +44,7 @@ struct rnntg_model_s {
   // profiles/r01), 0 = never.
   int fused_pe = 1;
   Scratch ready;
+  int32_t slot_mult = 1;  // token slots per frame of the current call (greedy S > 1)
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
   Scratch finfo, nodebest, lattice, flag, feat, hid;
   int64_t lat_cap_hint = 0;
@@ -111,7 +112,7 @@ rnntg_status prepare(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem)
   if (mem == RNNTG_MEM_HOST)
     RNNTG_CUDA_TRY(h->enc.ensure(sizeof(float) * std::max<int64_t>(1, total) * D));
   RNNTG_CUDA_TRY(h->pe.ensure(sizeof(float) * std::max<int64_t>(1, total) * J));
-  RNNTG_CUDA_TRY(h->tok.ensure(sizeof(int32_t) * std::max<int64_t>(1, total)));
+  RNNTG_CUDA_TRY(h->tok.ensure(sizeof(int32_t) * std::max<int64_t>(1, total * h->slot_mult)));
   RNNTG_CUDA_TRY(h->len.ensure(sizeof(int32_t) * std::max(1, B)));
   RNNTG_CUDA_TRY(h->score.ensure(sizeof(double) * std::max(1, B)));
   RNNTG_CUDA_TRY(h->counters.ensure(sizeof(unsigned long long) * 16));
@@ -252,11 +253,12 @@ rnntg_status run_pipeline(rnntg_model_t h, const float* enc, const int32_t* fs, 
 __global__ void compact_tokens_kernel(const int32_t* __restrict__ slot_tokens,
                                       const int32_t* __restrict__ fs,
                                       const int32_t* __restrict__ out_splits,
-                                      int32_t B, int32_t* __restrict__ out) {
+                                      int32_t B, int32_t mult, int32_t* __restrict__ out) {
   const int s = blockIdx.x;
   if (s >= B) return;
   const int32_t n = out_splits[s + 1] - out_splits[s];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) out[out_splits[s] + i] = slot_tokens[fs[s] + i];
+  const int64_t base = static_cast<int64_t>(mult) * fs[s];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[out_splits[s] + i] = slot_tokens[base + i];
 }
 
 // Common back half: lengths -> out_splits, tokens compacted to the ragged
@@ -265,7 +267,7 @@ rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
                     int32_t* out_splits, int32_t* out_tokens, double* out_scores,
                     int64_t launches) {
   RNNTG_CUDA_TRY(cudaEventRecord(h->ev[2], h->stream));
-  const int64_t total = B > 0 ? fs[B] : 0;
+  const int64_t total = B > 0 ? static_cast<int64_t>(fs[B]) * h->slot_mult : 0;
   std::vector<int32_t> lens(std::max(1, B));
   if (B > 0)
     RNNTG_CUDA_TRY(cudaMemcpyAsync(lens.data(), h->len.ptr, sizeof(int32_t) * B,
@@ -285,7 +287,8 @@ rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
                                        cudaMemcpyDeviceToHost, h->stream));
       RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
       for (int32_t i = 0; i < B; ++i)
-        std::memcpy(out_tokens + out_splits[i], slots.data() + fs[i], sizeof(int32_t) * lens[i]);
+        std::memcpy(out_tokens + out_splits[i], slots.data() + static_cast<int64_t>(fs[i]) * h->slot_mult,
+                    sizeof(int32_t) * lens[i]);
     } else if (out_scores && B > 0) {
       RNNTG_CUDA_TRY(cudaMemcpy(out_scores, h->score.ptr, sizeof(double) * B, cudaMemcpyDeviceToHost));
     }
@@ -295,7 +298,8 @@ rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
                                    cudaMemcpyHostToDevice, h->stream));
     if (B > 0 && total > 0) {
       compact_tokens_kernel<<<B, 128, 0, h->stream>>>(h->tok.as<int32_t>(), h->splits.as<int32_t>(),
-                                                      h->out_splits.as<int32_t>(), B, out_tokens);
+                                                      h->out_splits.as<int32_t>(), B, h->slot_mult,
+                                                      out_tokens);
       RNNTG_CUDA_TRY(cudaGetLastError());
       ++launches;
     }
@@ -319,6 +323,7 @@ rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
   for (int i = 0; i < 4; ++i) h->stats.phase_cycles[i] = static_cast<int64_t>(cnt[8 + i]);
   h->stats.joiner_rows_computed = static_cast<int64_t>(cnt[5]);
   h->stats.gather_cycles = static_cast<int64_t>(cnt[6]);
+  h->stats.capped_frames = h->slot_mult > 1 ? static_cast<int64_t>(cnt[13]) : 0;
   h->stats.gemm_wait_cycles = static_cast<int64_t>(cnt[7]);
   for (int i = 0; i < 4; ++i) h->stats.fused_pe_cycles[i] = static_cast<int64_t>(cnt[12 + i]);
   h->stats.gpu_ms = ms_all;
@@ -500,20 +505,19 @@ rnntg_status rnntg_get_stats(rnntg_model_t h, rnntg_stats* out) {
   return RNNTG_OK;
 }
 
-rnntg_status rnntg_greedy_search_batch(rnntg_model_t h, const float* enc,
-                                       const int32_t* fs, int32_t B,
-                                       int32_t max_symbols, int32_t mem,
-                                       int32_t* out_splits, int32_t* out_tokens) {
-  if (!h) return invalid("null model");
-  // search.hpp:110-111.
-  if (max_symbols != 1) return invalid("greedy_search_batch supports max_symbols = 1 only");
-  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
-  rnntg_status st = check_frames(enc, fs, B);
-  if (st) return st;
-  if (!out_splits) return invalid("out_splits is null");
-  std::lock_guard<std::mutex> lk(h->mu);
+namespace {
+// Greedy body shared by greedy_search_batch (cap 1) and greedy_search (cap
+// = S, or 10 with the frames stopped by the cap counted when S is
+// unlimited).  Caller holds h->mu and has validated the arguments.
+rnntg_status greedy_impl(rnntg_model_t h, const float* enc, const int32_t* fs, int32_t B, int32_t cap,
+                         bool count_capped, int32_t mem, int32_t* out_splits, int32_t* out_tokens) {
   RNNTG_CUDA_TRY(cudaSetDevice(h->device));
-  if ((st = prepare(h, fs, B, mem))) return st;
+  h->slot_mult = cap;
+  rnntg_status st = prepare(h, fs, B, mem);
+  if (st) {
+    h->slot_mult = 1;
+    return st;
+  }
   int64_t launches = 0;
   if (B > 0) {
     const int G = std::min(32, std::max(1, (B + h->num_sms - 1) / h->num_sms));
@@ -529,11 +533,52 @@ rnntg_status rnntg_greedy_search_batch(rnntg_model_t h, const float* enc,
       a.lengths = h->len.as<int32_t>() + b0;
       a.scores = h->score.as<double>() + b0;
       a.counters = h->counters.as<unsigned long long>();
+      a.symbol_cap = cap;
+      a.count_capped = count_capped ? 1 : 0;
       return rnntg::launch_decode_greedy(a, cs);
     });
-    if (st) return st;
+    if (st) {
+      h->slot_mult = 1;
+      return st;
+    }
   }
-  return finish(h, fs, B, mem, out_splits, out_tokens, nullptr, launches);
+  st = finish(h, fs, B, mem, out_splits, out_tokens, nullptr, launches);
+  h->slot_mult = 1;
+  return st;
+}
+}  // namespace
+
+rnntg_status rnntg_greedy_search_batch(rnntg_model_t h, const float* enc,
+                                       const int32_t* fs, int32_t B,
+                                       int32_t max_symbols, int32_t mem,
+                                       int32_t* out_splits, int32_t* out_tokens) {
+  if (!h) return invalid("null model");
+  // search.hpp:110-111.
+  if (max_symbols != 1) return invalid("greedy_search_batch supports max_symbols = 1 only");
+  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
+  rnntg_status st = check_frames(enc, fs, B);
+  if (st) return st;
+  if (!out_splits) return invalid("out_splits is null");
+  std::lock_guard<std::mutex> lk(h->mu);
+  return greedy_impl(h, enc, fs, B, 1, false, mem, out_splits, out_tokens);
+}
+
+rnntg_status rnntg_greedy_search(rnntg_model_t h, const float* enc, const int32_t* fs, int32_t B,
+                                 int32_t max_symbols, int32_t mem, int32_t* out_splits,
+                                 int32_t* out_tokens, int64_t* capped_frames) {
+  if (!h) return invalid("null model");
+  // search.hpp:80 and 31-34 (kNoSymbolLimit -> kMaxSymbolsPerFrameSafety = 10).
+  if (max_symbols < 1) return invalid("max_symbols must be >= 1");
+  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
+  rnntg_status st = check_frames(enc, fs, B);
+  if (st) return st;
+  if (!out_splits) return invalid("out_splits is null");
+  const bool unlimited = max_symbols == RNNTG_NO_SYMBOL_LIMIT;
+  const int32_t cap = unlimited ? 10 : max_symbols;
+  std::lock_guard<std::mutex> lk(h->mu);
+  st = greedy_impl(h, enc, fs, B, cap, unlimited, mem, out_splits, out_tokens);
+  if (!st && capped_frames) *capped_frames = h->stats.capped_frames;
+  return st;
 }
 
 rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,

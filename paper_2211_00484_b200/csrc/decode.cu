@@ -34,7 +34,12 @@ namespace {
 using namespace dec;
 
 // ---------------------------------------------------------------------------
-// Greedy (search.hpp:107-167, S = 1).
+// Greedy.  cap = 1: greedy_search_batch (search.hpp:107-167, S = 1).  cap > 1:
+// greedy_search (search.hpp:76-100) per stream — on a frame, repeat
+// {joiner, first-max argmax} until blank or `cap` emissions, each emission
+// advancing the context; every sub-step is one GEMM pass over the streams
+// still open on the frame.  Stream i's tokens go to its slot region
+// [cap * frame_splits[i], cap * frame_splits[i+1]).
 // ---------------------------------------------------------------------------
 struct GreedySmem {
   uint64_t bar[2];
@@ -44,13 +49,15 @@ struct GreedySmem {
   int32_t row_stream[kRowCap];
   int32_t ctx[kRowCap];
   int32_t len[kRowCap];
+  int32_t open[kRowCap];
+  int32_t capped;
   int32_t nrows;
 };
 
 __global__ void __launch_bounds__(kDecodeThreads, 1)
     greedy_kernel(ModelView m, const float* __restrict__ pe,
                   const int32_t* __restrict__ frame_splits, int32_t B,
-                  int32_t G, int32_t* __restrict__ tokens,
+                  int32_t G, int32_t cap, int32_t count_capped, int32_t* __restrict__ tokens,
                   int32_t* __restrict__ lengths,
                   unsigned long long* __restrict__ counters) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -73,6 +80,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     S.len[threadIdx.x] = 0;
   }
   if (threadIdx.x == 0) {
+    S.capped = 0;
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
     fence_mbar_init();
@@ -86,50 +94,62 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   unsigned long long rows_total = 0;
 
   for (int32_t t = 0; t < tmax; ++t) {
-    if (threadIdx.x == 0) {  // A. one row per live stream
-      int R = 0;
-      for (int i = 0; i < ns; ++i) {
-        const int32_t fs = frame_splits[s0 + i];
-        if (t < frame_splits[s0 + i + 1] - fs) {
-          S.row_pe[R] = fs + t;
+    if (threadIdx.x < ns) {
+      const int32_t fs = frame_splits[s0 + threadIdx.x];
+      S.open[threadIdx.x] = t < frame_splits[s0 + threadIdx.x + 1] - fs;
+    }
+    for (int32_t n = 0; n < cap; ++n) {
+      __syncthreads();
+      if (threadIdx.x == 0) {  // A. one row per stream still open on the frame
+        int R = 0;
+        for (int i = 0; i < ns; ++i) {
+          if (!S.open[i]) continue;
+          S.row_pe[R] = frame_splits[s0 + i] + t;
           S.row_ctx[R] = S.ctx[i];
           S.row_stream[R] = i;
           ++R;
         }
+        S.nrows = R;
       }
-      S.nrows = R;
-    }
-    __syncthreads();
-    const int R = S.nrows;
-    rows_total += R;
-    build_h(m, pe, S.row_pe, S.row_ctx, R, HL);
-    joiner_gemm(m, pipe, g, HL, R);
-    // D+E. first-max argmax of the raw float logits, append non-blank.
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int r = warp; r < R; r += kWarps) {
-      const float* L = HL + static_cast<int64_t>(r) * m.Vp;
-      float bv = -FLT_MAX;
-      int bk = 0x7fffffff;
-      for (int k = lane; k < m.V; k += 32)
-        if (tok_before(L[k], k, bv, bk)) {
-          bv = L[k];
-          bk = k;
-        }
+      __syncthreads();
+      const int R = S.nrows;
+      if (R == 0) break;  // CTA-uniform
+      rows_total += R;
+      build_h(m, pe, S.row_pe, S.row_ctx, R, HL);
+      joiner_gemm(m, pipe, g, HL, R);
+      // D+E. first-max argmax of the raw float logits (search.hpp:59-66);
+      // blank closes the stream's frame, a token advances its context.
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int r = warp; r < R; r += kWarps) {
+        const float* L = HL + static_cast<int64_t>(r) * m.Vp;
+        float bv = -FLT_MAX;
+        int bk = 0x7fffffff;
+        for (int k = lane; k < m.V; k += 32)
+          if (tok_before(L[k], k, bv, bk)) {
+            bv = L[k];
+            bk = k;
+          }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
-        if (tok_before(ov, ok, bv, bk)) {
-          bv = ov;
-          bk = ok;
+        for (int o = 16; o > 0; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+          if (tok_before(ov, ok, bv, bk)) {
+            bv = ov;
+            bk = ok;
+          }
         }
-      }
-      if (lane == 0 && bk != 0) {
-        const int i = S.row_stream[r];
-        const int32_t len = S.len[i];
-        tokens[frame_splits[s0 + i] + len] = bk;
-        S.len[i] = len + 1;
-        S.ctx[i] = (S.ctx[i] % m.V) * m.V + bk;
+        if (lane == 0) {
+          const int i = S.row_stream[r];
+          if (bk == 0) {
+            S.open[i] = 0;
+          } else {
+            const int32_t len = S.len[i];
+            tokens[static_cast<int64_t>(cap) * frame_splits[s0 + i] + len] = bk;
+            S.len[i] = len + 1;
+            S.ctx[i] = (S.ctx[i] % m.V) * m.V + bk;
+            if (n + 1 == cap && count_capped) atomicAdd(&S.capped, 1);
+          }
+        }
       }
     }
     __syncthreads();
@@ -143,6 +163,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
     atomicAdd(&counters[0], sf);
     atomicAdd(&counters[1], rows_total);
+    if (S.capped) atomicAdd(&counters[13], static_cast<unsigned long long>(S.capped));
   }
 }
 
@@ -1093,8 +1114,8 @@ cudaError_t launch_decode_greedy(const DecodeArgs& a, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   const int grid = (a.B + a.streams_per_cta - 1) / a.streams_per_cta;
   greedy_kernel<<<grid, kDecodeThreads, smem, s>>>(
-      m, a.pe, a.frame_splits, a.B, a.streams_per_cta, a.tokens, a.lengths,
-      a.counters);
+      m, a.pe, a.frame_splits, a.B, a.streams_per_cta, std::max(1, a.symbol_cap), a.count_capped,
+      a.tokens, a.lengths, a.counters);
   return cudaGetLastError();
 }
 

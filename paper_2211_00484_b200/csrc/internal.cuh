@@ -101,6 +101,9 @@ struct DecodeArgs {
   int32_t* lengths;         // device [B]
   double* scores;           // device [B]
   unsigned long long* counters; // device [8]
+  // greedy: symbols per frame (1 = greedy_search_batch; > 1 = greedy_search)
+  int32_t symbol_cap;
+  int32_t count_capped;     // count frames stopped by the cap (S unlimited)
   // beam
   int32_t beam_size, merge_op, length_norm, max_total;
   int32_t joiner_bf16;      // 1: tcgen05 bf16 joiner variant (not token-exact)

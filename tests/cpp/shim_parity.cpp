@@ -80,6 +80,24 @@ int main() {
         ++bad;
       }
   }
+  // greedy_search with S = 3 and S unlimited (search.hpp:76-100)
+  for (int32_t S : {3, kNoSymbolLimit}) {
+    int64_t gcap = 0;
+    auto gy = gpu::greedy_search_batched(ctx, m, batch, S, &gcap);
+    int64_t rcap = 0;
+    for (size_t i = 0; i < batch.size(); ++i) {
+      int64_t c = 0;
+      if (gy[i] != greedy_search(m, batch[i], S, &c)) {
+        std::printf("greedy S=%d mismatch %zu\n", S, i);
+        ++bad;
+      }
+      rcap += c;
+    }
+    if (S == kNoSymbolLimit && gcap != rcap) {
+      std::printf("capped frames %lld vs %lld\n", static_cast<long long>(gcap), static_cast<long long>(rcap));
+      ++bad;
+    }
+  }
   try {
     gpu::greedy_search_batch(ctx, m, batch, 2);
     ++bad;
