@@ -146,7 +146,8 @@ inline std::vector<std::vector<int32_t>> beam_search_batch(
   rnntg_beam_params p{params.beam_size, params.max_symbols,
                       params.merge_op == MergeOp::kLogAdd ? RNNTG_MERGE_LOG_ADD : RNNTG_MERGE_MAX,
                       params.length_norm ? 1 : 0, params.max_total_symbols};
-  std::vector<int32_t> splits(B + 1), toks(std::max<int32_t>(1, f.splits.back()));
+  const int64_t cap = params.max_symbols == kNoSymbolLimit ? kMaxSymbolsPerFrameSafety : params.max_symbols;
+  std::vector<int32_t> splits(B + 1), toks(std::max<int64_t>(1, f.splits.back() * cap));
   std::vector<double> sc(std::max<int32_t>(1, B));
   check(rnntg_beam_search_batch(ctx.handle(), f.enc.data(), f.splits.data(), B, &p,
                                 RNNTG_MEM_HOST, splits.data(), toks.data(), sc.data()));

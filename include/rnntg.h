@@ -90,10 +90,13 @@ typedef struct {
   const float* out_b;   /* [V]      */
 } rnntg_model_desc;
 
-/* SearchParams (search.hpp:44-50) restricted to max_symbols = 1. */
+/* SearchParams (search.hpp:44-50).  max_symbols: 1..10 or
+ * RNNTG_NO_SYMBOL_LIMIT (unlimited, at most 10 per frame as the reference's
+ * safety cap; the frames stopped by it are counted in rnntg_stats).  With
+ * S > 1 out_tokens must hold frame_splits[B] * min(S, 10) int32. */
 typedef struct {
   int32_t beam_size;         /* >= 1 */
-  int32_t max_symbols;       /* must be 1 (one symbol per frame) */
+  int32_t max_symbols;       /* S: 1..10 or RNNTG_NO_SYMBOL_LIMIT */
   int32_t merge_op;          /* rnntg_merge_op */
   int32_t length_norm;       /* 0/1 */
   int32_t max_total_symbols; /* 0 = uncapped */

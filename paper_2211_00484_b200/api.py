@@ -375,7 +375,8 @@ class Decoder:
         if mem == MEM_DEVICE:
             tokp, scp = C.c_void_p(out_tokens.data_ptr()), C.c_void_p(out_scores.data_ptr())
         else:
-            tok = np.zeros(max(1, int(splits[-1])), np.int32)
+            cap = 10 if params.max_symbols == NO_SYMBOL_LIMIT else max(1, params.max_symbols)
+            tok = np.zeros(max(1, int(splits[-1]) * cap), np.int32)
             sc = np.zeros(max(1, B), np.float64)
             tokp, scp = _ptr(tok), _ptr(sc)
         _check(self._lib.rnntg_beam_search_batch(self.h, p, _i32p(splits), B, C.byref(bp), mem, _i32p(osp), tokp, scp))

@@ -44,6 +44,7 @@ struct rnntg_model_s {
   // profiles/r01), 0 = never.
   int fused_pe = 1;
   Scratch ready;
+  Scratch pool;           // beam S > 1: sequence node pool
   int32_t slot_mult = 1;  // token slots per frame of the current call (greedy S > 1)
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
   Scratch finfo, nodebest, lattice, flag, feat, hid;
@@ -590,10 +591,6 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
   // beam_search validation, search.hpp:210-212.
   if (p->max_symbols < 1) return invalid("max_symbols must be >= 1");
   if (p->beam_size < 1) return invalid("beam_size must be >= 1");
-  if (p->max_symbols != 1) {
-    set_error("only one symbol per frame (max_symbols = 1) is implemented");
-    return RNNTG_UNSUPPORTED;
-  }
   if (p->beam_size > rnntg::kMaxBeam) {
     set_error("beam_size > 8 is beyond this build's per-stream hypothesis cap");
     return RNNTG_UNSUPPORTED;
@@ -605,8 +602,48 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
   if (!out_splits) return invalid("out_splits is null");
   std::lock_guard<std::mutex> lk(h->mu);
   RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  // S > 1 (search.hpp:228-235): up to `cap` sub-steps per frame, cap = 10
+  // for kNoSymbolLimit (frames stopped by it counted in the stats).
+  const bool unlimited = p->max_symbols == RNNTG_NO_SYMBOL_LIMIT;
+  const int32_t cap = unlimited ? 10 : p->max_symbols;
+  if (cap > 10) {
+    set_error("beam search with 10 < max_symbols < unlimited is beyond this build's per-frame cap");
+    return RNNTG_UNSUPPORTED;
+  }
+  h->slot_mult = cap;
+  struct SlotReset {
+    rnntg_model_t h;
+    ~SlotReset() { h->slot_mult = 1; }
+  } slot_reset{h};
   if ((st = prepare(h, fs, B, mem))) return st;
   int64_t launches = 0;
+  if (B > 0 && cap > 1) {
+    RNNTG_CUDA_TRY(h->pool.ensure(sizeof(int32_t) * 2 * (static_cast<int64_t>(fs[B]) * cap + B) * rnntg::kMaxBeam));
+    const int gmax = std::max(1, 32 / p->beam_size);
+    const int G = std::min(gmax, std::max(1, (B + h->num_sms - 1) / h->num_sms));
+    st = run_pipeline(h, enc, fs, B, mem, G, &launches, [&](int32_t b0, int32_t b1, cudaStream_t cs) {
+      rnntg::DecodeArgs a{};
+      a.m = &h->d;
+      a.pe = h->pe.as<float>();
+      a.frame_splits = h->splits.as<int32_t>() + b0;
+      a.B = b1 - b0;
+      a.streams_per_cta = G;
+      a.tokens = h->tok.as<int32_t>();
+      a.lengths = h->len.as<int32_t>() + b0;
+      a.scores = h->score.as<double>() + b0;
+      a.counters = h->counters.as<unsigned long long>();
+      a.beam_size = p->beam_size;
+      a.merge_op = p->merge_op;
+      a.length_norm = p->length_norm;
+      a.max_total = p->max_total_symbols;
+      a.symbol_cap = cap;
+      a.count_capped = unlimited ? 1 : 0;
+      a.node_pool = h->pool.as<int32_t>() + 2 * static_cast<int64_t>(b0);  // region base uses the global stream index
+      return rnntg::launch_decode_beam(a, cs);
+    });
+    if (st) return st;
+    return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+  }
   if (B > 0) {
     const int64_t total = fs[B];
     RNNTG_CUDA_TRY(h->bp.ensure(sizeof(uint32_t) * (total + B) * rnntg::kMaxBeam));

@@ -1091,6 +1091,391 @@ __global__ void __launch_bounds__(kDualThreads, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Modified beam search with S > 1 symbols per frame (beam_search,
+// search.hpp:206-277, any max_symbols).  Per frame and stream: level := the
+// beam; repeat { one joiner row per distinct context of the level; every
+// level hypothesis' blank continuation is merged into next_frame (by full
+// sequence identity, max or log_add); the level's extensions are cut to the
+// beam and become the next level } until the level is empty or `cap`
+// sub-steps ran (then the level is merged into next_frame with no score
+// factor); next_frame is cut to the beam.  Each sub-step is one CTA-wide
+// GEMM pass over the streams whose level is non-empty.  Sequences are kept
+// as nodes (parent, token) in a per-stream HBM pool (only extensions create
+// nodes; a blank continuation is its hypothesis' own node), which serves the
+// traceback and hyp_better's lexicographic tie rule.
+// ---------------------------------------------------------------------------
+constexpr int kNfCap = kMaxBeam * 11;  // next_frame entries: beam x (cap + 1), cap <= 10
+
+struct NfEntry {
+  double score;
+  uint64_t h1, h2;
+  int32_t len, ctx, last, node;
+};
+
+struct MStream {
+  int32_t node[kMaxBeam];  // level hypotheses' pool nodes
+  NfEntry nf[kNfCap];
+  int32_t nf_n;
+  int32_t pool_n;
+  BeamCand cand[kMaxBeam * kMaxBeam];
+};
+
+struct MultiSmem {
+  unsigned long long stat[16];
+  uint64_t bar[2];
+  uint32_t wcur[2];
+  int64_t row_pe[kRowCap];
+  int32_t row_ctx[kRowCap];
+  double row_lse[kRowCap];
+  float row_l0[kRowCap];
+  float row_tl[kRowCap][kMaxBeam];
+  int32_t row_tk[kRowCap][kMaxBeam];
+  int32_t nrows;
+};
+
+// Lexicographic order of two equal-length sequences given as pool nodes
+// (<0, 0, >0): walk back in lockstep, the last difference seen is the first
+// position where they differ.
+__device__ int node_lex(const int2* __restrict__ pool, int a, int b) {
+  int res = 0;
+  while (a != b) {
+    const int2 x = pool[a], y = pool[b];
+    if (x.y != y.y) res = x.y < y.y ? -1 : 1;
+    a = x.x;
+    b = y.x;
+  }
+  return res;
+}
+
+// hyp_better (search.hpp:172-178) for (key, len, node [, pending token]).
+__device__ __forceinline__ bool seq_before(double ka, int la, int na, int ta, double kb, int lb, int nb,
+                                           int tb, const int2* pool, unsigned long long* ties) {
+  if (ka != kb) return ka > kb;
+  if (la != lb) return la < lb;
+  ++*ties;
+  // equal lengths: compare the parents' sequences, then the pending tokens
+  const int c = node_lex(pool, na, nb);
+  if (c != 0) return c < 0;
+  return ta < tb;
+}
+
+__device__ __forceinline__ void nf_merge(NfEntry& e, double v, int merge_log) {
+  if (merge_log) {  // log_add, common.hpp:48-54
+    const double a = e.score, b = v;
+    if (a == -INFINITY) {
+      e.score = b;
+    } else if (b != -INFINITY) {
+      const double hi = a > b ? a : b, lo = a > b ? b : a;
+      e.score = hi + log1p(exp(lo - hi));
+    }
+  } else {
+    e.score = e.score > v ? e.score : v;
+  }
+}
+
+// Merges level hypotheses j (lane j < nl) into next_frame with scores v_j.
+// Level hypotheses are distinct sequences, so each lane's entry is hit by
+// no other lane of this call; misses are appended in lane order.
+__device__ __forceinline__ void nf_merge_level(MStream& st, const Hyps& lev, int nl, double v, int merge_log) {
+  const int lane = threadIdx.x & 31;
+  int hit = -1;
+  const int n0 = st.nf_n;
+  if (lane < nl) {
+    for (int q = 0; q < n0; ++q) {
+      const NfEntry& e = st.nf[q];
+      if (e.len == lev.len[lane] && e.h1 == lev.h1[lane] && e.h2 == lev.h2[lane]) {
+        hit = q;
+        break;
+      }
+    }
+  }
+  const unsigned miss = __ballot_sync(0xffffffffu, lane < nl && hit < 0);
+  if (lane < nl) {
+    if (hit >= 0) {
+      nf_merge(st.nf[hit], v, merge_log);
+    } else {
+      NfEntry& e = st.nf[n0 + __popc(miss & ((1u << lane) - 1u))];
+      e.score = v;
+      e.h1 = lev.h1[lane];
+      e.h2 = lev.h2[lane];
+      e.len = lev.len[lane];
+      e.ctx = lev.ctx[lane];
+      e.last = lev.last[lane];
+      e.node = st.node[lane];
+    }
+  }
+  __syncwarp();
+  if (lane == 0) st.nf_n = n0 + __popc(miss);
+  __syncwarp();
+}
+
+template <int BCAP>
+__global__ void __launch_bounds__(kDecodeThreads, 1)
+    beam_multi_kernel(ModelView m, const float* __restrict__ pe, const int32_t* __restrict__ frame_splits,
+                      int32_t B, int32_t G, int32_t cap, int32_t count_capped, int32_t beam,
+                      int32_t merge_log, int32_t length_norm, int32_t max_total, int2* __restrict__ pool,
+                      int32_t* __restrict__ tokens, int32_t* __restrict__ lengths, double* __restrict__ scores,
+                      unsigned long long* __restrict__ counters) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* HL = reinterpret_cast<float*>(smem_raw);
+  const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
+  float* W0 = HL + hl_floats;
+  float* W1 = W0 + kBKSmall * m.Vp;
+  MultiSmem& S = *reinterpret_cast<MultiSmem*>(W1 + kBKSmall * m.Vp);
+  Hyps* L = reinterpret_cast<Hyps*>(&S + 1);         // [G] levels
+  MStream* MS = reinterpret_cast<MStream*>(L + G);   // [G]
+  const int s0 = blockIdx.x * G;
+  const int ns = min(G, B - s0);
+  if (ns <= 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const WPipe pipe = make_wpipe(W0, W1, S.bar, S.wcur, m, kBKSmall);
+
+  int32_t tmax = 0;
+  for (int i = 0; i < ns; ++i) tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
+  for (int i = threadIdx.x; i < ns; i += kDecodeThreads) {
+    Hyps& h = L[i];  // the beam {[]: 0.0}
+    h.nh = 1;
+    h.score[0] = 0.0;
+    h.ctx[0] = 0;
+    h.len[0] = 0;
+    h.last[0] = -1;
+    h.h1[0] = 0x243f6a8885a308d3ull;
+    h.h2[0] = 0x13198a2e03707344ull;
+    h.p1[0] = h.p2[0] = 0;
+    MS[i].node[0] = 0;
+    MS[i].pool_n = 1;
+    const int64_t pb = static_cast<int64_t>(frame_splits[s0 + i]) * cap * kMaxBeam + s0 + i;
+    pool[pb] = make_int2(0, 0);  // root
+  }
+  if (threadIdx.x < 16) S.stat[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    wpipe_issue(pipe, m, 0);
+    wpipe_issue(pipe, m, 1);
+  }
+  uint32_t g = 0;
+  constexpr int kCandPerStream = kMaxBeam * kMaxBeam;
+
+  for (int32_t t = 0; t < tmax; ++t) {
+    for (int i = warp; i < ns; i += kWarps)
+      if (lane == 0) MS[i].nf_n = 0;
+    for (int32_t n = 0;; ++n) {
+      __syncthreads();
+      if (n == cap) {  // emission budget exhausted: forced advance, blank prob 1
+        for (int i = warp; i < ns; i += kWarps) {
+          const int32_t T = frame_splits[s0 + i + 1] - frame_splits[s0 + i];
+          if (t >= T || L[i].nh == 0) continue;
+          // scores unchanged; merge each level hypothesis with its own score
+          const double v = lane < L[i].nh ? L[i].score[lane] : 0.0;
+          nf_merge_level(MS[i], L[i], L[i].nh, v, merge_log);
+          if (count_capped && lane == 0) atomicAdd(&S.stat[13], 1ull);
+        }
+        break;
+      }
+      if (warp == 0) {
+        const int R0 = beam_rows(L, ns, frame_splits + s0, t, S.row_pe, S.row_ctx);
+        if (lane == 0) S.nrows = R0;
+      }
+      __syncthreads();
+      const int R = S.nrows;
+      if (R == 0) break;  // every live level is empty
+      if (threadIdx.x == 0) S.stat[1] += R;
+      build_h(m, pe, S.row_pe, S.row_ctx, R, HL);
+      joiner_gemm(m, pipe, g, HL, R);
+      const RowRes rr{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
+      if (R <= kWarps) {
+        if (warp < R) beam_row_reduce_n<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr);
+      } else if (warp < R - kWarps || warp < kWarps) {
+        beam_row_reduce_n<BCAP, 2>(HL, m.Vp, m.V, beam, warp, R, rr);
+      }
+      __syncthreads();
+      for (int i = warp; i < ns; i += kWarps) {
+        const int32_t fs = frame_splits[s0 + i];
+        const int32_t T = frame_splits[s0 + i + 1] - fs;
+        Hyps& h = L[i];
+        MStream& st = MS[i];
+        const int nl = h.nh;
+        if (t >= T || nl == 0) continue;
+        const int64_t pb = static_cast<int64_t>(fs) * cap * kMaxBeam + s0 + i;
+        const int2* P = pool + pb;
+        // blank continuations into next_frame: score + lp[0]
+        const double vb = lane < nl ? h.score[lane] + (static_cast<double>(rr.l0[h.row[lane]]) - rr.lse[h.row[lane]]) : 0.0;
+        nf_merge_level(st, h, nl, vb, merge_log);
+        // extensions: each hypothesis' top-`beam` tokens, then the level's top `beam`
+        BeamCand* cand = st.cand;
+        const int next = nl * beam;
+        for (int c = lane; c < next; c += 32) {
+          const int j = c / beam, q = c % beam;
+          const int r = h.row[j];
+          const bool may_emit = max_total <= 0 || h.len[j] < max_total;
+          const int k = rr.tk[r][q];
+          BeamCand& e = cand[c];
+          e.score = (may_emit && k < m.V) ? h.score[j] + (static_cast<double>(rr.tl[r][q]) - rr.lse[r]) : -INFINITY;
+          e.parent = j;
+          e.tok = k;
+          e.len = h.len[j] + 1;
+        }
+        __syncwarp();
+        int rank[2] = {0x7fffffff, 0x7fffffff};
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int c = lane + u * 32;
+          if (c >= next || cand[c].score == -INFINITY) continue;
+          const BeamCand a = cand[c];
+          int rk = 0;
+          for (int d = 0; d < next; ++d) {
+            const BeamCand& b = cand[d];
+            if (d == c || b.score == -INFINITY) continue;
+            if (seq_before(b.score, b.len, st.node[b.parent], b.tok, a.score, a.len, st.node[a.parent], a.tok, P,
+                           &S.stat[4]))
+              ++rk;
+          }
+          rank[u] = rk;
+        }
+        BeamCand sel[2];
+        int selnode[2] = {0, 0};
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (rank[u] < beam) sel[u] = cand[lane + u * 32];
+        int nsel = (rank[0] < beam ? 1 : 0) + (rank[1] < beam ? 1 : 0);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nsel += __shfl_xor_sync(0xffffffffu, nsel, o);
+        // new level (slot = rank) with fresh pool nodes (parent, token)
+        const int pn = st.pool_n;
+        uint64_t h1n[2], h2n[2];
+        int ctxn[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (rank[u] >= beam) continue;
+          const int gp = sel[u].parent;
+          h1n[u] = hash_ext1(h.h1[gp], sel[u].tok);
+          h2n[u] = hash_ext2(h.h2[gp], sel[u].tok);
+          ctxn[u] = (h.ctx[gp] % m.V) * m.V + sel[u].tok;
+          selnode[u] = pn + rank[u];
+          pool[pb + selnode[u]] = make_int2(st.node[gp], sel[u].tok);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (rank[u] >= beam) continue;
+          const int rk = rank[u];
+          h.score[rk] = sel[u].score;
+          h.h1[rk] = h1n[u];
+          h.h2[rk] = h2n[u];
+          h.ctx[rk] = ctxn[u];
+          h.len[rk] = sel[u].len;
+          h.last[rk] = sel[u].tok;
+          st.node[rk] = selnode[u];
+        }
+        __syncwarp();
+        if (lane == 0) {
+          h.nh = min(nsel, beam);
+          st.pool_n = pn + min(nsel, beam);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // next_frame cut to the beam (prune_to_beam): rank every entry by hyp_better
+    for (int i = warp; i < ns; i += kWarps) {
+      const int32_t fs = frame_splits[s0 + i];
+      const int32_t T = frame_splits[s0 + i + 1] - fs;
+      if (t >= T) continue;
+      Hyps& h = L[i];
+      MStream& st = MS[i];
+      const int64_t pb = static_cast<int64_t>(fs) * cap * kMaxBeam + s0 + i;
+      const int2* P = pool + pb;
+      const int nn = st.nf_n;
+      int rk3[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff};
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int c = lane + 32 * u;
+        if (c >= nn) continue;
+        const NfEntry& a = st.nf[c];
+        int rk = 0;
+        for (int d = 0; d < nn; ++d) {
+          if (d == c) continue;
+          const NfEntry& b = st.nf[d];
+          if (seq_before(b.score, b.len, b.node, -1, a.score, a.len, a.node, -1, P, &S.stat[4])) ++rk;
+        }
+        rk3[u] = rk;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        if (rk3[u] >= beam) continue;
+        const NfEntry& a = st.nf[lane + 32 * u];
+        const int rk = rk3[u];
+        h.score[rk] = a.score;
+        h.h1[rk] = a.h1;
+        h.h2[rk] = a.h2;
+        h.ctx[rk] = a.ctx;
+        h.len[rk] = a.len;
+        h.last[rk] = a.last;
+        st.node[rk] = a.node;
+      }
+      __syncwarp();
+      if (lane == 0) h.nh = min(nn, beam);
+      __syncwarp();
+      if (t + 1 == T && lane == 0) {  // final answer (search.hpp:261-276)
+        int best = 0;
+        for (int j = 1; j < h.nh; ++j) {
+          const double kj = length_norm ? h.score[j] / max(1, h.len[j]) : h.score[j];
+          const double kb = length_norm ? h.score[best] / max(1, h.len[best]) : h.score[best];
+          if (seq_before(kj, h.len[j], st.node[j], -1, kb, h.len[best], st.node[best], -1, P, &S.stat[4]))
+            best = j;
+        }
+        scores[s0 + i] = h.score[best];
+        lengths[s0 + i] = h.len[best];
+        int pos = h.len[best];
+        int nd = st.node[best];
+        const int64_t ob = static_cast<int64_t>(cap) * fs;
+        while (nd != 0) {
+          const int2 e = P[nd];
+          tokens[ob + --pos] = e.y;
+          nd = e.x;
+        }
+      }
+    }
+  }
+  for (int i = threadIdx.x; i < ns; i += kDecodeThreads)
+    if (frame_splits[s0 + i + 1] == frame_splits[s0 + i]) {
+      lengths[s0 + i] = 0;
+      scores[s0 + i] = 0.0;
+    }
+  __syncthreads();
+  if (threadIdx.x < 16 && threadIdx.x != 0 && S.stat[threadIdx.x] != 0)
+    atomicAdd(&counters[threadIdx.x], S.stat[threadIdx.x]);
+  if (threadIdx.x == 0) {
+    mbar_wait(&S.bar[g & 1u], (g >> 1) & 1u);
+    mbar_wait(&S.bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);
+    unsigned long long sf = 0;
+    for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
+    atomicAdd(&counters[0], sf);
+  }
+}
+
+template <int BCAP>
+cudaError_t launch_beam_multi(const DecodeArgs& a, cudaStream_t s) {
+  const ModelView m = view_of(*a.m);
+  const int G = a.streams_per_cta;
+  const size_t smem = smem_common(m, kBKSmall) + sizeof(MultiSmem) + (sizeof(Hyps) + sizeof(MStream)) * G;
+  cudaError_t e = cudaFuncSetAttribute(beam_multi_kernel<BCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int grid = (a.B + G - 1) / G;
+  beam_multi_kernel<BCAP><<<grid, kDecodeThreads, smem, s>>>(
+      m, a.pe, a.frame_splits, a.B, G, a.symbol_cap, a.count_capped, a.beam_size, a.merge_op, a.length_norm,
+      a.max_total, static_cast<int2*>(a.node_pool), a.tokens, a.lengths, a.scores, a.counters);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 int decode_num_sms_current() {
@@ -1451,6 +1836,12 @@ cudaError_t launch_beam_mode(const DecodeArgs& a, cudaStream_t s) {
 // registers); the runtime beam_size selects the smallest capacity >= it.
 // a.joiner_bf16 selects the tcgen05 joiner variant.
 cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s) {
+  if (a.symbol_cap > 1) {  // S > 1: sub-steps within a frame
+    if (a.beam_size <= 1) return launch_beam_multi<1>(a, s);
+    if (a.beam_size <= 2) return launch_beam_multi<2>(a, s);
+    if (a.beam_size <= 4) return launch_beam_multi<4>(a, s);
+    return launch_beam_multi<8>(a, s);
+  }
   return a.joiner_bf16 ? launch_beam_mode<true>(a, s) : launch_beam_mode<false>(a, s);
 }
 

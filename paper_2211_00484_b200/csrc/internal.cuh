@@ -111,6 +111,7 @@ struct DecodeArgs {
   int32_t beam_impl;        // 1: single 512-thread CTA per SM (default); 0: dual-residency kernel
   int32_t cta_slots;        // dual kernel: CTA slots this launch may fill (0: 2 x SMs)
   uint32_t* backptr;        // device [(sum T + B) * kMaxBeam]
+  void* node_pool;          // beam S > 1: device int2 [(sum T * cap + B) * kMaxBeam] (parent, token) nodes
   // beam, fused encoder projection (pe computed inside the decode kernel):
   const float* fused_enc;   // device [sum T][D] frames, or nullptr (pe precomputed by K1)
   float* fused_pe;          // device [sum T][J] written by the kernel (== pe)

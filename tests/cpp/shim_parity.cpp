@@ -98,6 +98,18 @@ int main() {
       ++bad;
     }
   }
+  // beam_search with S = 2 and S unlimited (search.hpp:206-277)
+  for (int32_t S : {2, kNoSymbolLimit}) {
+    SearchParams bp;
+    bp.beam_size = 4;
+    bp.max_symbols = S;
+    auto gb = gpu::beam_search_batch(ctx, m, batch, bp);
+    for (size_t i = 0; i < batch.size(); ++i)
+      if (gb[i] != beam_search(m, batch[i], bp)) {
+        std::printf("beam S=%d mismatch %zu\n", S, i);
+        ++bad;
+      }
+  }
   try {
     gpu::greedy_search_batch(ctx, m, batch, 2);
     ++bad;
