@@ -170,7 +170,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
 // ---------------------------------------------------------------------------
 // Modified beam search (beam_search at max_symbols = 1, search.hpp:206-277).
 // ---------------------------------------------------------------------------
-constexpr int kMaxG = kRowCap;  // streams per CTA (beam 1)
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x ^= x >> 30;
@@ -1032,8 +1031,7 @@ __global__ void __launch_bounds__(kDualThreads, 2)
   __syncthreads();
   if (threadIdx.x == 0) dual_pipe_prime(pipe, m);
   uint32_t g = 0;
-  unsigned long long rows_total = 0, ties = 0, rows_padded = 0;
-  long long tsplit = 0, ph_gather = 0, ph_pe[4] = {0, 0, 0, 0}, wcyc[2] = {0, 0};
+  unsigned long long rows_total = 0, ties = 0;
   long long ph_h = 0, ph_gemm = 0, ph_epi = 0, ph_step = 0;  // phase cycles (thread 0)
 
   for (int32_t t = 0; t < tmax; ++t) {
@@ -1260,7 +1258,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     wpipe_issue(pipe, m, 1);
   }
   uint32_t g = 0;
-  constexpr int kCandPerStream = kMaxBeam * kMaxBeam;
 
   for (int32_t t = 0; t < tmax; ++t) {
     for (int i = warp; i < ns; i += kWarps)

@@ -37,7 +37,6 @@ constexpr int kMaxStates = kFsaMaxStates;  // device cap on max_states
 constexpr int kHashCap = 256;    // hot-candidate hash entries per stream
 constexpr int kBins = 256;
 constexpr int kSurvHash = 128;
-constexpr int kMaxGroups = 4;    // streams per CTA
 constexpr int kMaxRaw = 32768;   // raw candidates per stream-frame (64 states x 511 arcs)
 constexpr uint64_t kEmptyKey = ~0ull;
 
