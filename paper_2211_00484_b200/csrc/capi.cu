@@ -682,6 +682,7 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       a.merge_op = p->merge_op;
       a.length_norm = p->length_norm;
       a.max_total = p->max_total_symbols;
+      // back-pointer rows are indexed (frame offset + stream index)
       a.backptr = h->bp.as<uint32_t>() + static_cast<int64_t>(b0) * rnntg::kMaxBeam;
       a.joiner_bf16 = h->joiner_mode == RNNTG_JOINER_BF16;
       a.warp_specialized = ws;
@@ -702,25 +703,7 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
     }
     st = run_pipeline(h, enc, fs, B, mem, G, &launches, [&](int32_t b0, int32_t b1, cudaStream_t cs) {
-      rnntg::DecodeArgs a{};
-      a.m = &h->d;
-      a.pe = h->pe.as<float>();
-      a.frame_splits = h->splits.as<int32_t>() + b0;
-      a.B = b1 - b0;
-      a.streams_per_cta = G;
-      a.tokens = h->tok.as<int32_t>();
-      a.lengths = h->len.as<int32_t>() + b0;
-      a.scores = h->score.as<double>() + b0;
-      a.counters = h->counters.as<unsigned long long>();
-      a.beam_size = p->beam_size;
-      a.merge_op = p->merge_op;
-      a.length_norm = p->length_norm;
-      a.max_total = p->max_total_symbols;
-      // back-pointer rows are indexed (frame offset + stream index)
-      a.backptr = h->bp.as<uint32_t>() + static_cast<int64_t>(b0) * rnntg::kMaxBeam;
-      a.joiner_bf16 = h->joiner_mode == RNNTG_JOINER_BF16;
-      a.warp_specialized = ws;
-      a.beam_impl = h->beam_impl;
+      rnntg::DecodeArgs a = args(b0, b1);
       // a chunk of the host-frame pipeline fills its share of the CTA slots
       a.cta_slots = static_cast<int32_t>((2LL * h->num_sms * (b1 - b0) + B - 1) / B);
       return rnntg::launch_decode_beam(a, cs);
