@@ -45,6 +45,9 @@ struct rnntg_model_s {
   int fused_pe = 1;
   Scratch ready;
   Scratch pool;           // beam S > 1: sequence node pool
+  // Small-batch greedy on thread-block clusters (cluster.cu);
+  // RNNTG_GREEDY_CLUSTER=0 disables.
+  bool greedy_cluster = true;
   int32_t slot_mult = 1;  // token slots per frame of the current call (greedy S > 1)
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
   Scratch finfo, nodebest, lattice, flag, feat, hid;
@@ -382,6 +385,7 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
   if (const char* ws = std::getenv("RNNTG_WS")) h->warp_specialized = std::atoi(ws) != 0;
   if (const char* bi = std::getenv("RNNTG_BEAM_IMPL")) h->beam_impl = std::atoi(bi);
   if (const char* fp = std::getenv("RNNTG_FUSED_PE")) h->fused_pe = std::atoi(fp);
+  if (const char* gc = std::getenv("RNNTG_GREEDY_CLUSTER")) h->greedy_cluster = std::atoi(gc) != 0;
   rnntg::DeviceModel& d = h->d;
   d.V = V;
   d.D = D;
@@ -536,6 +540,8 @@ rnntg_status greedy_impl(rnntg_model_t h, const float* enc, const int32_t* fs, i
       a.counters = h->counters.as<unsigned long long>();
       a.symbol_cap = cap;
       a.count_capped = count_capped ? 1 : 0;
+      if (cap == 1 && h->greedy_cluster && rnntg::greedy_cluster_fits(h->d, b1 - b0))
+        return rnntg::launch_decode_greedy_cluster(a, cs);
       return rnntg::launch_decode_greedy(a, cs);
     });
     if (st) {

@@ -133,6 +133,10 @@ struct DecodeArgs {
 };
 
 cudaError_t launch_decode_greedy(const DecodeArgs& a, cudaStream_t s);
+// small batches (<= 144 streams): thread-block clusters with out_w slices
+// resident in shared memory (cluster.cu)
+bool greedy_cluster_fits(const DeviceModel& d, int32_t B);
+cudaError_t launch_decode_greedy_cluster(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s);
 int decode_num_sms(int device);

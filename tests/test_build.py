@@ -52,7 +52,7 @@ def _functions(sass):
 def test_no_ffma_outside_division(lib):
     sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
     funcs = _functions(sass)
-    exact = [f for f in funcs if re.search(r"gemm_exact|beam_(dual_|ws_)?kernel|greedy_kernel|fsa_kernel|joiner_rows", f)]
+    exact = [f for f in funcs if re.search(r"gemm_exact|beam_(dual_|ws_|multi_)?kernel|greedy_(cluster_)?kernel|fsa_kernel|joiner_rows", f)]
     assert len(exact) >= 6
     for f in exact:
         ins = funcs[f]
