@@ -22,7 +22,8 @@ import numpy as np
 from . import build as _build
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = _build.LIB
+# RNNTG_LIB: development only, A/B timing of an alternate build of the same library
+lib_path = os.environ.get("RNNTG_LIB") or _build.LIB
 
 PARAM_NAMES = ("emb", "ctx_w", "ctx_b", "j_we", "j_wd", "j_b", "out_w", "out_b")
 

@@ -43,6 +43,15 @@ struct rnntg_model_s {
   // 2 = also device frames (measured slower there than K1 + decode:
   // profiles/r01), 0 = never.
   int fused_pe = 1;
+  // Time-sliced host-frame path for the beam kernel (copy + K1 of slice k+1
+  // under the decode of slice k).  RNNTG_SLICED: 1 = host frames of uniform
+  // length (default; preferred over the fused path), 0 = never.
+  // RNNTG_SLICE_FIRST / RNNTG_SLICE_MAX: first slice length (frames) and
+  // the cap its doubling grows to.
+  int sliced = 1;
+  int32_t slice_first = 16, slice_max = 256;
+  Scratch hstate;                     // per-stream hypothesis sets between slices
+  std::vector<cudaEvent_t> slice_ev;  // one per slice: its frames have landed
   Scratch ready;
   Scratch pool;           // beam S > 1: sequence node pool
   // Small-batch greedy on thread-block clusters (cluster.cu);
@@ -199,6 +208,55 @@ rnntg_status run_fused(rnntg_model_t h, const float* enc, const int32_t* fs, int
     RNNTG_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->done[0], 0));
   }
   h->pipelined = false;
+  return RNNTG_OK;
+}
+
+// Host frames of uniform length T, decoded in time slices: slice k = frames
+// [cut_k, cut_{k+1}) of every stream.  A copy stream moves each slice with
+// one pitched cudaMemcpy2DAsync and records the slice's event; the compute
+// stream waits for it, projects the slice (K1 over row groups) and decodes it
+// (beam kernel resuming from the hypothesis sets the previous slice stored).
+// The copies run ahead on the copy engine, so only the first (short) slice's
+// copy is exposed; K1 and decode keep the unfused kernels' code.
+template <typename Launch>
+rnntg_status run_sliced(rnntg_model_t h, const float* enc, const int32_t* fs, int32_t B,
+                        int64_t* launches, Launch&& launch) {
+  const int32_t D = h->d.D, J = h->d.J, T = fs[1] - fs[0];
+  std::vector<int32_t> cut{0};
+  for (int32_t len = h->slice_first; cut.back() < T; len = std::min(2 * len, std::max(h->slice_first, h->slice_max)))
+    cut.push_back(std::min(T, cut.back() + len));
+  const int nsl = static_cast<int>(cut.size()) - 1;
+  RNNTG_CUDA_TRY(h->hstate.ensure(rnntg::beam_state_bytes() * static_cast<size_t>(B)));
+  while (static_cast<int>(h->slice_ev.size()) < nsl) {
+    cudaEvent_t e;
+    RNNTG_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->slice_ev.push_back(e);
+  }
+  if (!h->cstream[0]) RNNTG_CUDA_TRY(cudaStreamCreateWithFlags(&h->cstream[0], cudaStreamNonBlocking));
+  cudaStream_t cs = h->cstream[0];
+  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
+  RNNTG_CUDA_TRY(cudaStreamWaitEvent(cs, h->ev[0], 0));  // the previous call is done with h->enc
+  const size_t pitch = sizeof(float) * static_cast<size_t>(T) * D;
+  float* d_enc = h->enc.as<float>();
+  for (int k = 0; k < nsl; ++k) {
+    const int32_t f0 = cut[k], nf = cut[k + 1] - cut[k];
+    RNNTG_CUDA_TRY(cudaMemcpy2DAsync(d_enc + static_cast<int64_t>(f0) * D, pitch, enc + static_cast<int64_t>(f0) * D,
+                                     pitch, sizeof(float) * static_cast<size_t>(nf) * D, B,
+                                     cudaMemcpyHostToDevice, cs));
+    RNNTG_CUDA_TRY(cudaEventRecord(h->slice_ev[k], cs));
+  }
+  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+  for (int k = 0; k < nsl; ++k) {
+    const int32_t f0 = cut[k], nf = cut[k + 1] - cut[k];
+    RNNTG_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->slice_ev[k], 0));
+    RNNTG_CUDA_TRY(rnntg::launch_gemm_exact_grouped(d_enc + static_cast<int64_t>(f0) * D, D, h->d.j_wet, h->d.Jp,
+                                                    nullptr, h->pe.as<float>() + static_cast<int64_t>(f0) * J, J,
+                                                    static_cast<int64_t>(B) * nf, J, D, false, nullptr, 0, 0, nf,
+                                                    T, h->stream));
+    RNNTG_CUDA_TRY(launch(cut[k], cut[k + 1], h->stream));
+    *launches += 2;
+  }
+  h->pipelined = true;  // decode overlaps the copies: the stats report the whole call
   return RNNTG_OK;
 }
 
@@ -385,6 +443,9 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
   if (const char* ws = std::getenv("RNNTG_WS")) h->warp_specialized = std::atoi(ws) != 0;
   if (const char* bi = std::getenv("RNNTG_BEAM_IMPL")) h->beam_impl = std::atoi(bi);
   if (const char* fp = std::getenv("RNNTG_FUSED_PE")) h->fused_pe = std::atoi(fp);
+  if (const char* e = std::getenv("RNNTG_SLICED")) h->sliced = std::atoi(e);
+  if (const char* e = std::getenv("RNNTG_SLICE_FIRST")) h->slice_first = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("RNNTG_SLICE_MAX")) h->slice_max = std::max(1, std::atoi(e));
   if (const char* gc = std::getenv("RNNTG_GREEDY_CLUSTER")) h->greedy_cluster = std::atoi(gc) != 0;
   rnntg::DeviceModel& d = h->d;
   d.V = V;
@@ -472,10 +533,12 @@ rnntg_status rnntg_model_destroy(rnntg_model_t h) {
   for (void* p : h->owned) cudaFree(p);
   for (Scratch* s : {&h->enc, &h->pe, &h->splits, &h->tok, &h->len, &h->score, &h->bp,
                      &h->counters, &h->ctx, &h->out_tok, &h->out_splits, &h->logits,
-                     &h->finfo, &h->nodebest, &h->lattice, &h->flag, &h->feat, &h->hid})
+                     &h->finfo, &h->nodebest, &h->lattice, &h->flag, &h->feat, &h->hid,
+                     &h->hstate, &h->ready, &h->pool})
     s->release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->slice_ev) cudaEventDestroy(e);
   for (int c = 0; c < 4; ++c) {
     if (h->cstream[c]) cudaStreamDestroy(h->cstream[c]);
     if (h->done[c]) cudaEventDestroy(h->done[c]);
@@ -695,6 +758,19 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       a.beam_impl = h->beam_impl;
       return a;
     };
+    const bool sliced = exact && !ws && h->beam_impl == 1 && h->sliced > 0 && mem == RNNTG_MEM_HOST && uniform &&
+                        fs[1] - fs[0] > h->slice_first;
+    if (sliced) {
+      st = run_sliced(h, enc, fs, B, &launches, [&](int32_t t0, int32_t t1, cudaStream_t cs) {
+        rnntg::DecodeArgs a = args(0, B);
+        a.t0 = t0;
+        a.t1 = t1;
+        a.hyps_state = h->hstate.ptr;
+        return rnntg::launch_decode_beam(a, cs);
+      });
+      if (st) return st;
+      return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+    }
     if (fused) {
       st = run_fused(h, enc, fs, B, mem, &launches, [&](const float* d_enc, const int32_t* rdy, int32_t S,
                                                        cudaStream_t cs) {

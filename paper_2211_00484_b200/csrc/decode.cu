@@ -196,6 +196,25 @@ struct Hyps {  // one stream's beam, sorted best first
   int32_t nh;
 };
 
+// Time-sliced launches (DecodeArgs::t0/t1): frames [t0, t1) of every stream;
+// the hypothesis sets are loaded from / stored to `state` (indexed by stream)
+// at the launch boundaries.  t0 = 0, t1 = INT_MAX, state = nullptr: one
+// launch over all frames.
+struct BeamSlice {
+  int32_t t0, t1;
+  Hyps* state;
+};
+static_assert(sizeof(Hyps) % 8 == 0, "hypothesis sets are copied as 8-byte words");
+
+// CTA-wide copy of n hypothesis sets (out of line: keeps the frame loop's
+// register allocation independent of the slice plumbing).
+__device__ __noinline__ void copy_hyps(Hyps* __restrict__ dst, const Hyps* __restrict__ src, int n) {
+  constexpr int W = sizeof(Hyps) / 8;
+  uint64_t* d = reinterpret_cast<uint64_t*>(dst);
+  const uint64_t* s = reinterpret_cast<const uint64_t*>(src);
+  for (int x = threadIdx.x; x < n * W; x += blockDim.x) d[x] = s[x];
+}
+
 struct BeamCand {  // stage-1 extension or stage-2 merged entry
   double score;
   uint64_t h1, h2, p1, p2;
@@ -411,6 +430,9 @@ __device__ __forceinline__ uint64_t tok_key(float v, int k) {
   return (static_cast<uint64_t>(ord_key(v + 0.0f)) << 32) | static_cast<uint32_t>(~k);  // -0 -> +0
 }
 
+#ifndef RNNTG_SL_RR_NI
+#define RNNTG_SL_RR_NI 1
+#endif
 template <int BCAP, int NR>
 __device__ __forceinline__ void beam_row_reduce_n(const float* HL, int Vp, int V, int beam, int r0,
                                                   int R, RowRes rr, int rs = 16) {
@@ -475,6 +497,14 @@ __device__ __forceinline__ void beam_row_reduce_n(const float* HL, int Vp, int V
       rr.l0[r0 + rs * j] = L[j][0];
     }
   }
+}
+
+// Out-of-line copy for the time-sliced kernel instantiation (measured faster
+// there than inlined; the single-launch kernel inlines it).
+template <int BCAP, int NR>
+__device__ __noinline__ void beam_row_reduce_ni(const float* HL, int Vp, int V, int beam, int r0, int R,
+                                                RowRes rr) {
+  beam_row_reduce_n<BCAP, NR>(HL, Vp, V, beam, r0, R, rr);
 }
 
 // E. one stream's frame (one warp).  Reference order (search.hpp:223-259 at
@@ -764,7 +794,11 @@ __device__ __noinline__ void fused_pe_pass(const ModelView& m, const FusedPe& fp
   }
 }
 
-template <int BCAP, bool TC, bool FPE>
+// SL: time-sliced launch (frames [sl.t0, sl.t1), hypothesis sets resumed
+// from / kept in sl.state).  A separate instantiation so the single-launch
+// kernel's code is untouched by the slice plumbing (ptxas's register
+// allocation of the frame loop is sensitive to it: ~1-2%).
+template <int BCAP, bool TC, bool FPE, bool SL = false>
 __global__ void __launch_bounds__(kDecodeThreads, 1)
     beam_kernel(ModelView m, const float* __restrict__ pe,
                 const int32_t* __restrict__ frame_splits, int32_t B, int32_t G,
@@ -772,7 +806,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
                 int32_t max_total, uint32_t* __restrict__ backptr,
                 int32_t* __restrict__ tokens, int32_t* __restrict__ lengths,
                 double* __restrict__ scores,
-                unsigned long long* __restrict__ counters, FusedPe fp) {
+                unsigned long long* __restrict__ counters, FusedPe fp, BeamSlice sl) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* HL = reinterpret_cast<float*>(smem_raw);
   const int hl_floats = max(max(m.J, fp.D) * kHStride, kRowCap * m.Vp);
@@ -815,16 +849,23 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   int32_t tmax = 0;
   for (int i = 0; i < ns; ++i)
     tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
-  for (int i = threadIdx.x; i < ns; i += kDecodeThreads) {
-    Hyps& h = H[i];
-    h.nh = 1;
-    h.score[0] = 0.0;
-    h.ctx[0] = 0;
-    h.len[0] = 0;
-    h.last[0] = -1;
-    h.h1[0] = 0x243f6a8885a308d3ull;
-    h.h2[0] = 0x13198a2e03707344ull;
-    h.p1[0] = h.p2[0] = 0;
+  // Only t_end stays live across the frame loop (it replaces tmax); sl.* are
+  // kernel parameters (constant bank), re-read where needed.
+  const int32_t t_end = SL ? min(sl.t1, tmax) : tmax;
+  if (SL && sl.t0 > 0) {  // resume: this CTA's hypothesis sets
+    copy_hyps(H, sl.state + s0, ns);
+  } else {
+    for (int i = threadIdx.x; i < ns; i += kDecodeThreads) {
+      Hyps& h = H[i];
+      h.nh = 1;
+      h.score[0] = 0.0;
+      h.ctx[0] = 0;
+      h.len[0] = 0;
+      h.last[0] = -1;
+      h.h1[0] = 0x243f6a8885a308d3ull;
+      h.h2[0] = 0x13198a2e03707344ull;
+      h.p1[0] = h.p2[0] = 0;
+    }
   }
   if (threadIdx.x < 16) S.stat[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
@@ -863,10 +904,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   // Frame blocks of F frames: the fused encoder projection runs once per
   // block, outside the per-frame loop (keeps that loop's register allocation
   // identical to the unfused kernel's).
-  const int32_t TB = FPE ? F : max(1, tmax);
-  for (int32_t tb = 0; tb < tmax; tb += TB) {
+  const int32_t t_begin = SL ? sl.t0 : 0;
+  const int32_t TB = FPE ? F : max(1, t_end - t_begin);
+  for (int32_t tb = t_begin; tb < t_end; tb += TB) {
   if constexpr (FPE) fused_pe_pass(m, fp, pipe, g, HL, S, frame_splits, s0, ns, tb, F, pst + 12);
-  const int32_t te = min(tb + TB, tmax);
+  const int32_t te = min(tb + TB, t_end);
   for (int32_t t = tb; t < te; ++t) {
     // A. rows: distinct contexts per live stream (lane = stream, G <= 32).
     if (warp == 0) {
@@ -907,10 +949,18 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     // token asc).  Each lane keeps a sorted local top-kMaxBeam, then `beam`
     // warp-wide pops.
     const RowRes rr{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
-    if (R <= kWarps) {
-      if (warp < R) beam_row_reduce_n<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr);
-    } else if (warp < R - kWarps || warp < kWarps) {
-      beam_row_reduce_n<BCAP, 2>(HL, m.Vp, m.V, beam, warp, R, rr);
+    if constexpr (SL && RNNTG_SL_RR_NI) {
+      if (R <= kWarps) {
+        if (warp < R) beam_row_reduce_ni<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr);
+      } else if (warp < R - kWarps || warp < kWarps) {
+        beam_row_reduce_ni<BCAP, 2>(HL, m.Vp, m.V, beam, warp, R, rr);
+      }
+    } else {
+      if (R <= kWarps) {
+        if (warp < R) beam_row_reduce_n<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr);
+      } else if (warp < R - kWarps || warp < kWarps) {
+        beam_row_reduce_n<BCAP, 2>(HL, m.Vp, m.V, beam, warp, R, rr);
+      }
     }
     __syncthreads();
 
@@ -944,6 +994,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       lengths[s0 + i] = 0;
       scores[s0 + i] = 0.0;
     }
+  if (SL)  // sliced launch: keep the hypothesis sets for the next slice
+    copy_hyps(sl.state + s0, H, ns);
   __syncthreads();
   if (threadIdx.x < 16 && threadIdx.x != 0 && threadIdx.x != 2 && st[threadIdx.x] != 0)
     atomicAdd(&counters[threadIdx.x], st[threadIdx.x]);
@@ -963,8 +1015,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       mbar_wait(&S.bar[g & 1u], (g >> 1) & 1u);
       mbar_wait(&S.bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);
     }
-    unsigned long long sf = 0;
-    for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
+    unsigned long long sf = 0;  // frames decoded by this launch
+    for (int i = 0; i < ns; ++i)
+      sf += SL ? max(0, min(frame_splits[s0 + i + 1] - frame_splits[s0 + i], t_end) - sl.t0)
+               : frame_splits[s0 + i + 1] - frame_splits[s0 + i];
     atomicAdd(&counters[0], sf);
   }
 }
@@ -1759,7 +1813,7 @@ cudaError_t launch_beam_ws(const DecodeArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int BCAP, bool TC, bool FPE>
+template <int BCAP, bool TC, bool FPE, bool SL = false>
 cudaError_t launch_beam_cap3(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);
   const int G = a.streams_per_cta;
@@ -1772,13 +1826,14 @@ cudaError_t launch_beam_cap3(const DecodeArgs& a, cudaStream_t s) {
   size_t smem = hl + static_cast<size_t>(2) * (TC ? 16 : kBK) * m.Vp * 4 + sizeof(BeamSmem) + sizeof(Hyps) * G +
                 sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
   if (TC) smem += 1024 + static_cast<size_t>(kRowCap) * m.J * 2 + sizeof(TcBars);
-  cudaError_t e = cudaFuncSetAttribute(beam_kernel<BCAP, TC, FPE>,
+  cudaError_t e = cudaFuncSetAttribute(beam_kernel<BCAP, TC, FPE, SL>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int grid = (a.B + G - 1) / G;
-  beam_kernel<BCAP, TC, FPE><<<grid, kDecodeThreads, smem, s>>>(
+  beam_kernel<BCAP, TC, FPE, SL><<<grid, kDecodeThreads, smem, s>>>(
       m, a.pe, a.frame_splits, a.B, G, a.beam_size, a.merge_op, a.length_norm, a.max_total,
-      a.backptr, a.tokens, a.lengths, a.scores, a.counters, fp);
+      a.backptr, a.tokens, a.lengths, a.scores, a.counters, fp,
+      BeamSlice{a.t0, a.t1, static_cast<Hyps*>(a.hyps_state)});
   return cudaGetLastError();
 }
 
@@ -1786,6 +1841,7 @@ template <int BCAP, bool TC>
 cudaError_t launch_beam_cap(const DecodeArgs& a, cudaStream_t s) {
   if constexpr (!TC) {
     if (a.fused_enc) return launch_beam_cap3<BCAP, false, true>(a, s);
+    if (a.hyps_state) return launch_beam_cap3<BCAP, false, false, true>(a, s);
   }
   return launch_beam_cap3<BCAP, TC, false>(a, s);
 }
@@ -1832,6 +1888,8 @@ cudaError_t launch_beam_mode(const DecodeArgs& a, cudaStream_t s) {
 // Hypothesis capacity is a compile-time bound (local top-k lists live in
 // registers); the runtime beam_size selects the smallest capacity >= it.
 // a.joiner_bf16 selects the tcgen05 joiner variant.
+size_t beam_state_bytes() { return sizeof(Hyps); }
+
 cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s) {
   if (a.symbol_cap > 1) {  // S > 1: sub-steps within a frame
     if (a.beam_size <= 1) return launch_beam_multi<1>(a, s);

@@ -232,10 +232,16 @@ __device__ __forceinline__ void gemm_pass(const ModelView& m, const WPipe& p,
 
 // One out_w chunk of a work item: NR <= 4 rows x 32*TN columns (lane
 // columns col[0..TN)), accumulated into acc[0..NR)[0..TN).
+// k steps unrolled per loop trip (2, 6 and 8 measured slower than 4; a
+// source-level software-pipelined variant too: DESIGN.md).
+#ifndef RNNTG_GEMM_UNROLL
+#define RNNTG_GEMM_UNROLL 4
+#endif
+constexpr int kGemmUnroll = RNNTG_GEMM_UNROLL;
 template <int TN, int NR, int HS = kHStride>
 __device__ __forceinline__ void gemm_chunk(const ModelView& m, uint32_t ws, const float* hp, int kk_end,
                                            const int* col, float (&acc)[4][8]) {
-#pragma unroll 4
+#pragma unroll kGemmUnroll
   for (int kk = 0; kk < kk_end; ++kk) {
     const float4 h4 = *reinterpret_cast<const float4*>(hp + kk * HS);
     const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
@@ -339,10 +345,21 @@ __device__ __forceinline__ void gemm_pass_bal(const ModelView& m, const WPipe& p
   __syncthreads();
 }
 
+#ifdef RNNTG_GEMM_EXTERN
+// gemm_bal.cu: gemm_pass_bal out of line in its own translation unit (one
+// schedule for every kernel).  Returns the chunk counter after the pass.
+__device__ uint32_t gemm_bal_x(const WPipe p, uint32_t g, uint32_t hl, int R, int Vp,
+                               const float* __restrict__ bias, int K, int nc, long long* wc);
+#endif
+
 __device__ __forceinline__ void joiner_gemm(const ModelView& m, const WPipe& p,
                                             uint32_t& g, float* HL, int R, long long* wc = nullptr) {
   if (m.Vp == 512 && R > 4) {
+#ifdef RNNTG_GEMM_EXTERN
+    g = gemm_bal_x(p, g, smem_u32(HL), R, m.Vp, m.out_b, m.J, p.nc, wc);
+#else
     gemm_pass_bal(m, p, g, HL, R, wc);
+#endif
     return;
   }
   const int rg = (R + 3) >> 2;

@@ -25,9 +25,17 @@ using rnntg_exact::fmul;
 constexpr int BM = 64, BN = 128, BK = 16, TM = 4, TN = 8;
 constexpr int kThreads = (BM / TM) * (BN / TN);  // 256
 
+// Row groups: logical row m of a launch is physical row
+// (m / grp) * gstride + m % grp of X and Y (grp = 0: m itself).  A time slice
+// [t0, t0 + grp) of B streams of uniform length T is grp = slice length,
+// gstride = T, X and Y offset by t0 rows.
+__device__ __forceinline__ int64_t phys_row(int64_t m, int32_t grp, int64_t gstride) {
+  return grp > 0 ? (m / grp) * gstride + m % grp : m;
+}
+
 template <bool kGather>
 __device__ __forceinline__ float load_x(const float* __restrict__ X, int64_t ldx,
-                                        int64_t m, int32_t k, int64_t M,
+                                        int64_t m, int64_t mp, int32_t k, int64_t M,
                                         int32_t K, const float* __restrict__ emb,
                                         int32_t V, int64_t ctx_base) {
   if (m >= M || k >= K) return 0.0f;
@@ -37,7 +45,7 @@ __device__ __forceinline__ float load_x(const float* __restrict__ X, int64_t ldx
     const int64_t tok = k < E ? c / V : c % V;
     return emb[tok * E + (k < E ? k : k - E)];
   } else {
-    return X[m * ldx + k];
+    return X[mp * ldx + k];
   }
 }
 
@@ -48,7 +56,7 @@ __global__ void __launch_bounds__(kThreads)
                       const float* __restrict__ bias, float* __restrict__ Y,
                       int64_t ldy, int64_t M, int32_t N, int32_t K,
                       const float* __restrict__ emb, int32_t V,
-                      int64_t ctx_base) {
+                      int64_t ctx_base, int32_t grp, int64_t gstride) {
   __shared__ __align__(16) float Xs[2][BK][BM];
   __shared__ __align__(16) float Ws[2][BK][BN];
 
@@ -61,13 +69,14 @@ __global__ void __launch_bounds__(kThreads)
   // Global->register staging: X tile is BM x BK (one row, 4 k per thread),
   // W tile is BK x BN (two float4 per thread).
   const int xr = tid / 4, xk = (tid % 4) * 4;
+  const int64_t xm = phys_row(m0 + xr, grp, gstride);
   float xreg[4];
   float4 wreg[2];
 
   auto gload = [&](int32_t k0) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      xreg[i] = load_x<kGather>(X, ldx, m0 + xr, k0 + xk + i, M, K, emb, V,
+      xreg[i] = load_x<kGather>(X, ldx, m0 + xr, xm, k0 + xk + i, M, K, emb, V,
                                 ctx_base);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -129,13 +138,14 @@ __global__ void __launch_bounds__(kThreads)
   for (int i = 0; i < TM; ++i) {
     const int64_t m = m0 + tm * 4 + i;
     if (m >= M) continue;
+    const int64_t mp = phys_row(m, grp, gstride);
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       const int32_t n = n0 + (j < 4 ? tn * 4 + j : 64 + tn * 4 + (j - 4));
       if (n < N) {
         float v = acc[i][j];
         if constexpr (kTanh) v = rnntg_exact::tanhf_glibc(v);
-        Y[m * ldy + n] = v;
+        Y[mp * ldy + n] = v;
       }
     }
   }
@@ -143,41 +153,54 @@ __global__ void __launch_bounds__(kThreads)
 
 }  // namespace
 
+cudaError_t launch_gemm_exact_grouped(const float* X, int64_t ldx, const float* Wt, int32_t ldw,
+                                      const float* bias, float* Y, int64_t ldy, int64_t M, int32_t N,
+                                      int32_t K, bool apply_tanh, const float* ctx_emb,
+                                      int32_t ctx_V, int64_t ctx_base, int32_t grp, int64_t gstride,
+                                      cudaStream_t stream) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  if (grp > 0 && (ctx_emb || M % grp != 0)) return cudaErrorInvalidValue;
+  // The grid's y dimension is limited to 65535 tiles per launch (a multiple
+  // of grp rows, so every launch starts on a group boundary).
+  int64_t max_rows = static_cast<int64_t>(65535) * BM;
+  if (grp > 0) max_rows = max_rows / grp * grp;
+  for (int64_t r0 = 0; r0 < M; r0 += max_rows) {
+    const int64_t rows = M - r0 < max_rows ? M - r0 : max_rows;
+    dim3 grid((N + BN - 1) / BN, static_cast<unsigned>((rows + BM - 1) / BM));
+    const int64_t p0 = grp > 0 ? r0 / grp * gstride : r0;
+    const float* Xp = ctx_emb ? nullptr : X + p0 * ldx;
+    float* Yp = Y + p0 * ldy;
+    if (ctx_emb) {
+      if (apply_tanh)
+        gemm_exact_kernel<true, true><<<grid, kThreads, 0, stream>>>(
+            Xp, ldx, Wt, ldw, bias, Yp, ldy, rows, N, K, ctx_emb, ctx_V,
+            ctx_base + r0, 0, 0);
+      else
+        gemm_exact_kernel<true, false><<<grid, kThreads, 0, stream>>>(
+            Xp, ldx, Wt, ldw, bias, Yp, ldy, rows, N, K, ctx_emb, ctx_V,
+            ctx_base + r0, 0, 0);
+    } else {
+      if (apply_tanh)
+        gemm_exact_kernel<false, true><<<grid, kThreads, 0, stream>>>(
+            Xp, ldx, Wt, ldw, bias, Yp, ldy, rows, N, K, nullptr, 0, 0, grp, gstride);
+      else
+        gemm_exact_kernel<false, false><<<grid, kThreads, 0, stream>>>(
+            Xp, ldx, Wt, ldw, bias, Yp, ldy, rows, N, K, nullptr, 0, 0, grp, gstride);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_gemm_exact(const float* X, int64_t ldx, const float* Wt,
                               int32_t ldw, const float* bias, float* Y,
                               int64_t ldy, int64_t M, int32_t N, int32_t K,
                               bool apply_tanh, const float* ctx_emb,
                               int32_t ctx_V, int64_t ctx_base,
                               cudaStream_t stream) {
-  if (M <= 0 || N <= 0) return cudaSuccess;
-  // The grid's y dimension is limited to 65535 tiles per launch.
-  const int64_t max_rows = static_cast<int64_t>(65535) * BM;
-  for (int64_t r0 = 0; r0 < M; r0 += max_rows) {
-    const int64_t rows = M - r0 < max_rows ? M - r0 : max_rows;
-    dim3 grid((N + BN - 1) / BN, static_cast<unsigned>((rows + BM - 1) / BM));
-    const float* Xp = ctx_emb ? nullptr : X + r0 * ldx;
-    float* Yp = Y + r0 * ldy;
-    if (ctx_emb) {
-      if (apply_tanh)
-        gemm_exact_kernel<true, true><<<grid, kThreads, 0, stream>>>(
-            Xp, ldx, Wt, ldw, bias, Yp, ldy, rows, N, K, ctx_emb, ctx_V,
-            ctx_base + r0);
-      else
-        gemm_exact_kernel<true, false><<<grid, kThreads, 0, stream>>>(
-            Xp, ldx, Wt, ldw, bias, Yp, ldy, rows, N, K, ctx_emb, ctx_V,
-            ctx_base + r0);
-    } else {
-      if (apply_tanh)
-        gemm_exact_kernel<false, true><<<grid, kThreads, 0, stream>>>(
-            Xp, ldx, Wt, ldw, bias, Yp, ldy, rows, N, K, nullptr, 0, 0);
-      else
-        gemm_exact_kernel<false, false><<<grid, kThreads, 0, stream>>>(
-            Xp, ldx, Wt, ldw, bias, Yp, ldy, rows, N, K, nullptr, 0, 0);
-    }
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+  return launch_gemm_exact_grouped(X, ldx, Wt, ldw, bias, Y, ldy, M, N, K, apply_tanh, ctx_emb,
+                                   ctx_V, ctx_base, 0, 0, stream);
 }
 
 }  // namespace rnntg

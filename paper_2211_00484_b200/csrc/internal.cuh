@@ -89,6 +89,15 @@ cudaError_t launch_gemm_exact(const float* X, int64_t ldx, const float* Wt,
                               bool apply_tanh, const float* ctx_emb,
                               int32_t ctx_V, int64_t ctx_base,
                               cudaStream_t stream);
+// The same over row groups: logical row m is physical row
+// (m / grp) * gstride + m % grp of X and Y (M a multiple of grp): a time
+// slice of grp frames of streams of uniform length gstride, X and Y offset
+// to the slice's first frame.  grp = 0: contiguous rows.
+cudaError_t launch_gemm_exact_grouped(const float* X, int64_t ldx, const float* Wt, int32_t ldw,
+                                      const float* bias, float* Y, int64_t ldy, int64_t M, int32_t N,
+                                      int32_t K, bool apply_tanh, const float* ctx_emb,
+                                      int32_t ctx_V, int64_t ctx_base, int32_t grp, int64_t gstride,
+                                      cudaStream_t stream);
 
 // ---- persistent decode kernels (decode.cu) ----
 struct DecodeArgs {
@@ -117,6 +126,11 @@ struct DecodeArgs {
   float* fused_pe;          // device [sum T][J] written by the kernel (== pe)
   const int32_t* ready;     // device: number of frame slices of fused_enc that have landed
   int32_t slice_frames;     // frames per slice (slice s = frames [s*slice_frames, ...) of every stream)
+  // beam, time-sliced launches (host frames: the copy and K1 of slice k+1
+  // overlap the decode of slice k): this launch decodes frames [t0, t1) of
+  // every stream; hypothesis sets persist between launches in hyps_state.
+  int32_t t0 = 0, t1 = 0x7fffffff;
+  void* hyps_state = nullptr;  // device [B] beam hypothesis sets (beam_state_bytes() each)
   // fsa
   const void* graph_arcs;   // device int4-packed arcs
   const int32_t* graph_splits;
@@ -133,6 +147,7 @@ struct DecodeArgs {
 };
 
 cudaError_t launch_decode_greedy(const DecodeArgs& a, cudaStream_t s);
+size_t beam_state_bytes();  // per-stream hypothesis set carried between time-sliced launches
 // small batches (<= 144 streams): thread-block clusters with out_w slices
 // resident in shared memory (cluster.cu)
 bool greedy_cluster_fits(const DeviceModel& d, int32_t B);

@@ -45,3 +45,20 @@ def api_weights(w: Weights):
     from paper_2211_00484_b200.api import ModelWeights
 
     return ModelWeights.from_dict(w.p)
+
+
+def decoder_env(m, **env):
+    """A Decoder created with the given RNNTG_* environment switches set (they
+    are read when the model is created), the environment restored after."""
+    from paper_2211_00484_b200.api import Decoder
+
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return Decoder(api_weights(m.w))
+    finally:
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v

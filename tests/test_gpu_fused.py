@@ -14,17 +14,8 @@ pytestmark = pytest.mark.gpu
 
 
 def _decoder(m, fused):
-    from paper_2211_00484_b200.api import Decoder
-
-    old = os.environ.get("RNNTG_FUSED_PE")
-    os.environ["RNNTG_FUSED_PE"] = str(fused)
-    try:
-        return Decoder(H.api_weights(m.w))
-    finally:
-        if old is None:
-            del os.environ["RNNTG_FUSED_PE"]
-        else:
-            os.environ["RNNTG_FUSED_PE"] = old
+    # RNNTG_SLICED=0: host frames take the fused path, not the time-sliced one
+    return H.decoder_env(m, RNNTG_FUSED_PE=str(fused), RNNTG_SLICED="0")
 
 
 @pytest.mark.parametrize("T,B", [(77, 300), (32, 9), (1, 5), (100, 1)])

@@ -1,0 +1,61 @@
+"""The time-sliced host-frame beam path (capi.cu run_sliced): frames copied
+per time slice, K1 over row groups, the beam kernel resumed slice after slice
+from hypothesis sets kept in HBM.  Tokens identical to the oracle, scores
+bit-identical to the single-launch device-frame path (the slicing changes
+launch boundaries only, never the arithmetic)."""
+import numpy as np
+import pytest
+
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize(
+    "T,B,first,cap",
+    [(77, 300, "3", "7"), (200, 1024, "16", "256"), (33, 9, "1", "1"), (17, 5, "16", "256"), (100, 1, "4", "32")],
+)
+def test_sliced_host_frames_match_oracle_and_device_path(T, B, first, cap):
+    import torch
+
+    from paper_2211_00484_b200.api import BeamParams
+
+    m = H.model(V=500, seed=1, blank_bias=0.4)
+    _, enc, splits = H.frames(m, [T] * B, seed0=52000 + T)
+    sliced = H.decoder_env(m, RNNTG_SLICED="1", RNNTG_SLICE_FIRST=first, RNNTG_SLICE_MAX=cap)
+    plain = H.decoder_env(m, RNNTG_SLICED="0", RNNTG_FUSED_PE="0")
+    try:
+        got, sc = sliced.beam_search_batch(enc, splits, BeamParams(beam_size=4))
+        assert sliced.stats()["stream_frames"] == B * T
+        if B <= 300:
+            want, want_sc = H.orc().beam(m.w, enc, splits, beam=4)
+            assert got == want
+            np.testing.assert_allclose(sc, want_sc, rtol=1e-9, atol=0)
+        d_enc = torch.from_numpy(enc).cuda()
+        tok = torch.zeros(max(1, int(splits[-1])), dtype=torch.int32, device="cuda")
+        dsc = torch.zeros(B, dtype=torch.float64, device="cuda")
+        osp, tok, dsc = plain.beam_search_batch(d_enc, splits, BeamParams(beam_size=4), tok, dsc)
+        t = tok.cpu().numpy()
+        assert [t[osp[i] : osp[i + 1]].tolist() for i in range(B)] == got
+        assert np.array_equal(dsc.cpu().numpy(), sc)
+    finally:
+        sliced.close()
+        plain.close()
+
+
+def test_sliced_repeated_calls_and_beam_sizes():
+    """Back-to-back calls on one handle reuse the slice events, the hypothesis
+    state and the frame buffer; every beam capacity (1, 2, 4, 8) resumes."""
+    from paper_2211_00484_b200.api import BeamParams
+
+    m = H.model(V=500, seed=2, blank_bias=0.4)
+    dec = H.decoder_env(m, RNNTG_SLICED="1", RNNTG_SLICE_FIRST="5", RNNTG_SLICE_MAX="11")
+    try:
+        for beam, T, B in [(1, 40, 20), (2, 60, 33), (8, 45, 17), (4, 40, 20)]:
+            _, enc, splits = H.frames(m, [T] * B, seed0=53000 + beam)
+            want, want_sc = H.orc().beam(m.w, enc, splits, beam=beam)
+            got, sc = dec.beam_search_batch(enc, splits, BeamParams(beam_size=beam))
+            assert got == want, beam
+            np.testing.assert_allclose(sc, want_sc, rtol=1e-9, atol=0)
+    finally:
+        dec.close()
