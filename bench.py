@@ -375,7 +375,8 @@ def main():
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        toks_host, scores_host = dec.beam_search_batch(pin, splits, params)
+        # the C ABI's flat result (out_splits, tokens, scores) read back to host memory
+        osp_host, toks_host, scores_host = dec.beam_search_batch(pin, splits, params, as_lists=False)
     e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
@@ -417,8 +418,10 @@ def main():
                 "value": world * B * T / e2e_step,
                 "unit": "frames/s",
                 "h2d_bytes_per_step": int(B * T * D * 4 + (B + 1) * 4),
-                "d2h_bytes_per_step": int(B * T * 4 + B * 4 + B * 8 + 64),
-                "api": "Decoder.beam_search_batch(pinned host frames) -> rnntg_beam_search_batch(RNNTG_MEM_HOST)",
+                # lengths + counters, then the compacted tokens and the scores
+                "d2h_bytes_per_step": int(B * 4 + 128 + 4 * int(osp_host[-1]) + B * 8),
+                "api": "Decoder.beam_search_batch(pinned host frames, as_lists=False) -> "
+                "rnntg_beam_search_batch(RNNTG_MEM_HOST): time-sliced copies, K1 and decode",
             },
             "gpu_launches": int(launches),
             "roofline": {

@@ -366,7 +366,12 @@ class Decoder:
                                              C.byref(capped)))
         return _ragged(osp, tok), int(capped.value)
 
-    def beam_search_batch(self, enc, frame_splits, params: BeamParams = BeamParams(), out_tokens=None, out_scores=None):
+    def beam_search_batch(self, enc, frame_splits, params: BeamParams = BeamParams(), out_tokens=None, out_scores=None,
+                          as_lists=True):
+        """Host frames: (token lists, scores), or with as_lists=False the flat
+        form the C ABI returns, (out_splits, tokens, scores) as numpy arrays
+        (no per-stream Python lists).  Device frames: (out_splits, out_tokens,
+        out_scores) written into the caller's device tensors."""
         p, mem, splits, keep = _frames(enc, frame_splits)
         B = len(splits) - 1
         osp = np.zeros(B + 1, np.int32)
@@ -377,12 +382,14 @@ class Decoder:
             tokp, scp = C.c_void_p(out_tokens.data_ptr()), C.c_void_p(out_scores.data_ptr())
         else:
             cap = 10 if params.max_symbols == NO_SYMBOL_LIMIT else max(1, params.max_symbols)
-            tok = np.zeros(max(1, int(splits[-1]) * cap), np.int32)
+            tok = np.empty(max(1, int(splits[-1]) * cap), np.int32)  # capacity; only osp[-1] are written
             sc = np.zeros(max(1, B), np.float64)
             tokp, scp = _ptr(tok), _ptr(sc)
         _check(self._lib.rnntg_beam_search_batch(self.h, p, _i32p(splits), B, C.byref(bp), mem, _i32p(osp), tokp, scp))
         if mem == MEM_DEVICE:
             return osp, out_tokens, out_scores
+        if not as_lists:
+            return osp, tok[: osp[-1]], sc[:B]
         return _ragged(osp, tok), sc[:B].copy()
 
     def beam_search(self, enc_one, params: BeamParams = BeamParams()):

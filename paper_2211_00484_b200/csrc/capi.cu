@@ -49,7 +49,13 @@ struct rnntg_model_s {
   // RNNTG_SLICE_FIRST / RNNTG_SLICE_MAX: first slice length (frames) and
   // the cap its doubling grows to.
   int sliced = 1;
-  int32_t slice_first = 16, slice_max = 256;
+  int32_t slice_first = 8, slice_max = 512;
+  // RNNTG_SLICE_OVERLAP=1: K1 of slice k+1 on a second stream (fills the
+  // decode tail of slice k) instead of in line on the compute stream.
+  int slice_overlap = 1;
+  int slice_throttle = 1;  // RNNTG_SLICE_THROTTLE: K1 k waits for decode k-2
+  cudaStream_t kstream = nullptr;
+  std::vector<cudaEvent_t> k1_ev;  // one per slice: its pe rows are written
   Scratch hstate;                     // per-stream hypothesis sets between slices
   std::vector<cudaEvent_t> slice_ev;  // one per slice: its frames have landed
   Scratch ready;
@@ -211,15 +217,18 @@ rnntg_status run_fused(rnntg_model_t h, const float* enc, const int32_t* fs, int
   return RNNTG_OK;
 }
 
-// Host frames of uniform length T, decoded in time slices: slice k = frames
-// [cut_k, cut_{k+1}) of every stream.  A copy stream moves each slice with
-// one pitched cudaMemcpy2DAsync and records the slice's event; the compute
-// stream waits for it, projects the slice (K1 over row groups) and decodes it
+// Frames of uniform length T, decoded in time slices: slice k = frames
+// [cut_k, cut_{k+1}) of every stream (lengths slice_first, doubling up to
+// slice_max).  Host frames: a copy stream moves each slice with one pitched
+// cudaMemcpy2DAsync and records the slice's event (device frames: the events
+// are recorded at once).  K1 of the slice (row groups) runs on a side stream
+// once its frames have landed — so it fills the SMs the previous slice's
+// decode is draining — and the compute stream decodes the slice after it
 // (beam kernel resuming from the hypothesis sets the previous slice stored).
-// The copies run ahead on the copy engine, so only the first (short) slice's
-// copy is exposed; K1 and decode keep the unfused kernels' code.
+// Only the first (short) slice's copy is exposed; K1 and decode keep the
+// unfused kernels' machine code.
 template <typename Launch>
-rnntg_status run_sliced(rnntg_model_t h, const float* enc, const int32_t* fs, int32_t B,
+rnntg_status run_sliced(rnntg_model_t h, const float* enc, const int32_t* fs, int32_t B, int32_t mem,
                         int64_t* launches, Launch&& launch) {
   const int32_t D = h->d.D, J = h->d.J, T = fs[1] - fs[0];
   std::vector<int32_t> cut{0};
@@ -237,23 +246,48 @@ rnntg_status run_sliced(rnntg_model_t h, const float* enc, const int32_t* fs, in
   RNNTG_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
   RNNTG_CUDA_TRY(cudaStreamWaitEvent(cs, h->ev[0], 0));  // the previous call is done with h->enc
   const size_t pitch = sizeof(float) * static_cast<size_t>(T) * D;
-  float* d_enc = h->enc.as<float>();
+  const float* d_enc = mem == RNNTG_MEM_HOST ? h->enc.as<float>() : enc;
   for (int k = 0; k < nsl; ++k) {
     const int32_t f0 = cut[k], nf = cut[k + 1] - cut[k];
-    RNNTG_CUDA_TRY(cudaMemcpy2DAsync(d_enc + static_cast<int64_t>(f0) * D, pitch, enc + static_cast<int64_t>(f0) * D,
+    if (mem != RNNTG_MEM_HOST) {  // frames already resident: the slice is ready now
+      RNNTG_CUDA_TRY(cudaEventRecord(h->slice_ev[k], cs));
+      continue;
+    }
+    RNNTG_CUDA_TRY(cudaMemcpy2DAsync(h->enc.as<float>() + static_cast<int64_t>(f0) * D, pitch, enc + static_cast<int64_t>(f0) * D,
                                      pitch, sizeof(float) * static_cast<size_t>(nf) * D, B,
                                      cudaMemcpyHostToDevice, cs));
     RNNTG_CUDA_TRY(cudaEventRecord(h->slice_ev[k], cs));
   }
   RNNTG_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+  cudaStream_t ks = h->stream;
+  if (h->slice_overlap) {
+    if (!h->kstream) RNNTG_CUDA_TRY(cudaStreamCreateWithFlags(&h->kstream, cudaStreamNonBlocking));
+    ks = h->kstream;
+    while (static_cast<int>(h->k1_ev.size()) < 2 * nsl) {  // [k]: K1 k done; [nsl + k]: decode k done
+      cudaEvent_t e;
+      RNNTG_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->k1_ev.push_back(e);
+    }
+    RNNTG_CUDA_TRY(cudaStreamWaitEvent(ks, h->ev[1], 0));  // pe buffer free
+  }
   for (int k = 0; k < nsl; ++k) {
     const int32_t f0 = cut[k], nf = cut[k + 1] - cut[k];
-    RNNTG_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->slice_ev[k], 0));
+    RNNTG_CUDA_TRY(cudaStreamWaitEvent(ks, h->slice_ev[k], 0));
+    // K1 of slice k is issued once decode k-2 is done, i.e. while decode k-1
+    // runs: its CTAs take the SMs that decode drains at its tail instead of
+    // delaying decode k-1's start.
+    if (ks != h->stream && h->slice_throttle && k >= 2)
+      RNNTG_CUDA_TRY(cudaStreamWaitEvent(ks, h->k1_ev[nsl + k - 2], 0));
     RNNTG_CUDA_TRY(rnntg::launch_gemm_exact_grouped(d_enc + static_cast<int64_t>(f0) * D, D, h->d.j_wet, h->d.Jp,
                                                     nullptr, h->pe.as<float>() + static_cast<int64_t>(f0) * J, J,
                                                     static_cast<int64_t>(B) * nf, J, D, false, nullptr, 0, 0, nf,
-                                                    T, h->stream));
+                                                    T, ks));
+    if (ks != h->stream) {
+      RNNTG_CUDA_TRY(cudaEventRecord(h->k1_ev[k], ks));
+      RNNTG_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->k1_ev[k], 0));
+    }
     RNNTG_CUDA_TRY(launch(cut[k], cut[k + 1], h->stream));
+    if (ks != h->stream) RNNTG_CUDA_TRY(cudaEventRecord(h->k1_ev[nsl + k], h->stream));
     *launches += 2;
   }
   h->pipelined = true;  // decode overlaps the copies: the stats report the whole call
@@ -341,16 +375,25 @@ rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
   for (int32_t i = 0; i < B; ++i) out_splits[i + 1] = out_splits[i] + lens[i];
   if (mem == RNNTG_MEM_HOST) {
     if (total > 0) {
-      std::vector<int32_t> slots(total);
-      RNNTG_CUDA_TRY(cudaMemcpyAsync(slots.data(), h->tok.ptr, sizeof(int32_t) * total,
-                                     cudaMemcpyDeviceToHost, h->stream));
+      // Compact on the device, then read back only the hypothesis tokens
+      // (~0.05 per frame here), not every per-frame token slot.
+      const int64_t ntok = out_splits[B];
+      RNNTG_CUDA_TRY(h->out_splits.ensure(sizeof(int32_t) * (B + 1)));
+      RNNTG_CUDA_TRY(h->out_tok.ensure(sizeof(int32_t) * std::max<int64_t>(1, ntok)));
+      RNNTG_CUDA_TRY(cudaMemcpyAsync(h->out_splits.ptr, out_splits, sizeof(int32_t) * (B + 1),
+                                     cudaMemcpyHostToDevice, h->stream));
+      compact_tokens_kernel<<<B, 128, 0, h->stream>>>(h->tok.as<int32_t>(), h->splits.as<int32_t>(),
+                                                      h->out_splits.as<int32_t>(), B, h->slot_mult,
+                                                      h->out_tok.as<int32_t>());
+      RNNTG_CUDA_TRY(cudaGetLastError());
+      ++launches;
+      if (ntok > 0)
+        RNNTG_CUDA_TRY(cudaMemcpyAsync(out_tokens, h->out_tok.ptr, sizeof(int32_t) * ntok,
+                                       cudaMemcpyDeviceToHost, h->stream));
       if (out_scores)
         RNNTG_CUDA_TRY(cudaMemcpyAsync(out_scores, h->score.ptr, sizeof(double) * B,
                                        cudaMemcpyDeviceToHost, h->stream));
       RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
-      for (int32_t i = 0; i < B; ++i)
-        std::memcpy(out_tokens + out_splits[i], slots.data() + static_cast<int64_t>(fs[i]) * h->slot_mult,
-                    sizeof(int32_t) * lens[i]);
     } else if (out_scores && B > 0) {
       RNNTG_CUDA_TRY(cudaMemcpy(out_scores, h->score.ptr, sizeof(double) * B, cudaMemcpyDeviceToHost));
     }
@@ -446,6 +489,8 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
   if (const char* e = std::getenv("RNNTG_SLICED")) h->sliced = std::atoi(e);
   if (const char* e = std::getenv("RNNTG_SLICE_FIRST")) h->slice_first = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RNNTG_SLICE_MAX")) h->slice_max = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("RNNTG_SLICE_OVERLAP")) h->slice_overlap = std::atoi(e);
+  if (const char* e = std::getenv("RNNTG_SLICE_THROTTLE")) h->slice_throttle = std::atoi(e);
   if (const char* gc = std::getenv("RNNTG_GREEDY_CLUSTER")) h->greedy_cluster = std::atoi(gc) != 0;
   rnntg::DeviceModel& d = h->d;
   d.V = V;
@@ -539,6 +584,8 @@ rnntg_status rnntg_model_destroy(rnntg_model_t h) {
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : h->slice_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->k1_ev) cudaEventDestroy(e);
+  if (h->kstream) cudaStreamDestroy(h->kstream);
   for (int c = 0; c < 4; ++c) {
     if (h->cstream[c]) cudaStreamDestroy(h->cstream[c]);
     if (h->done[c]) cudaEventDestroy(h->done[c]);
@@ -758,10 +805,10 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       a.beam_impl = h->beam_impl;
       return a;
     };
-    const bool sliced = exact && !ws && h->beam_impl == 1 && h->sliced > 0 && mem == RNNTG_MEM_HOST && uniform &&
-                        fs[1] - fs[0] > h->slice_first;
+    const bool sliced = exact && !ws && h->beam_impl == 1 && uniform && fs[1] - fs[0] > h->slice_first &&
+                        ((mem == RNNTG_MEM_HOST && h->sliced > 0) || (mem == RNNTG_MEM_DEVICE && h->sliced > 1));
     if (sliced) {
-      st = run_sliced(h, enc, fs, B, &launches, [&](int32_t t0, int32_t t1, cudaStream_t cs) {
+      st = run_sliced(h, enc, fs, B, mem, &launches, [&](int32_t t0, int32_t t1, cudaStream_t cs) {
         rnntg::DecodeArgs a = args(0, B);
         a.t0 = t0;
         a.t1 = t1;

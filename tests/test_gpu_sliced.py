@@ -59,3 +59,31 @@ def test_sliced_repeated_calls_and_beam_sizes():
             np.testing.assert_allclose(sc, want_sc, rtol=1e-9, atol=0)
     finally:
         dec.close()
+
+
+def test_sliced_device_frames_opt_in():
+    """RNNTG_SLICED=2 also slices device-resident frames (K1 per slice on the
+    side stream): the same tokens and bit-identical scores as K1 + decode."""
+    import torch
+
+    from paper_2211_00484_b200.api import BeamParams
+
+    m = H.model(V=500, seed=3, blank_bias=0.4)
+    T, B = 90, 160
+    _, enc, splits = H.frames(m, [T] * B, seed0=54000)
+    d_enc = torch.from_numpy(enc).cuda()
+    outs = []
+    for env in ({"RNNTG_SLICED": "2", "RNNTG_SLICE_FIRST": "4", "RNNTG_SLICE_MAX": "16"}, {"RNNTG_SLICED": "0"}):
+        dec = H.decoder_env(m, **env)
+        try:
+            tok = torch.zeros(B * T, dtype=torch.int32, device="cuda")
+            dsc = torch.zeros(B, dtype=torch.float64, device="cuda")
+            osp, tok, dsc = dec.beam_search_batch(d_enc, splits, BeamParams(beam_size=4), tok, dsc)
+            t = tok.cpu().numpy()
+            outs.append(([t[osp[i] : osp[i + 1]].tolist() for i in range(B)], dsc.cpu().numpy()))
+        finally:
+            dec.close()
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1], outs[1][1])
+    want, _ = H.orc().beam(m.w, enc[: 20 * T], splits[:21], beam=4)
+    assert outs[0][0][:20] == want
