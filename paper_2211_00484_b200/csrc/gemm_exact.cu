@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kThreads)
     const int buf = c & 1;
     if (c + 1 < nk) gload((c + 1) * BK);
     const int kk_end = min(BK, K - c * BK);
-    for (int kk = 0; kk < kk_end; ++kk) {
+    auto step = [&](int kk) {
       const float4 x4 = *reinterpret_cast<const float4*>(&Xs[buf][kk][tm * 4]);
       const float4 wa = *reinterpret_cast<const float4*>(&Ws[buf][kk][tn * 4]);
       const float4 wb =
@@ -127,6 +127,12 @@ __global__ void __launch_bounds__(kThreads)
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = fadd(acc[i][j], fmul(wv[j], xv[i]));
+    };
+    if (kk_end == BK) {  // full chunk: straight-line code, no loop overhead
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) step(kk);
+    } else {
+      for (int kk = 0; kk < kk_end; ++kk) step(kk);
     }
     if (c + 1 < nk) {
       sstore(buf ^ 1);
