@@ -352,9 +352,14 @@ __device__ uint32_t gemm_bal_x(const WPipe p, uint32_t g, uint32_t hl, int R, in
                                const float* __restrict__ bias, int K, int nc, long long* wc);
 #endif
 
+// Rows from which the SMSP-balanced tiling is used; below, the uniform
+// tilings of gemm_pass (up to 16 equal items of 4 rows x 32*TN columns).
+#ifndef RNNTG_BAL_MIN_R
+#define RNNTG_BAL_MIN_R 5
+#endif
 __device__ __forceinline__ void joiner_gemm(const ModelView& m, const WPipe& p,
                                             uint32_t& g, float* HL, int R, long long* wc = nullptr) {
-  if (m.Vp == 512 && R > 4) {
+  if (m.Vp == 512 && R >= RNNTG_BAL_MIN_R) {
 #ifdef RNNTG_GEMM_EXTERN
     g = gemm_bal_x(p, g, smem_u32(HL), R, m.Vp, m.out_b, m.J, p.nc, wc);
 #else
