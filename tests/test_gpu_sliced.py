@@ -87,3 +87,37 @@ def test_sliced_device_frames_opt_in():
     assert np.array_equal(outs[0][1], outs[1][1])
     want, _ = H.orc().beam(m.w, enc[: 20 * T], splits[:21], beam=4)
     assert outs[0][0][:20] == want
+
+
+def test_sliced_bench_scale_matches_single_launch_and_oracle_sample():
+    """The bench shape (1024 streams x 1000 frames, default slices 8 ... 496):
+    sliced host path == K1 + one decode launch on device frames (tokens and
+    scores bit-identical), and the first 8 streams == the reference."""
+    import torch
+
+    from paper_2211_00484_b200.api import BeamParams
+
+    m = H.model(V=500, seed=1, blank_bias=0.4)
+    B, T, U = 1024, 1000, 8
+    rng = np.random.default_rng(7)
+    enc_u = np.tanh(rng.standard_normal((U, T, 512)).astype(np.float32) * 0.7)
+    enc = np.ascontiguousarray(np.concatenate([enc_u] * (B // U)).reshape(B * T, 512))
+    splits = (np.arange(B + 1) * T).astype(np.int32)
+    sliced = H.decoder_env(m, RNNTG_SLICED="1")
+    plain = H.decoder_env(m, RNNTG_SLICED="0", RNNTG_FUSED_PE="0")
+    try:
+        osp, tok, sc = sliced.beam_search_batch(torch.from_numpy(enc).pin_memory(), splits,
+                                                BeamParams(beam_size=4), as_lists=False)
+        d_enc = torch.from_numpy(enc).cuda()
+        dtok = torch.zeros(B * T, dtype=torch.int32, device="cuda")
+        dsc = torch.zeros(B, dtype=torch.float64, device="cuda")
+        osp2, dtok, dsc = plain.beam_search_batch(d_enc, splits, BeamParams(beam_size=4), dtok, dsc)
+        assert np.array_equal(osp, osp2)
+        assert np.array_equal(tok, dtok.cpu().numpy()[: osp2[-1]])
+        assert np.array_equal(sc, dsc.cpu().numpy())
+        want, want_sc = H.orc().beam(m.w, enc[: U * T], splits[: U + 1], beam=4)
+        assert [tok[osp[i] : osp[i + 1]].tolist() for i in range(U)] == want
+        np.testing.assert_allclose(sc[:U], want_sc, rtol=1e-9, atol=0)
+    finally:
+        sliced.close()
+        plain.close()
