@@ -430,6 +430,9 @@ __device__ __forceinline__ uint64_t tok_key(float v, int k) {
   return (static_cast<uint64_t>(ord_key(v + 0.0f)) << 32) | static_cast<uint32_t>(~k);  // -0 -> +0
 }
 
+#ifndef RNNTG_SL_STEP_NI
+#define RNNTG_SL_STEP_NI 1
+#endif
 #ifndef RNNTG_SL_RR_NI
 #define RNNTG_SL_RR_NI 1
 #endif
@@ -684,6 +687,16 @@ __device__ void beam_stream_step(const ModelView& m, Hyps& h, BeamCand* cand, ui
       if (tok != 0) tokens[fs + --pos] = tok;
     }
   }
+}
+
+// Out-of-line call for the time-sliced instantiation (RNNTG_SL_STEP_NI).
+template <int BCAP>
+__device__ __noinline__ void beam_stream_step_ni(const ModelView& m, Hyps& h, BeamCand* cand, uint32_t* bp, int t,
+                                                 int T, int fs, int beam, int merge_log, int length_norm,
+                                                 int max_total, RowRes rr, int32_t* tokens, int32_t* out_len,
+                                                 double* out_score, unsigned long long* ties) {
+  beam_stream_step<BCAP>(m, h, cand, bp, t, T, fs, beam, merge_log, length_norm, max_total, rr, tokens, out_len,
+                         out_score, ties);
 }
 
 // Fused encoder projection (joiner_project_enc, model.hpp:263-271):
@@ -973,10 +986,16 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       const int32_t fs = frame_splits[s0 + i];
       const int32_t T = frame_splits[s0 + i + 1] - fs;
       if (t >= T) continue;
-      beam_stream_step<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
-                             backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs, beam,
-                             merge_log, length_norm, max_total, rr, tokens, lengths + s0 + i,
-                             scores + s0 + i, &st[4]);
+      if constexpr (SL && RNNTG_SL_STEP_NI)
+        beam_stream_step_ni<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
+                                  backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs, beam,
+                                  merge_log, length_norm, max_total, rr, tokens, lengths + s0 + i,
+                                  scores + s0 + i, &st[4]);
+      else
+        beam_stream_step<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
+                               backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs, beam,
+                               merge_log, length_norm, max_total, rr, tokens, lengths + s0 + i,
+                               scores + s0 + i, &st[4]);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
