@@ -430,6 +430,12 @@ __device__ __forceinline__ uint64_t tok_key(float v, int k) {
   return (static_cast<uint64_t>(ord_key(v + 0.0f)) << 32) | static_cast<uint32_t>(~k);  // -0 -> +0
 }
 
+#ifndef RNNTG_MAIN_STEP_NI
+#define RNNTG_MAIN_STEP_NI 0
+#endif
+#ifndef RNNTG_MAIN_RR_NI
+#define RNNTG_MAIN_RR_NI 0
+#endif
 #ifndef RNNTG_SL_STEP_NI
 #define RNNTG_SL_STEP_NI 1
 #endif
@@ -962,7 +968,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     // token asc).  Each lane keeps a sorted local top-kMaxBeam, then `beam`
     // warp-wide pops.
     const RowRes rr{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
-    if constexpr (SL && RNNTG_SL_RR_NI) {
+    if constexpr ((SL && RNNTG_SL_RR_NI) || (!SL && RNNTG_MAIN_RR_NI)) {
       if (R <= kWarps) {
         if (warp < R) beam_row_reduce_ni<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr);
       } else if (warp < R - kWarps || warp < kWarps) {
@@ -986,7 +992,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       const int32_t fs = frame_splits[s0 + i];
       const int32_t T = frame_splits[s0 + i + 1] - fs;
       if (t >= T) continue;
-      if constexpr (SL && RNNTG_SL_STEP_NI)
+      if constexpr ((SL && RNNTG_SL_STEP_NI) || (!SL && RNNTG_MAIN_STEP_NI))
         beam_stream_step_ni<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
                                   backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs, beam,
                                   merge_log, length_norm, max_total, rr, tokens, lengths + s0 + i,
