@@ -53,7 +53,7 @@ struct rnntg_model_s {
   // RNNTG_SLICE_OVERLAP=1: K1 of slice k+1 on a second stream (fills the
   // decode tail of slice k) instead of in line on the compute stream.
   int slice_overlap = 1;
-  int slice_throttle = 1;  // RNNTG_SLICE_THROTTLE: K1 k waits for decode k-2
+  int slice_throttle = 1;  // RNNTG_SLICE_THROTTLE=n: K1 k waits for decode k-1-n (0: no wait)
   cudaStream_t kstream = nullptr;
   std::vector<cudaEvent_t> k1_ev;  // one per slice: its pe rows are written
   Scratch hstate;                     // per-stream hypothesis sets between slices
@@ -276,8 +276,8 @@ rnntg_status run_sliced(rnntg_model_t h, const float* enc, const int32_t* fs, in
     // K1 of slice k is issued once decode k-2 is done, i.e. while decode k-1
     // runs: its CTAs take the SMs that decode drains at its tail instead of
     // delaying decode k-1's start.
-    if (ks != h->stream && h->slice_throttle && k >= 2)
-      RNNTG_CUDA_TRY(cudaStreamWaitEvent(ks, h->k1_ev[nsl + k - 2], 0));
+    if (ks != h->stream && h->slice_throttle > 0 && k >= 1 + h->slice_throttle)
+      RNNTG_CUDA_TRY(cudaStreamWaitEvent(ks, h->k1_ev[nsl + k - 1 - h->slice_throttle], 0));
     RNNTG_CUDA_TRY(rnntg::launch_gemm_exact_grouped(d_enc + static_cast<int64_t>(f0) * D, D, h->d.j_wet, h->d.Jp,
                                                     nullptr, h->pe.as<float>() + static_cast<int64_t>(f0) * J, J,
                                                     static_cast<int64_t>(B) * nf, J, D, false, nullptr, 0, 0, nf,
