@@ -430,6 +430,10 @@ __device__ __forceinline__ uint64_t tok_key(float v, int k) {
   return (static_cast<uint64_t>(ord_key(v + 0.0f)) << 32) | static_cast<uint32_t>(~k);  // -0 -> +0
 }
 
+#ifndef RNNTG_LSE_UNROLL
+#define RNNTG_LSE_UNROLL 2
+#endif
+constexpr int kLseUnroll = RNNTG_LSE_UNROLL;  // exp-sum loop trips unrolled (row reduction)
 #ifndef RNNTG_MAIN_STEP_NI
 #define RNNTG_MAIN_STEP_NI 0
 #endif
@@ -494,7 +498,7 @@ __device__ __forceinline__ void beam_row_reduce_n(const float* HL, int Vp, int V
   double s[NR];
 #pragma unroll
   for (int j = 0; j < NR; ++j) s[j] = 0.0;
-#pragma unroll 4
+#pragma unroll kLseUnroll
   for (int k = lane; k < V; k += 32)
 #pragma unroll
     for (int j = 0; j < NR; ++j) s[j] += exp_lse(static_cast<double>(L[j][k]) - static_cast<double>(M[j]));
