@@ -430,6 +430,10 @@ __device__ __forceinline__ uint64_t tok_key(float v, int k) {
   return (static_cast<uint64_t>(ord_key(v + 0.0f)) << 32) | static_cast<uint32_t>(~k);  // -0 -> +0
 }
 
+#ifndef RNNTG_TOPK_UNROLL
+#define RNNTG_TOPK_UNROLL 2  // 0: compiler's choice
+#endif
+constexpr int kTopkUnroll = RNNTG_TOPK_UNROLL > 0 ? RNNTG_TOPK_UNROLL : 1;
 #ifndef RNNTG_LSE_UNROLL
 #define RNNTG_LSE_UNROLL 2
 #endif
@@ -460,6 +464,9 @@ __device__ __forceinline__ void beam_row_reduce_n(const float* HL, int Vp, int V
 #pragma unroll
     for (int q = 0; q < BCAP; ++q) t[j][q] = 0;
   }
+#if RNNTG_TOPK_UNROLL > 0
+#pragma unroll kTopkUnroll
+#endif
   for (int k = lane; k < V; k += 32) {
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
