@@ -3,25 +3,37 @@
 D=J=E=512, T=1000 frames per stream, 1024 streams per GPU.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--scaling weak|strong]
+
+Inputs are the reference's own: init_model(seed 0) weights
+with blank bias +0.4 on out_b[0], and per-stream features
+DetRng(7000 + global stream index).gaussian() [T x 80], regenerated bit for
+bit by librnntg's host generators (rnntg_init_model_weights,
+rnntg_gaussian_features) and run through the GPU encoder (bit-exact
+encoder_forward).  The reference arm decodes a prefix of the very same
+streams with the very same model.
 
 One step = one pass of the hot path (decoder-context lookup, exact joiner,
-log-softmax, beam pruning / merging, traceback) over one batch of 1024
-synthetic streams whose encoder frames are already resident in HBM.  Under
-torchrun each rank decodes its own 1024 streams (streams are independent;
-weak scaling, no collective on the data path); the timed region is
-barrier + synchronize on both sides and the reported time is the max over
-ranks.  Rank 0 prints ONE JSON line.
+log-softmax, beam pruning / merging, traceback) over one batch of streams
+whose encoder frames are already resident in HBM (`value`), or which come
+from pinned host memory through the C ABI with the results read back and
+gathered on rank 0 (`e2e`).  --gpus N > 1 launches N ranks (torchrun, one
+per GPU, NCCL); --scaling weak (default) gives every rank 1024 streams of its
+own, --scaling strong cuts one batch of 1024 streams across the ranks.
+Streams are independent, so the only collective is the final result gather
+(inside `e2e`); timing is barrier + synchronize on both sides, max over ranks.
 
 `--impl reference` times the reference's own CPU implementation
 (rnnt-kit beam_search, compiled from /root/reference into
 oracle/_ref/librnnt_ref.so) on this host's cores over a bounded sample of the
-same workload.
+same workload (rank 0 only).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -38,48 +50,44 @@ T_FRAMES = 1000
 BATCH_PER_GPU = 1024
 BEAM = 4
 BLANK_BIAS = 0.4
+MODEL_SEED = 0  # ModelConfig::seed default (model.hpp:36)
+FEAT_SEED0 = 7000  # stream g's features: DetRng(FEAT_SEED0 + g)
 METRIC = "decoded frames/sec (and RTF) at beam=4, batch 1024, 1/2/4/8 B200 vs CPU ref"
-WORKLOAD = "modified_beam_search beam=4 max_symbols=1, 1024 streams/GPU x T=1000, V=500 D=E=J=512 (config 5 point)"
+DATA = (
+    "synthetic, the reference's own inputs: init_model(seed 0) weights + blank bias 0.4 on out_b[0], "
+    "features DetRng(7000+stream).gaussian() [T x 80] through the toy encoder (bit-exact on GPU)"
+)
 
 
-def synthetic_weights(seed=1):
-    """init_model's distribution (model.hpp:129-169: uniform +-1/sqrt(fan_in)),
-    seeded numpy PCG64, blank bias on out_b[0]."""
-    rng = np.random.Generator(np.random.PCG64(seed))
-
-    def u(shape, fan_in):
-        s = 1.0 / np.sqrt(fan_in)
-        return rng.uniform(-s, s, size=shape).astype(np.float32)
-
-    p = {
-        "enc_w1": u((D, F), F),
-        "enc_b1": u((1, D), F),
-        "enc_w2": u((D, D), D),
-        "enc_b2": u((1, D), D),
-        "emb": u((V, E), E),
-        "ctx_w": u((E, 2 * E), 2 * E),
-        "ctx_b": u((1, E), 2 * E),
-        "j_we": u((J, D), D),
-        "j_wd": u((J, E), E),
-        "j_b": u((1, J), D),
-        "out_w": u((V, J), J),
-        "out_b": u((1, V), J),
-    }
-    p["out_b"][0, 0] += BLANK_BIAS
-    return p
+def workload(scaling, world, batch):
+    per = batch if scaling == "weak" else f"{batch}/{world}"
+    return (
+        f"modified_beam_search beam=4 max_symbols=1, {per} streams/GPU x T=1000, "
+        f"V=500 D=E=J=512 (config 5 point, {scaling} scaling)"
+    )
 
 
-def synthetic_frames(dec, B, T, seed, device):
-    """Encoder frames of the reference's toy encoder: features ~ N(0,1)
-     through rnntg_encoder_forward on the GPU (bit-exact
-    encoder_forward).  Returns the frames in HBM and the frame splits."""
+def reference_weights():
+    """init_model(ModelConfig{500, 80, 512, 512, 512, seed 0}) + blank bias,
+    bit-identical to the reference (librnntg host generator)."""
+    from paper_2211_00484_b200.api import init_model_weights
+
+    return init_model_weights(V, F, D, E, J, seed=MODEL_SEED, blank_bias=BLANK_BIAS)
+
+
+def synthetic_frames(dec, g0, B, T, device):
+    """Encoder frames of global streams g0 .. g0+B-1: DetRng features on the
+    host (bit-identical to the reference's), the toy encoder on the GPU
+    (rnntg_encoder_forward, bit-exact).  Returns (frames in HBM, splits)."""
     import torch
 
-    g = torch.Generator(device=device).manual_seed(seed)
-    feats = torch.randn((B * T, F), generator=g, device=device, dtype=torch.float32)
+    from paper_2211_00484_b200.api import gaussian_features
+
+    feats = torch.from_numpy(gaussian_features(FEAT_SEED0 + g0, B, T, F)).to(device)
     splits = (np.arange(B + 1, dtype=np.int64) * T).astype(np.int32)
     enc = torch.empty((B * T, D), dtype=torch.float32, device=device)
     dec.encoder_forward(feats, splits, enc)
+    torch.cuda.synchronize()
     del feats
     return enc, splits
 
@@ -152,17 +160,19 @@ class ClockSampler:
         }
 
 
-def fp32_nonfused_peak_tflops():
-    """Measured non-fused fp32 (FMUL+FADD) rate of this GPU: the bound of the
-    exact joiner, which may not fuse."""
+def fp32_probe():
+    """Measured FMUL+FADD / FFMA rates of this GPU (tools/fp32_peak.cu), context
+    for the nominal peak; None if the probe is unavailable."""
     exe = os.path.join(ROOT, "tools", "fp32_peak")
-    if not os.path.exists(exe):
-        src = os.path.join(ROOT, "tools", "fp32_peak.cu")
-        subprocess.run(
-            ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", exe, src], check=True, capture_output=True
-        )
-    out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout
-    return json.loads(out.strip().splitlines()[-1])
+    try:
+        if not os.path.exists(exe):
+            src = os.path.join(ROOT, "tools", "fp32_peak.cu")
+            subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", exe, src],
+                           check=True, capture_output=True)
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception:
+        return None
 
 
 def load_traffic():
@@ -175,34 +185,53 @@ def load_traffic():
     return None
 
 
-def cpu_baseline(threads, streams, T):
-    """The reference's beam_search on this host (oracle/_ref): a bounded
-    sample of the same workload, one utterance per thread task (the
-    reference CLI's parallel_for).  Includes the reference's internal encoder,
-    which is timed alone too and subtracted for the search-only rate."""
-    from oracle.py_oracle import Reference
+def cpu_baseline_and_parity(threads, streams, T, gpu_tokens, gpu_scores):
+    """The reference's beam_search on this host (oracle/_ref) over the first
+    `streams` streams of the GPU workload (same model, same features): a
+    bounded sample, one utterance per thread task (the CLI's parallel_for).
+    Includes the reference's internal encoder, which is timed alone too and
+    subtracted for the search-only rate.  The same run is the bench's parity
+    sample: the GPU arm's tokens for those streams must equal the
+    reference's, and its scores the oracle restatement's (the reference's
+    beam_search returns tokens only)."""
+    from oracle.py_oracle import Oracle, Reference
 
     ref = Reference()
-    m = ref.model(V, F, D, E, J, 1, BLANK_BIAS)
-    feats = np.concatenate([ref.features(5000 + i, T, F) for i in range(streams)])
+    m = ref.model(V, F, D, E, J, MODEL_SEED, BLANK_BIAS)
+    feats = np.concatenate([ref.features(FEAT_SEED0 + i, T, F) for i in range(streams)])
     splits = (np.arange(streams + 1) * T).astype(np.int32)
     t0 = time.perf_counter()
-    m.encoder(feats, splits, threads=threads)
+    enc = m.encoder(feats, splits, threads=threads)
     t_enc = time.perf_counter() - t0
     t0 = time.perf_counter()
-    m.beam(feats, splits, beam=BEAM, threads=threads)
+    want = m.beam(feats, splits, beam=BEAM, threads=threads)
     t_all = time.perf_counter() - t0
     frames = streams * T
-    return {
+    base = {
         "value": frames / max(1e-9, t_all - t_enc),
         "unit": "frames/s",
         "cores": threads,
         "kind": "reference",
-        "sample": f"{streams} streams x T={T} (beam 4, V=500), reference beam_search via parallel_for; "
-        f"search-only (encoder {t_enc:.2f}s subtracted from {t_all:.2f}s)",
+        "sample": f"first {streams} streams of the workload x T={T} (beam 4, V=500), reference beam_search via "
+        f"parallel_for; search-only (encoder {t_enc:.2f}s subtracted from {t_all:.2f}s)",
         "value_with_encoder": frames / t_all,
         "rtf": (t_all - t_enc) / (frames * 0.01),
     }
+    _, osc = Oracle().beam(m.w, enc, splits, beam=BEAM, threads=threads)
+    got = gpu_tokens[:streams]
+    same = [a == b for a, b in zip(got, want)]
+    rel = np.abs(np.asarray(gpu_scores[:streams]) - osc) / np.maximum(1e-300, np.abs(osc))
+    parity = {
+        "streams": streams,
+        "frames_per_stream": T,
+        "against": "tokens: compiled reference beam_search (oracle/_ref); scores: oracle restatement",
+        "tokens_identical_streams": int(sum(same)),
+        "tokens_identical": bool(all(same)),
+        "max_score_rel_err": float(rel.max()) if len(rel) else 0.0,
+        "score_tolerance": 1e-9,
+        "reference_tokens_per_frame": sum(len(x) for x in want) / frames,
+    }
+    return base, parity
 
 
 def run_reference(args):
@@ -214,11 +243,11 @@ def run_reference(args):
     from oracle.py_oracle import Reference
 
     ref = Reference()
-    m = ref.model(V, F, D, E, J, 1, BLANK_BIAS)
-    feats = np.concatenate([ref.features(7000 + i, T, F) for i in range(streams)])
+    m = ref.model(V, F, D, E, J, MODEL_SEED, BLANK_BIAS)
+    feats = np.concatenate([ref.features(FEAT_SEED0 + i, T, F) for i in range(streams)])
     splits = (np.arange(streams + 1) * T).astype(np.int32)
     for _ in range(args.warmup):
-        m.beam(feats[: T * min(streams, threads)], splits[: min(streams, threads) + 1], beam=BEAM, threads=threads)
+        m.beam(feats, splits, beam=BEAM, threads=threads)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
@@ -226,21 +255,26 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     ms = 1e3 * statistics.mean(times)
     value = streams * T / (ms * 1e-3)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     line = {
         "impl": "reference",
         "metric": METRIC,
         "value": value,
         "unit": "frames/s",
-        "n_gpus": args.gpus,
+        "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f32 logits / f64 scores",
-        "data": "synthetic features (DetRng gaussian) through the reference encoder; reference init_model weights",
-        "config": {"workload": WORKLOAD, "sample_per_step": f"{streams} streams x T={T}", "threads": threads},
+        "data": DATA,
+        "config": {
+            "workload": workload(args.scaling, world, args.batch),
+            "sample_per_step": f"first {streams} streams of the workload x T={T} (same model and features as the GPU arm)",
+            "threads": threads,
+        },
         "rtf": (ms * 1e-3) / (streams * T * 0.01),
         "cpu_baseline": {
             "value": value,
@@ -255,18 +289,42 @@ def run_reference(args):
     return 0
 
 
-def main():
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def torchrun_cmd(argv, n):
+    """The command that runs this script on n ranks of one node (one per GPU)."""
+    return [
+        sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+        "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv,
+    ]
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=BATCH_PER_GPU)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--batch", type=int, default=BATCH_PER_GPU,
+                    help="streams per GPU (weak) or in total (strong)")
     ap.add_argument("--frames", type=int, default=T_FRAMES)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
+    ap.add_argument("--no-bf16", action="store_true")
+    args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (rank 0 prints the line)
+        env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "WARN"))
+        return subprocess.run(torchrun_cmd(argv, args.gpus), env=env).returncode
 
     import torch
     import torch.distributed as dist
@@ -275,14 +333,19 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    device = f"cuda:{local}"
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2211_00484_b200.api import BeamParams, Decoder, ModelWeights
+    from paper_2211_00484_b200.shard import gather_flat, plan_streams
 
-    B, T = args.batch, args.frames
+    T = args.frames
+    g0, g1 = plan_streams(world, rank, args.batch, args.scaling)
+    B = g1 - g0
+    total_streams = args.batch * (world if args.scaling == "weak" else 1)
     t0 = time.perf_counter()
-    weights = synthetic_weights()
+    weights = reference_weights()
     dec = Decoder(ModelWeights.from_dict(weights), device=local)
     torch.cuda.synchronize()
     model_prep_s = time.perf_counter() - t0
@@ -290,11 +353,10 @@ def main():
     stream = torch.cuda.current_stream()
     dec.set_stream(stream.cuda_stream)
 
-    d_enc, splits = synthetic_frames(dec, B, T, seed=100 + rank, device=f"cuda:{local}")
-    torch.cuda.synchronize()
-    enc = d_enc.cpu().numpy()
-    tok = torch.zeros(B * T, dtype=torch.int32, device=f"cuda:{local}")
-    sc = torch.zeros(B, dtype=torch.float64, device=f"cuda:{local}")
+    d_enc, splits = synthetic_frames(dec, g0, B, T, device)
+    enc_host = d_enc.cpu().pin_memory()
+    tok = torch.zeros(max(1, B * T), dtype=torch.int32, device=device)
+    sc = torch.zeros(max(1, B), dtype=torch.float64, device=device)
     params = BeamParams(beam_size=BEAM)
 
     def step():
@@ -325,21 +387,21 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     elapsed_ms = ev0.elapsed_time(ev1)
-    tokens_emitted = int(dec.stats()["stream_frames"])  # placeholder overwritten below
     osp, _, _ = step()
+    torch.cuda.synchronize()
+    ex_osp = osp.copy()
+    ex_tok = tok.cpu().numpy()
+    ex_sc = sc.cpu().numpy()
     tokens_emitted = int(osp[-1])
-    t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device=f"cuda:{local}")
+    t_max = torch.tensor([elapsed_ms], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t_max.item())
-    ms_per_step = elapsed_ms / args.steps
-    value = world * B * T / (ms_per_step * 1e-3)
+    ms_per_step = float(t_max.item()) / args.steps
+    value = total_streams * T / (ms_per_step * 1e-3)
 
     # ---- bf16 tcgen05 joiner variant (reported separately, not token-exact) ----
     bf16 = None
-    if rank == 0:
-        ex_osp = osp.copy()
-        ex_tok = tok.cpu().numpy()
+    if rank == 0 and not args.no_bf16:
         dec.set_joiner_mode("bf16")
         step()
         torch.cuda.synchronize()
@@ -366,29 +428,31 @@ def main():
             "joiner": "tcgen05.mma kind::f16 (bf16 x bf16 -> fp32 TMEM), swap-AB M=128 vocab tiles, N=16/32 rows",
         }
 
-    # ---- e2e through the public API with pinned host buffers ----
-    pin = torch.from_numpy(enc).pin_memory()
+    # ---- e2e through the public API: pinned host frames in, host results out, gathered on rank 0 ----
     e2e_steps = max(1, min(args.steps, 3))
-    dec.beam_search_batch(pin, splits, params)
+    dec.beam_search_batch(enc_host, splits, params)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         # the C ABI's flat result (out_splits, tokens, scores) read back to host memory
-        osp_host, toks_host, scores_host = dec.beam_search_batch(pin, splits, params, as_lists=False)
-    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=f"cuda:{local}")
+        osp_h, toks_h, scores_h = dec.beam_search_batch(enc_host, splits, params, as_lists=False)
+        g_osp, g_tok, g_sc = gather_flat(osp_h, toks_h, scores_h, device=device)
+    e2e_s = torch.tensor([(time.perf_counter() - t0) / e2e_steps], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_step = float(e2e_s.item())
 
-    line = None
     if rank == 0:
-        peak = fp32_nonfused_peak_tflops()
         mean_decode_ms = statistics.mean(decode_ms)
         rows_per_step = rows / args.steps
         flops = 2.0 * rows_per_step * V * J  # exact joiner output projection per launch
         achieved = flops / (mean_decode_ms * 1e-3) / 1e12
+        sm_max = clk.summary().get("sm_max_mhz") or 1965.0
+        nsm = torch.cuda.get_device_properties(local).multi_processor_count
+        peak = nsm * 128 * sm_max * 1e6 / 1e12  # FP32 lanes x clock: one FMUL or FADD per lane per cycle
+        probe = fp32_probe()
         traffic = load_traffic()
         line = {
             "metric": METRIC,
@@ -399,43 +463,46 @@ def main():
             "warmup": max(args.warmup, 3),
             "ms_per_step": ms_per_step,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": "f32 (exact non-fused joiner) / f64 scores",
-            "data": "synthetic: features ~ N(0,1) through the reference toy encoder (bit-exact on GPU), frames resident in HBM; init_model-distributed random weights (numpy PCG64), blank bias 0.4",
+            "data": DATA + "; frames resident in HBM for `value`",
             "config": {
-                "workload": WORKLOAD,
-                "global_batch": world * B,
+                "workload": workload(args.scaling, world, args.batch),
+                "global_batch": total_streams,
                 "batch_per_gpu": B,
                 "frames_per_stream": T,
                 "beam": BEAM,
                 "vocab": V,
-                "parallelism": f"dp{world} (streams sharded, no data-path collective)",
+                "parallelism": f"dp{world} (streams sharded, no data-path collective; final result gather in e2e)",
                 "l2": "inputs larger than L2 (enc %.1f GB per step per GPU)" % (B * T * D * 4 / 1e9),
             },
-            "rtf": (ms_per_step * 1e-3) / (B * T * 0.01),
+            "rtf": (ms_per_step * 1e-3) / (total_streams * T * 0.01),
             "e2e": {
-                "value": world * B * T / e2e_step,
+                "value": total_streams * T / e2e_step,
                 "unit": "frames/s",
                 "h2d_bytes_per_step": int(B * T * D * 4 + (B + 1) * 4),
                 # lengths + counters, then the compacted tokens and the scores
-                "d2h_bytes_per_step": int(B * 4 + 128 + 4 * int(osp_host[-1]) + B * 8),
+                "d2h_bytes_per_step": int(B * 4 + 128 + 4 * int(osp_h[-1]) + B * 8),
                 "api": "Decoder.beam_search_batch(pinned host frames, as_lists=False) -> "
-                "rnntg_beam_search_batch(RNNTG_MEM_HOST): time-sliced copies, K1 and decode",
+                "rnntg_beam_search_batch(RNNTG_MEM_HOST): time-sliced copies, K1 and decode"
+                + ("; results gathered on rank 0 (shard.gather_flat, NCCL)" if world > 1 else ""),
+                "gathered_streams": int(len(g_sc)) if g_sc is not None else None,
             },
             "gpu_launches": int(launches),
             "roofline": {
                 "bound": "fp32-nonfused",
                 "achieved": achieved,
-                "peak": peak["nonfused_tflops"],
+                "peak": peak,
                 "unit": "TFLOP/s",
-                "frac": achieved / peak["nonfused_tflops"],
+                "frac": achieved / peak,
                 "traffic": traffic.get("bytes_per_launch") if traffic else None,
                 "kernel": "beam_kernel (persistent decode; excludes the pe projection GEMM)",
                 "algorithmic": "2*V*J FLOP per joiner row (V=500, J=512); rows counted on device",
-                "peak_source": "tools/fp32_peak.cu measured at run time: FMUL+FADD (the reference's "
-                "unfused sequential fp32 dot product cannot use FFMA or tensor cores and stay bit-exact); "
-                f"FFMA peak {peak['ffma_tflops']:.1f} TF/s, bf16 tensor peak 1632 TF/s for context",
+                "peak_source": f"nominal FP32 issue rate: {nsm} SMs x 128 lanes x {sm_max:.0f} MHz, one FMUL or FADD "
+                "per lane per cycle (the reference's unfused sequential fp32 dot product cannot use FFMA or tensor "
+                "cores and stay bit-exact); bf16 tensor peak 1673 TF/s (MEASURED_PEAKS) for context",
+                "probe": probe,
             },
             "decode_kernel_ms": mean_decode_ms,
             "decode_phase_share": {
@@ -452,11 +519,14 @@ def main():
         if not args.no_cpu_baseline and world == 1:
             threads = os.cpu_count() or 1
             try:
-                line["cpu_baseline"] = cpu_baseline(threads, 2 * threads, T)
+                gpu_lists = [ex_tok[ex_osp[i] : ex_osp[i + 1]].tolist() for i in range(min(B, 2 * threads))]
+                line["cpu_baseline"], line["parity_sample"] = cpu_baseline_and_parity(
+                    threads, min(B, 2 * threads), T, gpu_lists, ex_sc)
             except Exception as e:  # reference build missing on this host
                 line["cpu_baseline"] = {"value": None, "unavailable": str(e)[:200]}
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
     dec.close()
     return 0

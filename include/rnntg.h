@@ -129,9 +129,6 @@ typedef struct {
                                for weight chunks (pipeline starvation) */
   int64_t capped_frames;  /* greedy_search with S unlimited: frames stopped by
                              the 10-symbol safety cap (search.hpp:31-34) */
-  int64_t fused_pe_cycles[4]; /* beam kernel, fused encoder projection (thread 0,
-                                 summed over CTAs): row list + slice wait, frame
-                                 staging, GEMM, pe write-back */
 } rnntg_stats;
 
 const char* rnntg_last_error(void);
@@ -141,7 +138,10 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
                                 rnntg_model_t* out);
 rnntg_status rnntg_model_destroy(rnntg_model_t model);
 /* Use `stream` (a cudaStream_t) for all work of this handle; NULL = the
- * handle's own stream. */
+ * handle's own (non-blocking) stream, which is NOT ordered with the legacy
+ * default stream: a caller whose device inputs are produced on the legacy
+ * default stream passes cudaStreamLegacy ((void*)0x1), not NULL.  Device
+ * frames are read in stream order on the selected stream. */
 rnntg_status rnntg_set_stream(rnntg_model_t model, void* stream);
 rnntg_status rnntg_set_joiner_mode(rnntg_model_t model, int32_t mode);
 rnntg_status rnntg_get_stats(rnntg_model_t model, rnntg_stats* out);
@@ -234,6 +234,33 @@ rnntg_status rnntg_model_set_encoder(rnntg_model_t model,
 rnntg_status rnntg_encoder_forward(rnntg_model_t model, const float* feats,
                                    const int32_t* frame_splits, int32_t B,
                                    int32_t mem, float* enc_out);
+
+/* Synthetic inputs bit-identical to the reference's (host only, no GPU).
+ *
+ * rnntg_init_model_weights <- init_model (model.hpp:129-169): DetRng(seed)
+ *   uniform(-1/sqrt(fan_in), 1/sqrt(fan_in)) fills in the reference's order
+ *   (common.hpp:86-105, model.hpp:94-97).  Every pointer of `w` receives its
+ *   param_views-shaped array (row-major fp32); a NULL pointer skips the
+ *   array but keeps the draw order.  The reference's ModelConfig seed.
+ * rnntg_gaussian_features  <- SURVEY.md §8(d) synthetic features: stream i of
+ *   B gets T x feat_dim floats (float)DetRng(seed0 + i).gaussian()
+ *   (Box-Muller with spare, common.hpp:108-121), stored [B][T][feat_dim].
+ *   threads <= 0: all hardware threads. */
+typedef struct {
+  int32_t vocab_size, feat_dim, enc_dim, emb_dim, joiner_dim;
+  uint64_t seed;
+} rnntg_model_config;
+
+typedef struct {
+  float *enc_w1, *enc_b1, *enc_w2, *enc_b2;
+  float *emb, *ctx_w, *ctx_b, *j_we, *j_wd, *j_b, *out_w, *out_b;
+} rnntg_weight_ptrs;
+
+rnntg_status rnntg_init_model_weights(const rnntg_model_config* cfg,
+                                      const rnntg_weight_ptrs* w);
+rnntg_status rnntg_gaussian_features(uint64_t seed0, int32_t B, int32_t T,
+                                     int32_t feat_dim, int32_t threads,
+                                     float* out);
 
 /* Kernel-level entry points (bit-exactness tests of the joiner pieces).
  * All pointers are host memory. */

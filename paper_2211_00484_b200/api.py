@@ -31,6 +31,7 @@ OK, INVALID_ARGUMENT, INTERNAL, CUDA_ERROR, UNSUPPORTED = range(5)
 MEM_HOST, MEM_DEVICE = 0, 1
 NO_SYMBOL_LIMIT = 2147483647  # RNNTG_NO_SYMBOL_LIMIT (search.hpp:30 kNoSymbolLimit)
 MERGE_MAX, MERGE_LOG_ADD = 0, 1
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy (driver_types.h)
 
 
 class RnntgError(RuntimeError):
@@ -94,7 +95,6 @@ class _Stats(C.Structure):
         ("gather_cycles", C.c_int64),
         ("gemm_wait_cycles", C.c_int64),
         ("capped_frames", C.c_int64),
-        ("fused_pe_cycles", C.c_int64 * 4),
     ]
 
 
@@ -130,6 +130,8 @@ def _load():
     lib.rnntg_debug_decoder_projection.argtypes = [vp, i32p, i32, f32p]
     lib.rnntg_debug_joiner_logits.argtypes = [vp, f32p, i32p, i32, f32p]
     lib.rnntg_debug_tanhf_chunk_hashes.argtypes = [i32, i32, i32, C.POINTER(C.c_uint64)]
+    lib.rnntg_init_model_weights.argtypes = [vp, vp]
+    lib.rnntg_gaussian_features.argtypes = [C.c_uint64, i32, i32, i32, i32, vp]
     for f in (
         "rnntg_model_create",
         "rnntg_model_destroy",
@@ -146,6 +148,8 @@ def _load():
         "rnntg_debug_decoder_projection",
         "rnntg_debug_joiner_logits",
         "rnntg_debug_tanhf_chunk_hashes",
+        "rnntg_init_model_weights",
+        "rnntg_gaussian_features",
     ):
         getattr(lib, f).restype = C.c_int
     _lib = lib
@@ -325,14 +329,23 @@ class Decoder:
         _check(self._lib.rnntg_set_joiner_mode(self.h, {"exact": 0, "bf16": 1}[mode]))
 
     def set_stream(self, stream_handle: int | None):
-        _check(self._lib.rnntg_set_stream(self.h, C.c_void_p(stream_handle or 0)))
+        """Run this handle's work on `stream_handle` (a cudaStream_t as an
+        int, e.g. torch.cuda.current_stream().cuda_stream).  None selects the
+        handle's own stream.  torch's default stream reports handle 0, which
+        is the legacy default stream: it is passed as cudaStreamLegacy so the
+        decode stays ordered with the caller's work (the C ABI reads NULL as
+        "the handle's own stream")."""
+        if stream_handle is None:
+            h = 0
+        else:
+            h = int(stream_handle) or CUDA_STREAM_LEGACY
+        _check(self._lib.rnntg_set_stream(self.h, C.c_void_p(h)))
 
     def stats(self) -> dict:
         s = _Stats()
         _check(self._lib.rnntg_get_stats(self.h, C.byref(s)))
         d = {f: getattr(s, f) for f, _ in _Stats._fields_}
         d["phase_cycles"] = list(d["phase_cycles"])
-        d["fused_pe_cycles"] = list(d["fused_pe_cycles"])
         return d
 
     # ---- searches ----
@@ -341,6 +354,8 @@ class Decoder:
         B = len(splits) - 1
         osp = np.zeros(B + 1, np.int32)
         if mem == MEM_DEVICE:
+            if out_tokens is None or not out_tokens.is_cuda:
+                raise ValidationError("device frames need a device out_tokens tensor")
             tok, tokp = out_tokens, C.c_void_p(out_tokens.data_ptr())
         else:
             tok = np.zeros(max(1, int(splits[-1])), np.int32)
@@ -379,6 +394,8 @@ class Decoder:
             params.beam_size, params.max_symbols, params.merge_op, int(params.length_norm), params.max_total_symbols
         )
         if mem == MEM_DEVICE:
+            if out_tokens is None or out_scores is None or not (out_tokens.is_cuda and out_scores.is_cuda):
+                raise ValidationError("device frames need device out_tokens and out_scores tensors")
             tokp, scp = C.c_void_p(out_tokens.data_ptr()), C.c_void_p(out_scores.data_ptr())
         else:
             cap = 10 if params.max_symbols == NO_SYMBOL_LIMIT else max(1, params.max_symbols)
@@ -398,18 +415,31 @@ class Decoder:
         ys, _ = self.beam_search_batch(enc_one, [0, enc_one.shape[0]], params)
         return ys[0]
 
-    def fsa_beam_search(self, enc, frame_splits, graph: Graph, params: FsaParams = FsaParams()):
+    def fsa_beam_search(self, enc, frame_splits, graph: Graph, params: FsaParams = FsaParams(), out_tokens=None,
+                        out_scores=None):
+        """Host frames: (token lists, best-path scores).  Device frames:
+        the caller's device tensors out_tokens (>= frame_splits[-1] int32)
+        and out_scores (B float64) are filled and (out_splits, out_tokens,
+        out_scores) returned, as beam_search_batch does."""
         p, mem, splits, keep = _frames(enc, frame_splits)
         B = len(splits) - 1
         osp = np.zeros(B + 1, np.int32)
-        tok = np.zeros(max(1, int(splits[-1])), np.int32)
-        sc = np.zeros(max(1, B), np.float64)
         fp = _FsaParams(float(params.beam), int(params.max_states), int(params.max_contexts))
+        if mem == MEM_DEVICE:
+            if out_tokens is None or out_scores is None or not (out_tokens.is_cuda and out_scores.is_cuda):
+                raise ValidationError("device frames need device out_tokens and out_scores tensors")
+            tokp, scp = C.c_void_p(out_tokens.data_ptr()), C.c_void_p(out_scores.data_ptr())
+        else:
+            tok = np.zeros(max(1, int(splits[-1])), np.int32)
+            sc = np.zeros(max(1, B), np.float64)
+            tokp, scp = _ptr(tok), _ptr(sc)
         _check(
             self._lib.rnntg_fsa_beam_search(
-                self.h, p, _i32p(splits), B, graph.h, C.byref(fp), mem, _i32p(osp), _ptr(tok), _ptr(sc)
+                self.h, p, _i32p(splits), B, graph.h, C.byref(fp), mem, _i32p(osp), tokp, scp
             )
         )
+        if mem == MEM_DEVICE:
+            return osp, out_tokens, out_scores
         return _ragged(osp, tok), sc[:B].copy()
 
     def fsa_lattice(self, stream: int) -> dict:
@@ -440,6 +470,48 @@ class Decoder:
         out = np.zeros((len(ctxs), self.V), np.float32)
         _check(self._lib.rnntg_debug_joiner_logits(self.h, _ptr(enc_rows), _i32p(ctxs), len(ctxs), _ptr(out)))
         return out
+
+
+class _ModelConfig(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("vocab_size", "feat_dim", "enc_dim", "emb_dim", "joiner_dim")] + [
+        ("seed", C.c_uint64)
+    ]
+
+
+_WEIGHT_ORDER = ("enc_w1", "enc_b1", "enc_w2", "enc_b2") + PARAM_NAMES
+
+
+class _WeightPtrs(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in _WEIGHT_ORDER]
+
+
+def init_model_weights(vocab_size=500, feat_dim=80, enc_dim=512, emb_dim=512, joiner_dim=512, seed=1,
+                       blank_bias=0.0) -> dict:
+    """The reference's init_model weights (model.hpp:129-169), bit for bit,
+    as param_views-named float32 arrays (encoder included); `blank_bias` is
+    added to out_b[0] in float, as the north-star configs do."""
+    V, F, D, E, J = vocab_size, feat_dim, enc_dim, emb_dim, joiner_dim
+    shapes = {"enc_w1": (D, F), "enc_b1": (1, D), "enc_w2": (D, D), "enc_b2": (1, D), "emb": (V, E),
+              "ctx_w": (E, 2 * E), "ctx_b": (1, E), "j_we": (J, D), "j_wd": (J, E), "j_b": (1, J),
+              "out_w": (V, J), "out_b": (1, V)}
+    p = {n: np.zeros(shapes[n], np.float32) for n in _WEIGHT_ORDER}
+    ptrs = _WeightPtrs(*[p[n].ctypes.data for n in _WEIGHT_ORDER])
+    _check(_load().rnntg_init_model_weights(C.byref(_ModelConfig(V, F, D, E, J, seed)), C.byref(ptrs)))
+    p["out_b"][0, 0] = np.float32(p["out_b"][0, 0] + np.float32(blank_bias))
+    return p
+
+
+def gaussian_features(seed0, B, T, feat_dim=80, threads=0, out=None):
+    """Per-stream synthetic features [B*T, feat_dim]: stream i is
+    DetRng(seed0 + i).gaussian(), bit-identical to the
+    reference's generator.  `out` may be a (pinned) host buffer to fill."""
+    if B < 0 or T < 0 or feat_dim < 1:
+        raise ValidationError("bad feature shape")
+    if out is None:
+        out = np.empty((B * T, feat_dim), np.float32)
+    ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+    _check(_load().rnntg_gaussian_features(C.c_uint64(seed0), B, T, feat_dim, threads, C.c_void_p(ptr)))
+    return out
 
 
 def tanhf_chunk_hashes(first_chunk=0, num_chunks=256, device=0):

@@ -30,22 +30,9 @@ struct rnntg_model_s {
   cudaStream_t stream = nullptr;
   int num_sms = 1;
   int joiner_mode = RNNTG_JOINER_EXACT;
-  // RNNTG_WS=1 selects the warp-specialised beam kernel (measured slower on
-  // B200 at batch 1024: profiles/r01/README.md); default single-group kernel.
-  bool warp_specialized = false;
-  // RNNTG_BEAM_IMPL: 1 = one 512-thread CTA per SM (beam_kernel /
-  // beam_ws_kernel; default), 0 = dual-residency 256-thread kernel (two CTAs
-  // per SM; measured slower, profiles/r01).
-  int beam_impl = 1;
-  // Fused encoder projection in the beam kernel (no separate K1 launch; host
-  // frames stream in per time slice).  RNNTG_FUSED_PE: 1 = host frames of
-  // uniform length (default; the copy engine streams while the SMs decode),
-  // 2 = also device frames (measured slower there than K1 + decode:
-  // profiles/r01), 0 = never.
-  int fused_pe = 1;
   // Time-sliced host-frame path for the beam kernel (copy + K1 of slice k+1
   // under the decode of slice k).  RNNTG_SLICED: 1 = host frames of uniform
-  // length (default; preferred over the fused path), 0 = never.
+  // length (default), 0 = never.
   // RNNTG_SLICE_FIRST / RNNTG_SLICE_MAX: first slice length (frames) and
   // the cap its doubling grows to.
   int sliced = 1;
@@ -58,7 +45,6 @@ struct rnntg_model_s {
   std::vector<cudaEvent_t> k1_ev;  // one per slice: its pe rows are written
   Scratch hstate;                     // per-stream hypothesis sets between slices
   std::vector<cudaEvent_t> slice_ev;  // one per slice: its frames have landed
-  Scratch ready;
   Scratch pool;           // beam S > 1: sequence node pool
   // Small-batch greedy on thread-block clusters (cluster.cu);
   // RNNTG_GREEDY_CLUSTER=0 disables.
@@ -136,84 +122,6 @@ rnntg_status prepare(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem)
   RNNTG_CUDA_TRY(h->score.ensure(sizeof(double) * std::max(1, B)));
   RNNTG_CUDA_TRY(h->counters.ensure(sizeof(unsigned long long) * 16));
   RNNTG_CUDA_TRY(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long) * 16, h->stream));
-  return RNNTG_OK;
-}
-
-// cuStreamWriteValue32 through the runtime's driver entry-point lookup (no
-// link-time libcuda dependency): a stream-ordered 32-bit store with no
-// kernel, so it lands while the decode kernel holds every SM.
-using StreamWrite32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-StreamWrite32 stream_write32() {
-  // Resolved once and proven with a real write + read-back before any kernel
-  // relies on it (a kernel waiting for a write that never lands would hang).
-  static StreamWrite32 fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !f)
-      return static_cast<StreamWrite32>(nullptr);
-    auto w = reinterpret_cast<StreamWrite32>(f);
-    int32_t* d = nullptr;
-    cudaStream_t st = nullptr;
-    int32_t got = 0;
-    bool ok = cudaMalloc(reinterpret_cast<void**>(&d), sizeof(int32_t)) == cudaSuccess &&
-              cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
-              cudaMemsetAsync(d, 0, sizeof(int32_t), st) == cudaSuccess &&
-              w(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(d), 0x5a5a5a5au,
-                CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS &&
-              cudaMemcpyAsync(&got, d, sizeof(int32_t), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-              cudaStreamSynchronize(st) == cudaSuccess && got == 0x5a5a5a5a;
-    if (st) cudaStreamDestroy(st);
-    if (d) cudaFree(d);
-    cudaGetLastError();
-    return ok ? w : static_cast<StreamWrite32>(nullptr);
-  }();
-  return fn;
-}
-
-// Frames -> decode with the encoder projection fused into the beam kernel.
-// Device frames: one launch.  Host frames (every stream T frames): the
-// kernel is launched first and polls a device counter of landed time slices;
-// a copy stream moves slice s = frames [s*S, (s+1)*S) of all streams with one
-// pitched cudaMemcpy2DAsync and then bumps the counter with a stream-ordered
-// write, so the copy engine streams frames in while the SMs decode.
-template <typename Launch>
-rnntg_status run_fused(rnntg_model_t h, const float* enc, const int32_t* fs, int32_t B, int32_t mem,
-                       int64_t* launches, Launch&& launch) {
-  constexpr int32_t kSlice = 32;
-  const int32_t D = h->d.D;
-  RNNTG_CUDA_TRY(h->ready.ensure(sizeof(int32_t)));
-  int32_t* ready = h->ready.as<int32_t>();
-  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
-  const float* d_enc = mem == RNNTG_MEM_HOST ? h->enc.as<float>() : enc;
-  RNNTG_CUDA_TRY(cudaMemsetAsync(ready, mem == RNNTG_MEM_HOST ? 0x00 : 0x7f, sizeof(int32_t), h->stream));
-  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
-  RNNTG_CUDA_TRY(launch(d_enc, ready, kSlice, h->stream));
-  ++*launches;
-  if (mem == RNNTG_MEM_HOST && fs[B] > 0) {
-    if (!h->cstream[0]) RNNTG_CUDA_TRY(cudaStreamCreateWithFlags(&h->cstream[0], cudaStreamNonBlocking));
-    cudaStream_t cs = h->cstream[0];
-    RNNTG_CUDA_TRY(cudaStreamWaitEvent(cs, h->ev[1], 0));
-    const int32_t T = fs[1] - fs[0];
-    const size_t pitch = sizeof(float) * static_cast<size_t>(T) * D;
-    StreamWrite32 w32 = stream_write32();
-    for (int32_t s = 0; s * kSlice < T; ++s) {
-      const int32_t f0 = s * kSlice, nf = std::min(kSlice, T - f0);
-      RNNTG_CUDA_TRY(cudaMemcpy2DAsync(h->enc.as<float>() + static_cast<int64_t>(f0) * D, pitch,
-                                       enc + static_cast<int64_t>(f0) * D, pitch,
-                                       sizeof(float) * static_cast<size_t>(nf) * D, B,
-                                       cudaMemcpyHostToDevice, cs));
-      if (w32(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(ready),
-              static_cast<cuuint32_t>(s + 1), CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
-        set_error("cuStreamWriteValue32 failed");
-        return RNNTG_CUDA_ERROR;
-      }
-    }
-    if (!h->done[0]) RNNTG_CUDA_TRY(cudaEventCreateWithFlags(&h->done[0], cudaEventDisableTiming));
-    RNNTG_CUDA_TRY(cudaEventRecord(h->done[0], cs));
-    RNNTG_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->done[0], 0));
-  }
-  h->pipelined = false;
   return RNNTG_OK;
 }
 
@@ -430,7 +338,6 @@ rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
   h->stats.gather_cycles = static_cast<int64_t>(cnt[6]);
   h->stats.capped_frames = h->slot_mult > 1 ? static_cast<int64_t>(cnt[13]) : 0;
   h->stats.gemm_wait_cycles = static_cast<int64_t>(cnt[7]);
-  for (int i = 0; i < 4; ++i) h->stats.fused_pe_cycles[i] = static_cast<int64_t>(cnt[12 + i]);
   h->stats.gpu_ms = ms_all;
   h->stats.decode_ms = ms_dec;
   return RNNTG_OK;
@@ -483,9 +390,6 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
   h->stream = h->own_stream;
   for (auto& e : h->ev) cudaEventCreate(&e);
   h->num_sms = rnntg::decode_num_sms(device);
-  if (const char* ws = std::getenv("RNNTG_WS")) h->warp_specialized = std::atoi(ws) != 0;
-  if (const char* bi = std::getenv("RNNTG_BEAM_IMPL")) h->beam_impl = std::atoi(bi);
-  if (const char* fp = std::getenv("RNNTG_FUSED_PE")) h->fused_pe = std::atoi(fp);
   if (const char* e = std::getenv("RNNTG_SLICED")) h->sliced = std::atoi(e);
   if (const char* e = std::getenv("RNNTG_SLICE_FIRST")) h->slice_first = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("RNNTG_SLICE_MAX")) h->slice_max = std::max(1, std::atoi(e));
@@ -579,7 +483,7 @@ rnntg_status rnntg_model_destroy(rnntg_model_t h) {
   for (Scratch* s : {&h->enc, &h->pe, &h->splits, &h->tok, &h->len, &h->score, &h->bp,
                      &h->counters, &h->ctx, &h->out_tok, &h->out_splits, &h->logits,
                      &h->finfo, &h->nodebest, &h->lattice, &h->flag, &h->feat, &h->hid,
-                     &h->hstate, &h->ready, &h->pool})
+                     &h->hstate, &h->pool})
     s->release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -773,16 +677,8 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
     const int64_t waves = (static_cast<int64_t>(B) + static_cast<int64_t>(h->num_sms) * gmax - 1) /
                           (static_cast<int64_t>(h->num_sms) * gmax);
     const int G = std::min<int64_t>(gmax, std::max<int64_t>(1, (B + waves * h->num_sms - 1) / (waves * h->num_sms)));
-    const bool ws = exact && G >= 2 && h->warp_specialized;
-    // Fused encoder projection: exact single-CTA kernel, out_w^T and j_we^T
-    // chunks of one shape, frames of uniform length when they come from the
-    // host (time slices), and a working stream-ordered write.
     bool uniform = true;
     for (int32_t i = 1; i < B; ++i) uniform = uniform && fs[i + 1] - fs[i] == fs[1] - fs[0];
-    const bool fused = exact && !ws && h->beam_impl == 1 && h->fused_pe > 0 && h->d.Jp == h->d.Vp &&
-                       h->d.D % 4 == 0 && h->d.D <= rnntg::kMaxJoiner &&
-                       ((mem == RNNTG_MEM_DEVICE && h->fused_pe > 1) ||
-                        (mem == RNNTG_MEM_HOST && uniform && stream_write32() != nullptr));
     auto args = [&](int32_t b0, int32_t b1) {
       rnntg::DecodeArgs a{};
       a.m = &h->d;
@@ -801,11 +697,9 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       // back-pointer rows are indexed (frame offset + stream index)
       a.backptr = h->bp.as<uint32_t>() + static_cast<int64_t>(b0) * rnntg::kMaxBeam;
       a.joiner_bf16 = h->joiner_mode == RNNTG_JOINER_BF16;
-      a.warp_specialized = ws;
-      a.beam_impl = h->beam_impl;
       return a;
     };
-    const bool sliced = exact && !ws && h->beam_impl == 1 && uniform && fs[1] - fs[0] > h->slice_first &&
+    const bool sliced = exact && uniform && fs[1] - fs[0] > h->slice_first &&
                         ((mem == RNNTG_MEM_HOST && h->sliced > 0) || (mem == RNNTG_MEM_DEVICE && h->sliced > 1));
     if (sliced) {
       st = run_sliced(h, enc, fs, B, mem, &launches, [&](int32_t t0, int32_t t1, cudaStream_t cs) {
@@ -818,23 +712,8 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       if (st) return st;
       return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
     }
-    if (fused) {
-      st = run_fused(h, enc, fs, B, mem, &launches, [&](const float* d_enc, const int32_t* rdy, int32_t S,
-                                                       cudaStream_t cs) {
-        rnntg::DecodeArgs a = args(0, B);
-        a.fused_enc = d_enc;
-        a.fused_pe = h->pe.as<float>();
-        a.ready = rdy;
-        a.slice_frames = S;
-        return rnntg::launch_decode_beam(a, cs);
-      });
-      if (st) return st;
-      return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
-    }
     st = run_pipeline(h, enc, fs, B, mem, G, &launches, [&](int32_t b0, int32_t b1, cudaStream_t cs) {
       rnntg::DecodeArgs a = args(b0, b1);
-      // a chunk of the host-frame pipeline fills its share of the CTA slots
-      a.cta_slots = static_cast<int32_t>((2LL * h->num_sms * (b1 - b0) + B - 1) / B);
       return rnntg::launch_decode_beam(a, cs);
     });
     if (st) return st;
@@ -923,6 +802,9 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
   if (st) return st;
   if (!out_splits) return invalid("out_splits is null");
   std::lock_guard<std::mutex> lk(h->mu);
+  // The lattice buffers are overwritten below; until this call succeeds there
+  // is no exportable lattice (rnntg_fsa_lattice).
+  h->last_fsa_fs.clear();
   RNNTG_CUDA_TRY(cudaSetDevice(h->device));
   if ((st = prepare(h, fs, B, mem))) return st;
   int64_t launches = 0;
@@ -1008,8 +890,9 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
       break;
     }
   }
-  h->last_fsa_fs.assign(fs, fs + B + 1);
-  return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+  st = finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+  if (st == RNNTG_OK) h->last_fsa_fs.assign(fs, fs + B + 1);
+  return st;
 }
 
 rnntg_status rnntg_fsa_lattice(rnntg_model_t h, int32_t s, int32_t* num_nodes, int32_t* num_arcs,

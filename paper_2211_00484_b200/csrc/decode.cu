@@ -226,8 +226,6 @@ struct BeamCand {  // stage-1 extension or stage-2 merged entry
 struct BeamSmem {
   unsigned long long stat[16];  // per-CTA counters (layout of DecodeArgs::counters)
   WPipe pipe;
-  int64_t pe_src[kRowCap];  // fused encoder projection: frame rows of this pass
-  int32_t pe_rows;
   uint64_t bar[2];
   uint32_t wcur[2];
   int64_t row_pe[kRowCap];
@@ -716,119 +714,17 @@ __device__ __noinline__ void beam_stream_step_ni(const ModelView& m, Hyps& h, Be
                          out_score, ties);
 }
 
-// Fused encoder projection (joiner_project_enc, model.hpp:263-271):
-// pe[row] = j_we . enc[row], sequential in k from 0.0f, for up to kRowCap
-// frame rows of the CTA's streams (F consecutive frames each), through the
-// same balanced exact GEMM and chunk pipeline as the joiner (the pipeline's
-// A matrix).  The frame rows are staged k-major in the h tile (row-fastest
-// units: conflict-free), the results are written to the global pe buffer the
-// h build reads.  With host frames streamed in time slices the pass first
-// waits until the slice holding its last frame has landed.
-struct FusedPe {
-  const float* enc;
-  float* pe;
-  const int32_t* ready;
-  int32_t slice_frames;
-  int32_t D;
-  const float* j_wet;
-  const float* zeros;
-  int32_t dbg_force_r;  // development: GEMM over this many rows every frame (0 = off)
+// Development knob: GEMM over this many rows every frame (0 = off;
+// RNNTG_DBG_FORCE_R, the joiner GEMM's marginal-rate experiment).
+struct DbgKnobs {
+  int32_t dbg_force_r;
 };
-
-__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <typename Smem>
-__device__ __noinline__ void fused_pe_pass(const ModelView& m, const FusedPe& fp, const WPipe& pipe,
-                                              uint32_t& g, float* HL, Smem& S,
-                                              const int32_t* __restrict__ frame_splits, int s0,
-                                              int ns, int t, int F, long long* ph) {
-  const long long q0 = clock64();
-  if (threadIdx.x < 32) {  // warp 0: rows in (frame, stream) order, lane = stream
-    const int lane = threadIdx.x;
-    int32_t fs = 0, T = 0;
-    if (lane < ns) {
-      fs = frame_splits[s0 + lane];
-      T = frame_splits[s0 + lane + 1] - fs;
-    }
-    int R = 0, last = t;
-    for (int f = 0; f < F; ++f) {
-      const bool ok = lane < ns && t + f < T;
-      const uint32_t bal = __ballot_sync(0xffffffffu, ok);
-      if (ok) S.pe_src[R + __popc(bal & ((1u << lane) - 1u))] = fs + t + f;
-      if (bal) last = t + f;
-      R += __popc(bal);
-    }
-    if (lane == 0) {
-      S.pe_rows = R;
-      const int32_t need = last / fp.slice_frames;
-      const long long t0 = clock64();
-      while (ld_acquire(fp.ready) <= need) {
-        __nanosleep(500);
-        if (clock64() - t0 > (1ll << 36)) __trap();  // ~35 s: a slice never landed; fail, don't hang
-      }
-    }
-  }
-  __syncthreads();
-  const long long q1 = clock64();
-  const int R = S.pe_rows;
-  const int D = fp.D, D4 = D >> 2, units = R * D4;
-  // Row-fastest units (conflict-free k-major stores); eight loads in flight
-  // per thread before any store.
-  for (int base = threadIdx.x; base < units; base += 8 * blockDim.x) {
-    float4 v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int x = base + u * blockDim.x;
-      if (x < units) {
-        const int i = (x / R) * 4, r = x - (i >> 2) * R;
-        v[u] = *reinterpret_cast<const float4*>(fp.enc + S.pe_src[r] * D + i);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int x = base + u * blockDim.x;
-      if (x < units) {
-        const int i = (x / R) * 4, r = x - (i >> 2) * R;
-        float* o = HL + i * kHStride + r;
-        o[0] = v[u].x;
-        o[kHStride] = v[u].y;
-        o[2 * kHStride] = v[u].z;
-        o[3 * kHStride] = v[u].w;
-      }
-    }
-  }
-  __syncthreads();
-  const long long q2 = clock64();
-  ModelView mp = m;
-  mp.J = D;          // contraction length
-  mp.out_wt = fp.j_wet;
-  mp.out_b = fp.zeros;  // acc starts from 0.0f
-  joiner_gemm(mp, pipe, g, HL, R);  // rows land in HL as [R][Vp] (Vp == Jp)
-  const long long q3 = clock64();
-  const int J = m.J, J4 = J >> 2;
-  for (int x = threadIdx.x; x < R * J4; x += blockDim.x) {
-    const int r = x / J4, j = (x - r * J4) * 4;
-    *reinterpret_cast<float4*>(fp.pe + S.pe_src[r] * J + j) =
-        *reinterpret_cast<const float4*>(HL + static_cast<int64_t>(r) * m.Vp + j);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    ph[0] += q1 - q0;
-    ph[1] += q2 - q1;
-    ph[2] += q3 - q2;
-    ph[3] += clock64() - q3;
-  }
-}
 
 // SL: time-sliced launch (frames [sl.t0, sl.t1), hypothesis sets resumed
 // from / kept in sl.state).  A separate instantiation so the single-launch
 // kernel's code is untouched by the slice plumbing (ptxas's register
 // allocation of the frame loop is sensitive to it: ~1-2%).
-template <int BCAP, bool TC, bool FPE, bool SL = false>
+template <int BCAP, bool TC, bool SL = false>
 __global__ void __launch_bounds__(kDecodeThreads, 1)
     beam_kernel(ModelView m, const float* __restrict__ pe,
                 const int32_t* __restrict__ frame_splits, int32_t B, int32_t G,
@@ -836,10 +732,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
                 int32_t max_total, uint32_t* __restrict__ backptr,
                 int32_t* __restrict__ tokens, int32_t* __restrict__ lengths,
                 double* __restrict__ scores,
-                unsigned long long* __restrict__ counters, FusedPe fp, BeamSlice sl) {
+                unsigned long long* __restrict__ counters, DbgKnobs fp, BeamSlice sl) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* HL = reinterpret_cast<float*>(smem_raw);
-  const int hl_floats = max(max(m.J, fp.D) * kHStride, kRowCap * m.Vp);
+  const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
   // weight stages: two kBK-row fp32 chunks, or (bf16 variant) kTcStages
   // 16 KB bf16 chunks = the area of two 16-row fp32 chunks
   const int wst = TC ? 16 * m.Vp : kBK * m.Vp;
@@ -862,18 +758,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   // chunk is waited for or issued instead of pinning ~14 registers across
   // every phase (register pressure here costs the GEMM its LDS prefetch).
   const WPipe& pipe = S.pipe;
-  // fused encoder projection: one A pass (j_we) per F frames, F frames x ns
-  // streams <= kRowCap rows
-  const int F = FPE ? max(1, min(4, kRowCap / ns)) : 1;
-  if (threadIdx.x == 0) {
-    S.pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
-    if constexpr (FPE) {
-      S.pipe.a_ptr = fp.j_wet;
-      S.pipe.a_K = fp.D;
-      S.pipe.a_nc = (fp.D + kBK - 1) / kBK;  // (bk == kBK for this kernel)
-      S.pipe.period = F;
-    }
-  }
+  if (threadIdx.x == 0) S.pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
   TcPipe tp{smem_u32(W0), tb->full, tb->empty, &tb->done, smem_u32(hb), 0u, m.J / kTcBK};
 
   int32_t tmax = 0;
@@ -931,13 +816,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   unsigned long long* st = S.stat;
   long long* pst = reinterpret_cast<long long*>(S.stat);
 
-  // Frame blocks of F frames: the fused encoder projection runs once per
-  // block, outside the per-frame loop (keeps that loop's register allocation
-  // identical to the unfused kernel's).
+  // One block of frames [t_begin, t_end) (the block structure is kept: the
+  // frame loop's register allocation is sensitive to its shape).
   const int32_t t_begin = SL ? sl.t0 : 0;
-  const int32_t TB = FPE ? F : max(1, t_end - t_begin);
+  const int32_t TB = max(1, t_end - t_begin);
   for (int32_t tb = t_begin; tb < t_end; tb += TB) {
-  if constexpr (FPE) fused_pe_pass(m, fp, pipe, g, HL, S, frame_splits, s0, ns, tb, F, pst + 12);
   const int32_t te = min(tb + TB, t_end);
   for (int32_t t = tb; t < te; ++t) {
     // A. rows: distinct contexts per live stream (lane = stream, G <= 32).
@@ -960,7 +843,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     if (threadIdx.x == 0) pst[6] += pst[2] - c0;
     // Next frame's encoder projections into L2 while the GEMM runs (each
     // stream's pe row is 2 KB of HBM read once; the h build then hits L2).
-    if constexpr (!FPE) {
+    {
       const int lines = (m.J * 4 + 127) >> 7;
       for (int x = threadIdx.x; x < ns * lines; x += kDecodeThreads) {
         const int i = x / lines, l = x - i * lines;
@@ -1055,126 +938,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     for (int i = 0; i < ns; ++i)
       sf += SL ? max(0, min(frame_splits[s0 + i + 1] - frame_splits[s0 + i], t_end) - sl.t0)
                : frame_splits[s0 + i + 1] - frame_splits[s0 + i];
-    atomicAdd(&counters[0], sf);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Dual-residency beam kernel: 256 threads, two CTAs per SM (decode_common.cuh
-// "Dual-residency exact joiner").  Same phases, arithmetic and decisions as
-// beam_kernel; CTA i owns streams [i*q + min(i, rem), +q + (i < rem)) of the
-// launch (q = B / NC, rem = B % NC), so per-SM stream counts differ by at
-// most one.
-// ---------------------------------------------------------------------------
-struct DualSmem {
-  uint64_t full[kStages2];
-  uint32_t empty_cnt[kStages2];
-  int64_t row_pe[kRowCap2];
-  int32_t row_ctx[kRowCap2];
-  double row_lse[kRowCap2];
-  float row_l0[kRowCap2];
-  float row_tl[kRowCap2][kMaxBeam];
-  int32_t row_tk[kRowCap2][kMaxBeam];
-  int32_t nrows;
-};
-
-template <int BCAP>
-__global__ void __launch_bounds__(kDualThreads, 2)
-    beam_dual_kernel(ModelView m, const float* __restrict__ pe,
-                     const int32_t* __restrict__ frame_splits, int32_t B, int32_t NC,
-                     int32_t beam, int32_t merge_log, int32_t length_norm,
-                     int32_t max_total, uint32_t* __restrict__ backptr,
-                     int32_t* __restrict__ tokens, int32_t* __restrict__ lengths,
-                     double* __restrict__ scores,
-                     unsigned long long* __restrict__ counters) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* HL = reinterpret_cast<float*>(smem_raw);
-  const int hl_floats = max(m.J * kHStride2, kRowCap2 * m.Vp);
-  float* W0 = HL + hl_floats;
-  DualSmem& S = *reinterpret_cast<DualSmem*>(W0 + kStages2 * kBK2 * m.Vp);
-  Hyps* H = reinterpret_cast<Hyps*>(&S + 1);
-  constexpr int kCandPerStream = BCAP * BCAP + 2 * BCAP;
-
-  const int q = B / NC, rem = B % NC;
-  const int s0 = blockIdx.x * q + min(static_cast<int>(blockIdx.x), rem);
-  const int ns = q + (static_cast<int>(blockIdx.x) < rem ? 1 : 0);
-  if (ns <= 0) return;
-  BeamCand* C = reinterpret_cast<BeamCand*>(H + ns);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const DualPipe pipe{smem_u32(W0), static_cast<uint32_t>(kBK2 * m.Vp * 4), S.full, S.empty_cnt,
-                      (m.J + kBK2 - 1) / kBK2};
-
-  int32_t tmax = 0;
-  for (int i = 0; i < ns; ++i) tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
-  for (int i = threadIdx.x; i < ns; i += kDualThreads) {
-    Hyps& h = H[i];
-    h.nh = 1;
-    h.score[0] = 0.0;
-    h.ctx[0] = 0;
-    h.len[0] = 0;
-    h.last[0] = -1;
-    h.h1[0] = 0x243f6a8885a308d3ull;
-    h.h2[0] = 0x13198a2e03707344ull;
-    h.p1[0] = h.p2[0] = 0;
-  }
-  if (threadIdx.x == 0) dual_pipe_init(pipe, m);
-  __syncthreads();
-  if (threadIdx.x == 0) dual_pipe_prime(pipe, m);
-  uint32_t g = 0;
-  unsigned long long rows_total = 0, ties = 0;
-  long long ph_h = 0, ph_gemm = 0, ph_epi = 0, ph_step = 0;  // phase cycles (thread 0)
-
-  for (int32_t t = 0; t < tmax; ++t) {
-    if (warp == 0) {  // A. rows: distinct contexts per live stream (lane = stream)
-      const int R0 = beam_rows(H, ns, frame_splits + s0, t, S.row_pe, S.row_ctx);
-      if (lane == 0) S.nrows = R0;
-    }
-    __syncthreads();
-    const int R = S.nrows;
-    rows_total += R;
-    const long long c0 = clock64();
-    build_h_g(m, pe, S.row_pe, S.row_ctx, R, HL, kHStride2, threadIdx.x, kDualThreads);
-    __syncthreads();
-    const long long c1 = clock64();
-    dual_gemm(m, pipe, g, HL, R);
-    const long long c2 = clock64();
-    const RowRes rr{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
-    for (int r = warp; r < R; r += kDualWarps)
-      beam_row_reduce<BCAP>(HL + static_cast<int64_t>(r) * m.Vp, m.V, beam, r, rr);
-    __syncthreads();
-    const long long c3 = clock64();
-    for (int i = warp; i < ns; i += kDualWarps) {
-      const int32_t fs = frame_splits[s0 + i];
-      const int32_t T = frame_splits[s0 + i + 1] - fs;
-      if (t >= T) continue;
-      beam_stream_step<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
-                             backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs, beam,
-                             merge_log, length_norm, max_total, rr, tokens, lengths + s0 + i,
-                             scores + s0 + i, &ties);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const long long c4 = clock64();
-      ph_h += c1 - c0;
-      ph_gemm += c2 - c1;
-      ph_epi += c3 - c2;
-      ph_step += c4 - c3;
-    }
-  }
-  for (int i = threadIdx.x; i < ns; i += kDualThreads)
-    if (frame_splits[s0 + i + 1] == frame_splits[s0 + i]) {
-      lengths[s0 + i] = 0;
-      scores[s0 + i] = 0.0;
-    }
-  atomicAdd(&counters[4], ties);
-  if (threadIdx.x == 0) {
-    dual_pipe_drain(pipe, g);
-    atomicAdd(&counters[8], static_cast<unsigned long long>(ph_h));
-    atomicAdd(&counters[9], static_cast<unsigned long long>(ph_gemm));
-    atomicAdd(&counters[10], static_cast<unsigned long long>(ph_epi));
-    atomicAdd(&counters[11], static_cast<unsigned long long>(ph_step));
-    unsigned long long sf = 0;
-    for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
     atomicAdd(&counters[0], sf);
   }
 }
@@ -1592,264 +1355,7 @@ cudaError_t launch_decode_greedy(const DecodeArgs& a, cudaStream_t s) {
 }
 
 namespace {
-// ---------------------------------------------------------------------------
-// Warp-specialised exact beam kernel.  The CTA's streams are split into two
-// halves with their own h/logits tiles.  Warps 0-11 (GEMM group) run only
-// the exact joiner contraction, half 0 then half 1 of each frame; warps
-// 12-15 (POST group, one per SM sub-partition) reduce the rows, step the
-// beams and build the next frame's rows and h tile (gather + tanhf) of one
-// half while the GEMM group computes the other half, so the latency-bound
-// phases hide behind the FMUL/FADD stream.  Hand-offs are named barriers
-// (bar.arrive by the producer group, bar.sync by the consumer):
-//   1+h  h tile of half h ready      (POST -> GEMM)
-//   3+h  logits of half h ready      (GEMM -> POST)
-//   5    GEMM group chunk hand-off, 6 POST group internal.
-// The GEMM is the SMSP-balanced tiling of gemm_pass_bal over the 12 GEMM
-// warps (<= 16 rows per half: at most 12 items).  Arithmetic and decisions
-// are identical to beam_kernel.
-// ---------------------------------------------------------------------------
-constexpr int kWsGemmWarps = 12;
-constexpr int kWsPostWarps = 4;
-constexpr int kWsThreads = (kWsGemmWarps + kWsPostWarps) * 32;
-constexpr int kWsHalfRows = 16;
-constexpr int kWsHStride = kWsHalfRows + 4;
-
-struct WsHalf {
-  int64_t row_pe[kWsHalfRows];
-  int32_t row_ctx[kWsHalfRows];
-  double row_lse[kWsHalfRows];
-  float row_l0[kWsHalfRows];
-  float row_tl[kWsHalfRows][kMaxBeam];
-  int32_t row_tk[kWsHalfRows][kMaxBeam];
-  int32_t nrows;
-};
-
-struct WsSmem {
-  unsigned long long stat[16];
-  WPipe pipe;
-  uint64_t bar[2];
-  uint32_t wcur[2];
-  WsHalf half[2];
-};
-
-__device__ __forceinline__ int ws_hl_floats(const ModelView& m) {
-  return max(m.J * kWsHStride, kWsHalfRows * m.Vp);
-}
-
-// Balanced exact GEMM for the 12-warp GEMM group (gemm_pass_bal's items;
-// chunk hand-off on named barrier 5; the last GEMM warp refills).
-__device__ __forceinline__ void ws_gemm(const ModelView& m, const WPipe& p, uint32_t& g, float* HL,
-                                        int R) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int full = R >> 2, rem = R & 3;
-  if (rem != 0 && 2 * (full & ~1) + 4 * (full & 1) + 4 > kWsGemmWarps) {
-    ++full;
-    rem = 0;
-  }
-  const int heavy = 2 * (full & ~1);
-  const int lfull = (full & 1) ? 4 : 0;
-  int tn = 0, nr = 4, rg = 0, cbase = 0;
-  if (warp < heavy) {
-    tn = 8;
-    rg = warp >> 1;
-    cbase = (warp & 1) * 256;
-  } else if (warp < heavy + lfull) {
-    tn = 4;
-    rg = full - 1;
-    cbase = (warp - heavy) * 128;
-  } else if (rem != 0 && warp < heavy + lfull + 4) {
-    tn = 4;
-    nr = rem;
-    rg = full;
-    cbase = (warp - heavy - lfull) * 128;
-  }
-  int col[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) col[j] = cbase + (j < 4 ? lane * 4 + j : 128 + lane * 4 + (j - 4));
-  float acc[4][8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float b = (tn == 8 || (tn == 4 && j < 4)) ? m.out_b[col[j]] : 0.0f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i][j] = b;
-  }
-  for (int32_t c = 0; c < p.nc; ++c, ++g) {
-    const uint32_t st = g & 1u;
-    if (tn != 0 || warp == 0) mbar_wait(p.bar + st, (g >> 1) & 1u);
-    const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(p.bk * m.Vp * 4);
-    const int kk_end = min(p.bk, m.J - c * p.bk);
-    const float* hp = HL + static_cast<int64_t>(c * p.bk) * kWsHStride + rg * 4;
-    if (tn == 8) gemm_chunk<8, 4, kWsHStride>(m, ws, hp, kk_end, col, acc);
-    else if (tn == 4 && nr == 4) gemm_chunk<4, 4, kWsHStride>(m, ws, hp, kk_end, col, acc);
-    else if (tn == 4 && nr == 3) gemm_chunk<4, 3, kWsHStride>(m, ws, hp, kk_end, col, acc);
-    else if (tn == 4 && nr == 2) gemm_chunk<4, 2, kWsHStride>(m, ws, hp, kk_end, col, acc);
-    else if (tn == 4) gemm_chunk<4, 1, kWsHStride>(m, ws, hp, kk_end, col, acc);
-    nbar_sync(5, kWsGemmWarps * 32);  // the GEMM group is done with this stage (and with h)
-    if (threadIdx.x == (kWsGemmWarps - 1) * 32) wpipe_issue(p, m, g + 2);
-  }
-  if (tn != 0) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = rg * 4 + i;
-      if (r < R) {
-        float* lr = HL + static_cast<int64_t>(r) * m.Vp;
-        *reinterpret_cast<float4*>(lr + col[0]) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-        if (tn == 8)
-          *reinterpret_cast<float4*>(lr + col[4]) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
-      }
-    }
-  }
-}
-
-template <int BCAP>
-__global__ void __launch_bounds__(kWsThreads, 1)
-    beam_ws_kernel(ModelView m, const float* __restrict__ pe,
-                   const int32_t* __restrict__ frame_splits, int32_t B, int32_t G, int32_t beam,
-                   int32_t merge_log, int32_t length_norm, int32_t max_total,
-                   uint32_t* __restrict__ backptr, int32_t* __restrict__ tokens,
-                   int32_t* __restrict__ lengths, double* __restrict__ scores,
-                   unsigned long long* __restrict__ counters) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int hl = ws_hl_floats(m);
-  float* HL0 = reinterpret_cast<float*>(smem_raw);
-  float* HL1 = HL0 + hl;
-  float* W0 = HL1 + hl;
-  float* W1 = W0 + kBK * m.Vp;
-  WsSmem& S = *reinterpret_cast<WsSmem*>(W1 + kBK * m.Vp);
-  Hyps* H = reinterpret_cast<Hyps*>(&S + 1);         // [G]
-  BeamCand* C = reinterpret_cast<BeamCand*>(H + G);  // [G][BCAP*BCAP + 2*BCAP]
-  constexpr int kCandPerStream = BCAP * BCAP + 2 * BCAP;
-  constexpr int kAll = kWsThreads;
-
-  const int s0 = blockIdx.x * G;
-  const int ns = min(G, B - s0);
-  if (ns <= 0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const WPipe& pipe = S.pipe;
-  const int nA = (ns + 1) >> 1;
-
-  int32_t tmax = 0;
-  for (int i = 0; i < ns; ++i) tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
-  for (int i = threadIdx.x; i < ns; i += kAll) {
-    Hyps& h = H[i];
-    h.nh = 1;
-    h.score[0] = 0.0;
-    h.ctx[0] = 0;
-    h.len[0] = 0;
-    h.last[0] = -1;
-    h.h1[0] = 0x243f6a8885a308d3ull;
-    h.h2[0] = 0x13198a2e03707344ull;
-    h.p1[0] = h.p2[0] = 0;
-  }
-  if (threadIdx.x < 16) S.stat[threadIdx.x] = 0;
-  if (threadIdx.x == 0) {
-    S.pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
-    mbar_init(&S.bar[0], 1);
-    mbar_init(&S.bar[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (warp < kWsGemmWarps) {
-    // ---- GEMM group: nothing but the joiner contraction ----
-    if (threadIdx.x == 0) {
-      wpipe_issue(pipe, m, 0);
-      wpipe_issue(pipe, m, 1);
-    }
-    uint32_t g = 0;
-    for (int32_t t = 0; t < tmax; ++t)
-      for (int hh = 0; hh < 2; ++hh) {
-        nbar_sync(1 + hh, kAll);  // h tile of half hh ready (POST group)
-        const int R = S.half[hh].nrows;
-        if (R > 0) ws_gemm(m, pipe, g, hh ? HL1 : HL0, R);
-        nbar_arrive(3 + hh, kAll);  // logits of half hh ready
-      }
-    if (threadIdx.x == 0) {
-      mbar_wait(&S.bar[g & 1u], (g >> 1) & 1u);
-      mbar_wait(&S.bar[(g + 1) & 1u], ((g + 1) >> 1) & 1u);
-    }
-  } else {
-    // ---- POST group: rows, h tile, row reduction, beam step ----
-    const int pw = warp - kWsGemmWarps, ptid = threadIdx.x - kWsGemmWarps * 32;
-    constexpr int kPost = kWsPostWarps * 32;
-    for (int32_t t = -1; t < tmax; ++t)
-      for (int hh = 0; hh < 2; ++hh) {
-        const int first = hh ? nA : 0, count = hh ? ns - nA : nA;
-        WsHalf& X = S.half[hh];
-        float* HLh = hh ? HL1 : HL0;
-        if (t >= 0) {
-          nbar_sync(3 + hh, kAll);  // logits of half hh (frame t)
-          const int R = X.nrows;
-          const RowRes rr{X.row_lse, X.row_l0, X.row_tl, X.row_tk};
-          // rows pw, pw + 4, pw + 8, pw + 12 of this warp, chains interleaved
-          if (R > 8) {
-            if (pw < R) beam_row_reduce_n<BCAP, 4>(HLh, m.Vp, m.V, beam, pw, R, rr, kWsPostWarps);
-          } else if (R > 4) {
-            if (pw < R) beam_row_reduce_n<BCAP, 2>(HLh, m.Vp, m.V, beam, pw, R, rr, kWsPostWarps);
-          } else if (pw < R) {
-            beam_row_reduce_n<BCAP, 1>(HLh, m.Vp, m.V, beam, pw, R, rr, kWsPostWarps);
-          }
-          nbar_sync(6, kPost);
-          for (int k = pw; k < count; k += kWsPostWarps) {
-            const int i = first + k;
-            const int32_t fs = frame_splits[s0 + i];
-            const int32_t T = frame_splits[s0 + i + 1] - fs;
-            if (t >= T) continue;
-            beam_stream_step<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
-                                   backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs,
-                                   beam, merge_log, length_norm, max_total, rr, tokens,
-                                   lengths + s0 + i, scores + s0 + i, &S.stat[4]);
-          }
-          nbar_sync(6, kPost);  // hypotheses of half hh stepped, its logits consumed
-        }
-        if (t + 1 < tmax) {  // rows + h tile of half hh for frame t + 1
-          if (pw == 0) {
-            const int R = beam_rows(H + first, count, frame_splits + s0 + first, t + 1, X.row_pe, X.row_ctx);
-            if (lane == 0) {
-              X.nrows = R;
-              S.stat[1] += R;
-            }
-          }
-          nbar_sync(6, kPost);
-          build_h_g(m, pe, X.row_pe, X.row_ctx, X.nrows, HLh, kWsHStride, ptid, kPost);
-          nbar_arrive(1 + hh, kAll);  // each POST thread releases its h writes
-        }
-
-      }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < ns; i += kAll)
-    if (frame_splits[s0 + i + 1] == frame_splits[s0 + i]) {
-      lengths[s0 + i] = 0;
-      scores[s0 + i] = 0.0;
-    }
-  if (threadIdx.x < 16 && threadIdx.x != 0 && S.stat[threadIdx.x] != 0)
-    atomicAdd(&counters[threadIdx.x], S.stat[threadIdx.x]);
-  if (threadIdx.x == 0) {
-    unsigned long long sf = 0;
-    for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
-    atomicAdd(&counters[0], sf);
-  }
-}
-
-template <int BCAP>
-cudaError_t launch_beam_ws(const DecodeArgs& a, cudaStream_t s) {
-  const ModelView m = view_of(*a.m);
-  const int G = a.streams_per_cta;
-  const size_t hl = static_cast<size_t>(std::max(m.J * kWsHStride, kWsHalfRows * m.Vp)) * 4;
-  const size_t smem = 2 * hl + static_cast<size_t>(2) * kBK * m.Vp * 4 + sizeof(WsSmem) +
-                      sizeof(Hyps) * G + sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
-  cudaError_t e = cudaFuncSetAttribute(beam_ws_kernel<BCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  const int grid = (a.B + G - 1) / G;
-  beam_ws_kernel<BCAP><<<grid, kWsThreads, smem, s>>>(
-      m, a.pe, a.frame_splits, a.B, G, a.beam_size, a.merge_op, a.length_norm, a.max_total,
-      a.backptr, a.tokens, a.lengths, a.scores, a.counters);
-  return cudaGetLastError();
-}
-
-template <int BCAP, bool TC, bool FPE, bool SL = false>
+template <int BCAP, bool TC, bool SL = false>
 cudaError_t launch_beam_cap3(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);
   const int G = a.streams_per_cta;
@@ -1857,16 +1363,16 @@ cudaError_t launch_beam_cap3(const DecodeArgs& a, cudaStream_t s) {
     const char* e = std::getenv("RNNTG_DBG_FORCE_R");
     return e ? std::atoi(e) : 0;
   }();
-  FusedPe fp{a.fused_enc, a.fused_pe, a.ready, a.slice_frames, FPE ? a.m->D : 0, a.m->j_wet, a.m->zeros, force_r};
-  const size_t hl = static_cast<size_t>(max(max(m.J, fp.D) * kHStride, kRowCap * m.Vp)) * 4;
+  DbgKnobs fp{force_r};
+  const size_t hl = static_cast<size_t>(max(m.J * kHStride, kRowCap * m.Vp)) * 4;
   size_t smem = hl + static_cast<size_t>(2) * (TC ? 16 : kBK) * m.Vp * 4 + sizeof(BeamSmem) + sizeof(Hyps) * G +
                 sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
   if (TC) smem += 1024 + static_cast<size_t>(kRowCap) * m.J * 2 + sizeof(TcBars);
-  cudaError_t e = cudaFuncSetAttribute(beam_kernel<BCAP, TC, FPE, SL>,
+  cudaError_t e = cudaFuncSetAttribute(beam_kernel<BCAP, TC, SL>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int grid = (a.B + G - 1) / G;
-  beam_kernel<BCAP, TC, FPE, SL><<<grid, kDecodeThreads, smem, s>>>(
+  beam_kernel<BCAP, TC, SL><<<grid, kDecodeThreads, smem, s>>>(
       m, a.pe, a.frame_splits, a.B, G, a.beam_size, a.merge_op, a.length_norm, a.max_total,
       a.backptr, a.tokens, a.lengths, a.scores, a.counters, fp,
       BeamSlice{a.t0, a.t1, static_cast<Hyps*>(a.hyps_state)});
@@ -1876,44 +1382,13 @@ cudaError_t launch_beam_cap3(const DecodeArgs& a, cudaStream_t s) {
 template <int BCAP, bool TC>
 cudaError_t launch_beam_cap(const DecodeArgs& a, cudaStream_t s) {
   if constexpr (!TC) {
-    if (a.fused_enc) return launch_beam_cap3<BCAP, false, true>(a, s);
-    if (a.hyps_state) return launch_beam_cap3<BCAP, false, false, true>(a, s);
+    if (a.hyps_state) return launch_beam_cap3<BCAP, false, true>(a, s);
   }
-  return launch_beam_cap3<BCAP, TC, false>(a, s);
-}
-
-template <int BCAP>
-cudaError_t launch_beam_dual(const DecodeArgs& a, cudaStream_t s) {
-  const ModelView m = view_of(*a.m);
-  const int gmax = std::max(1, kRowCap2 / std::max(1, a.beam_size));
-  const int slots = a.cta_slots > 0 ? a.cta_slots : 2 * decode_num_sms_current();
-  const int NC = std::max((a.B + gmax - 1) / gmax, std::min(a.B, slots));
-  const int ns_max = (a.B + NC - 1) / NC;
-  const size_t smem = smem_dual(m) + sizeof(DualSmem) + sizeof(Hyps) * ns_max +
-                      sizeof(BeamCand) * ns_max * (BCAP * BCAP + 2 * BCAP);
-  cudaError_t e = cudaFuncSetAttribute(beam_dual_kernel<BCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  beam_dual_kernel<BCAP><<<NC, kDualThreads, smem, s>>>(
-      m, a.pe, a.frame_splits, a.B, NC, a.beam_size, a.merge_op, a.length_norm, a.max_total,
-      a.backptr, a.tokens, a.lengths, a.scores, a.counters);
-  return cudaGetLastError();
+  return launch_beam_cap3<BCAP, TC>(a, s);
 }
 
 template <bool TC>
 cudaError_t launch_beam_mode(const DecodeArgs& a, cudaStream_t s) {
-  if (!TC && a.beam_impl == 0) {  // exact joiner, dual-residency kernel (opt-in)
-    if (a.beam_size <= 1) return launch_beam_dual<1>(a, s);
-    if (a.beam_size <= 2) return launch_beam_dual<2>(a, s);
-    if (a.beam_size <= 4) return launch_beam_dual<4>(a, s);
-    return launch_beam_dual<8>(a, s);
-  }
-  if (!TC && a.warp_specialized) {  // exact joiner, >= 2 streams per CTA
-    if (a.beam_size <= 1) return launch_beam_ws<1>(a, s);
-    if (a.beam_size <= 2) return launch_beam_ws<2>(a, s);
-    if (a.beam_size <= 4) return launch_beam_ws<4>(a, s);
-    return launch_beam_ws<8>(a, s);
-  }
   if (a.beam_size <= 1) return launch_beam_cap<1, TC>(a, s);
   if (a.beam_size <= 2) return launch_beam_cap<2, TC>(a, s);
   if (a.beam_size <= 4) return launch_beam_cap<4, TC>(a, s);

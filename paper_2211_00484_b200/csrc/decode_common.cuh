@@ -345,13 +345,6 @@ __device__ __forceinline__ void gemm_pass_bal(const ModelView& m, const WPipe& p
   __syncthreads();
 }
 
-#ifdef RNNTG_GEMM_EXTERN
-// gemm_bal.cu: gemm_pass_bal out of line in its own translation unit (one
-// schedule for every kernel).  Returns the chunk counter after the pass.
-__device__ uint32_t gemm_bal_x(const WPipe p, uint32_t g, uint32_t hl, int R, int Vp,
-                               const float* __restrict__ bias, int K, int nc, long long* wc);
-#endif
-
 // Rows from which the SMSP-balanced tiling is used; below, the uniform
 // tilings of gemm_pass (up to 16 equal items of 4 rows x 32*TN columns).
 #ifndef RNNTG_BAL_MIN_R
@@ -360,11 +353,7 @@ __device__ uint32_t gemm_bal_x(const WPipe p, uint32_t g, uint32_t hl, int R, in
 __device__ __forceinline__ void joiner_gemm(const ModelView& m, const WPipe& p,
                                             uint32_t& g, float* HL, int R, long long* wc = nullptr) {
   if (m.Vp == 512 && R >= RNNTG_BAL_MIN_R) {
-#ifdef RNNTG_GEMM_EXTERN
-    g = gemm_bal_x(p, g, smem_u32(HL), R, m.Vp, m.out_b, m.J, p.nc, wc);
-#else
     gemm_pass_bal(m, p, g, HL, R, wc);
-#endif
     return;
   }
   const int rg = (R + 3) >> 2;
@@ -769,169 +758,6 @@ __device__ __forceinline__ void tc_gemm(const ModelView& m, const TcPipe& p, uin
 inline size_t smem_common(const ModelView& m, int bk = kBK) {
   const size_t hl = static_cast<size_t>(max(m.J * kHStride, kRowCap * m.Vp)) * 4;
   return hl + static_cast<size_t>(2) * bk * m.Vp * 4;
-}
-
-// ---------------------------------------------------------------------------
-// Dual-residency exact joiner (two 256-thread CTAs per SM).
-//
-// Each CTA owns <= kRowCap2 joiner rows per frame.  Its 8 warps split the
-// vocabulary by columns — warp w owns columns {w*32 + lane, 256 + w*32 +
-// lane} — and every warp carries ALL of the frame's rows, so the work is
-// balanced for any row count.  out_w streams from L2 in kBK2-row k-chunks
-// through a kStages2-deep ring of `full` mbarriers (no CTA-wide barrier
-// per chunk): `full` completes on the bulk copy's bytes; each warp releases
-// a stage through a shared-memory counter and the last warp to release it
-// refills it, so no warp waits on another inside the GEMM.  The chunk
-// sequence is data independent, so the ring prefetches across frame
-// boundaries.  Two CTAs share each SM so one CTA's latency-bound row
-// reduction / beam step hides behind the other's FMUL/FADD stream.
-// ---------------------------------------------------------------------------
-constexpr int kDualThreads = 256;
-constexpr int kDualWarps = kDualThreads / 32;  // 8
-constexpr int kRowCap2 = 16;                   // joiner rows per CTA per frame
-constexpr int kHStride2 = kRowCap2 + 4;        // k-major h tile stride (floats)
-constexpr int kBK2 = 8;                        // k rows per out_w chunk
-constexpr int kStages2 = 3;
-
-struct DualPipe {
-  uint32_t stage0;   // smem address of stage 0
-  uint32_t stage_bytes;
-  uint64_t* full;    // [kStages2]
-  uint32_t* empty_cnt;  // [kStages2] monotonic release counters
-  int32_t nc;        // chunks per frame
-};
-
-__device__ __forceinline__ void dual_issue(const DualPipe& p, const ModelView& m, uint32_t g) {
-  const int32_t c = static_cast<int32_t>(g % static_cast<uint32_t>(p.nc));
-  const int32_t rows = min(kBK2, m.J - c * kBK2);
-  const uint32_t bytes = static_cast<uint32_t>(rows) * m.Vp * 4u;
-  const uint32_t st = g % kStages2;
-  uint64_t* bar = p.full + st;
-  fence_proxy_async();
-  mbar_expect_tx(bar, bytes);
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          p.stage0 + st * p.stage_bytes),
-      "l"(m.out_wt + static_cast<int64_t>(c) * kBK2 * m.Vp), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void dual_pipe_init(const DualPipe& p, const ModelView& m) {
-  // caller: thread 0, before the CTA's first barrier
-  for (int s = 0; s < kStages2; ++s) {
-    mbar_init(p.full + s, 1);
-    p.empty_cnt[s] = 0;
-  }
-  fence_mbar_init();
-}
-
-__device__ __forceinline__ void dual_pipe_prime(const DualPipe& p, const ModelView& m) {
-  for (int s = 0; s < kStages2; ++s) dual_issue(p, m, s);  // thread 0, after the barrier
-}
-
-__device__ __forceinline__ void dual_pipe_drain(const DualPipe& p, uint32_t g) {
-  // thread 0: the kStages2 chunks prefetched for a frame that never came
-  for (uint32_t x = g; x < g + kStages2; ++x) mbar_wait(p.full + x % kStages2, (x / kStages2) & 1u);
-}
-
-// logits[r][n] = out_b[n] + sum_k out_w[n][k] * h[r][k], k in order, for
-// NG*4 >= R rows.  HL: k-major h tile [J][kHStride2]; the logits are written
-// row-major [R][Vp] over it after the CTA-wide barrier that retires h.
-template <int NG>
-__device__ __forceinline__ void dual_gemm_ng(const ModelView& m, const DualPipe& p, uint32_t& g,
-                                             float* HL, int R) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c0 = warp * 32 + lane, c1 = c0 + kDualWarps * 32;
-  const bool v0 = c0 < m.Vp, v1 = c1 < m.Vp;
-  float acc[NG * 4][2];
-  {
-    const float b0 = v0 ? m.out_b[c0] : 0.0f, b1 = v1 ? m.out_b[c1] : 0.0f;
-#pragma unroll
-    for (int i = 0; i < NG * 4; ++i) {
-      acc[i][0] = b0;
-      acc[i][1] = b1;
-    }
-  }
-  const uint32_t hbase = smem_u32(HL);
-  for (int32_t c = 0; c < p.nc; ++c, ++g) {
-    const uint32_t st = g % kStages2;
-    mbar_wait(p.full + st, (g / kStages2) & 1u);
-    const uint32_t ws = p.stage0 + st * p.stage_bytes;
-    const int kk_end = min(kBK2, m.J - c * kBK2);
-    const uint32_t hp = hbase + static_cast<uint32_t>(c * kBK2 * kHStride2) * 4u;
-    if (kk_end == kBK2) {
-#pragma unroll
-      for (int kk = 0; kk < kBK2; ++kk) {
-        const uint32_t wr = ws + static_cast<uint32_t>(kk * m.Vp) * 4u;
-        float w0 = 0.0f, w1 = 0.0f;
-        if (v0) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(w0) : "r"(wr + c0 * 4u));
-        if (v1) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(w1) : "r"(wr + c1 * 4u));
-#pragma unroll
-        for (int q = 0; q < NG; ++q) {
-          const float4 h4 = lds128(hp + static_cast<uint32_t>(kk * kHStride2 + q * 4) * 4u);
-          const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            acc[q * 4 + i][0] = fadd(acc[q * 4 + i][0], fmul(w0, hv[i]));
-            acc[q * 4 + i][1] = fadd(acc[q * 4 + i][1], fmul(w1, hv[i]));
-          }
-        }
-      }
-    } else {
-      for (int kk = 0; kk < kk_end; ++kk) {
-        const uint32_t wr = ws + static_cast<uint32_t>(kk * m.Vp) * 4u;
-        float w0 = 0.0f, w1 = 0.0f;
-        if (v0) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(w0) : "r"(wr + c0 * 4u));
-        if (v1) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(w1) : "r"(wr + c1 * 4u));
-#pragma unroll
-        for (int q = 0; q < NG; ++q) {
-          const float4 h4 = lds128(hp + static_cast<uint32_t>(kk * kHStride2 + q * 4) * 4u);
-          const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            acc[q * 4 + i][0] = fadd(acc[q * 4 + i][0], fmul(w0, hv[i]));
-            acc[q * 4 + i][1] = fadd(acc[q * 4 + i][1], fmul(w1, hv[i]));
-          }
-        }
-      }
-    }
-    // Release the stage; the warp that releases it last refills it with
-    // chunk g + kStages2 (no warp ever blocks on the others here).  The
-    // counter is monotonic: arrivals 8u..8u+7 belong to the stage's u-th use.
-    __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();  // this warp's reads of the stage happen-before the refill
-      const uint32_t n = atomicAdd(p.empty_cnt + st, 1u);
-      if (n % kDualWarps == kDualWarps - 1) {
-        __threadfence_block();
-        dual_issue(p, m, g + kStages2);
-      }
-    }
-  }
-  __syncthreads();  // every warp is done reading h: the logits may overwrite it
-#pragma unroll
-  for (int i = 0; i < NG * 4; ++i) {
-    if (i < R) {
-      float* lr = HL + static_cast<int64_t>(i) * m.Vp;
-      if (v0) lr[c0] = acc[i][0];
-      if (v1) lr[c1] = acc[i][1];
-    }
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void dual_gemm(const ModelView& m, const DualPipe& p, uint32_t& g,
-                                          float* HL, int R) {
-  const int ng = (R + 3) >> 2;
-  if (ng <= 1) dual_gemm_ng<1>(m, p, g, HL, R);
-  else if (ng == 2) dual_gemm_ng<2>(m, p, g, HL, R);
-  else if (ng == 3) dual_gemm_ng<3>(m, p, g, HL, R);
-  else dual_gemm_ng<4>(m, p, g, HL, R);
-}
-
-inline size_t smem_dual(const ModelView& m) {
-  const size_t hl = static_cast<size_t>(max(m.J * kHStride2, kRowCap2 * m.Vp)) * 4;
-  return hl + static_cast<size_t>(kStages2) * kBK2 * m.Vp * 4;
 }
 
 inline ModelView view_of(const DeviceModel& d) {

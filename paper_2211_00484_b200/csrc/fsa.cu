@@ -513,7 +513,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         }
       // ---- prune_streams ----
       if (grp.tid == 0) {
-        if (max_states > kMaxStates && D > kMaxStates) atomicExch(error_flag, 4);
+        // max_states beyond the device cap binds when more than kMaxStates
+        // distinct keys are at or above the floor: either the hash already
+        // holds more, or it holds exactly kMaxStates while candidates in bins
+        // past the hot threshold were never scanned.
+        if (max_states > kMaxStates && (D > kMaxStates || (D == kMaxStates && S.bstar < kBins)))
+          atomicExch(error_flag, 4);
         const int npass = min(K, D);  // all hot entries are >= floor
         int kept[kMaxStates];
         int nk = 0, nsurv = 0;

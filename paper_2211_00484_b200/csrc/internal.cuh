@@ -116,16 +116,8 @@ struct DecodeArgs {
   // beam
   int32_t beam_size, merge_op, length_norm, max_total;
   int32_t joiner_bf16;      // 1: tcgen05 bf16 joiner variant (not token-exact)
-  int32_t warp_specialized; // 1: beam_ws_kernel (GEMM / POST warp groups)
-  int32_t beam_impl;        // 1: single 512-thread CTA per SM (default); 0: dual-residency kernel
-  int32_t cta_slots;        // dual kernel: CTA slots this launch may fill (0: 2 x SMs)
   uint32_t* backptr;        // device [(sum T + B) * kMaxBeam]
   void* node_pool;          // beam S > 1: device int2 [(sum T * cap + B) * kMaxBeam] (parent, token) nodes
-  // beam, fused encoder projection (pe computed inside the decode kernel):
-  const float* fused_enc;   // device [sum T][D] frames, or nullptr (pe precomputed by K1)
-  float* fused_pe;          // device [sum T][J] written by the kernel (== pe)
-  const int32_t* ready;     // device: number of frame slices of fused_enc that have landed
-  int32_t slice_frames;     // frames per slice (slice s = frames [s*slice_frames, ...) of every stream)
   // beam, time-sliced launches (host frames: the copy and K1 of slice k+1
   // overlap the decode of slice k): this launch decodes frames [t0, t1) of
   // every stream; hypothesis sets persist between launches in hyps_state.

@@ -23,7 +23,7 @@ def test_sliced_host_frames_match_oracle_and_device_path(T, B, first, cap):
     m = H.model(V=500, seed=1, blank_bias=0.4)
     _, enc, splits = H.frames(m, [T] * B, seed0=52000 + T)
     sliced = H.decoder_env(m, RNNTG_SLICED="1", RNNTG_SLICE_FIRST=first, RNNTG_SLICE_MAX=cap)
-    plain = H.decoder_env(m, RNNTG_SLICED="0", RNNTG_FUSED_PE="0")
+    plain = H.decoder_env(m, RNNTG_SLICED="0")
     try:
         got, sc = sliced.beam_search_batch(enc, splits, BeamParams(beam_size=4))
         assert sliced.stats()["stream_frames"] == B * T
@@ -104,7 +104,7 @@ def test_sliced_bench_scale_matches_single_launch_and_oracle_sample():
     enc = np.ascontiguousarray(np.concatenate([enc_u] * (B // U)).reshape(B * T, 512))
     splits = (np.arange(B + 1) * T).astype(np.int32)
     sliced = H.decoder_env(m, RNNTG_SLICED="1")
-    plain = H.decoder_env(m, RNNTG_SLICED="0", RNNTG_FUSED_PE="0")
+    plain = H.decoder_env(m, RNNTG_SLICED="0")
     try:
         osp, tok, sc = sliced.beam_search_batch(torch.from_numpy(enc).pin_memory(), splits,
                                                 BeamParams(beam_size=4), as_lists=False)

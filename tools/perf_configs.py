@@ -93,13 +93,13 @@ def run(name, m, B, T, kind, params, graph=None, ref_graph=None, cpu_streams=Non
     dec.close()
 
 
-m4 = ref.model(500, 80, 512, 512, 512, 1, 0.4)
+m4 = ref.model(500, 80, 512, 512, 512, 0, 0.4)
 run("config1 greedy B=8 T=200", m4, 8, 200, "greedy", {}, cpu_streams=8)
 run("config2 beam4 B=256 T=500", m4, 256, 500, "beam", {"beam_size": 4}, cpu_streams=2 * THREADS)
 tg = ref.graph_trivial(500)
 run("config3 fsa trivial (4,8,4) B=512 T=500", m4, 512, 500, "fsa", [4.0, 8, 4], graph=tg.g, ref_graph=tg,
     cpu_streams=2 * THREADS)
-m14 = ref.model(500, 80, 512, 512, 512, 1, -1.4)
+m14 = ref.model(500, 80, 512, 512, 512, 0, -1.4)
 lg = ref.graph_from_arpa(synthetic_arpa(500), 500)
 out["ngram_graph"] = {"states": lg.g.num_states, "arcs": lg.g.num_arcs}
 run("config4 fsa ngram (8,64,8) B=256 T=500", m14, 256, 500, "fsa", [8.0, 64, 8], graph=lg.g, ref_graph=lg,

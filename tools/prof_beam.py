@@ -1,6 +1,5 @@
 """Beam-search timing on the bench workload (reference-encoder frames in HBM),
-for A/B comparisons of the decode kernels (RNNTG_BEAM_IMPL / RNNTG_WS) and
-for ncu captures.  Usage: python tools/prof_beam.py [B] [T] [reps]"""
+for A/B comparisons of builds / knobs and for ncu captures.  Usage: python tools/prof_beam.py [B] [T] [reps]"""
 import json
 import sys
 
@@ -13,10 +12,10 @@ from paper_2211_00484_b200.api import BeamParams, Decoder, ModelWeights  # noqa:
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-w = bench.synthetic_weights()
+w = bench.reference_weights()
 dec = Decoder(ModelWeights.from_dict(w))
 dec.set_encoder(w)
-d_enc, splits = bench.synthetic_frames(dec, B, T, seed=100, device="cuda:0")
+d_enc, splits = bench.synthetic_frames(dec, 0, B, T, "cuda:0")
 tok = torch.zeros(B * T, dtype=torch.int32, device="cuda")
 sc = torch.zeros(B, dtype=torch.float64, device="cuda")
 out = []
@@ -31,7 +30,6 @@ print(json.dumps(dict(B=B, T=T, decode_ms=out, gpu_ms=st["gpu_ms"], fps_decode=B
                       gather_share=round(st["gather_cycles"] / tot, 3),
                       gemm_wait_share=round(st["gemm_wait_cycles"] / tot, 4),
                       gemm_bar_share=round(st["lattice_arcs"] / tot, 4),
-                      fused_pe_share=[round(x / tot, 4) for x in st["fused_pe_cycles"]],
                       padded_per_row=st["joiner_rows_computed"] / max(1, st["joiner_rows"]),
                       gemm_mac_per_s_per_sm=st["joiner_rows_computed"] * 512 * 512 /
                       max(1e-9, st["phase_cycles"][1] / 1.965e9),

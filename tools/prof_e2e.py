@@ -14,10 +14,10 @@ from paper_2211_00484_b200.api import BeamParams, Decoder, ModelWeights  # noqa:
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-w = bench.synthetic_weights()
+w = bench.reference_weights()
 dec = Decoder(ModelWeights.from_dict(w))
 dec.set_encoder(w)
-d_enc, splits = bench.synthetic_frames(dec, B, T, seed=100, device="cuda:0")
+d_enc, splits = bench.synthetic_frames(dec, 0, B, T, "cuda:0")
 pin = torch.from_numpy(d_enc.cpu().numpy()).pin_memory()
 dec.beam_search_batch(pin, splits, BeamParams(4))
 wall, gpu = [], []
