@@ -368,114 +368,6 @@ __device__ __forceinline__ void joiner_gemm(const ModelView& m, const WPipe& p,
   }
 }
 
-// ---------------------------------------------------------------------------
-// Warp-specialised variant of C for a subset of the CTA's warps (the "GEMM
-// group": warps 0..NW-1).  Same arithmetic and ordering as gemm_pass; the
-// stage hand-off uses named barrier `bar_id` over the group instead of
-// __syncthreads, and nothing after the last chunk (the caller signals the
-// consumers of the logits).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void nbar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-__device__ __forceinline__ void nbar_arrive(int id, int nthreads) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-template <int TN>
-__device__ __forceinline__ void gemm_pass_g(const ModelView& m, const WPipe& p, uint32_t& g,
-                                            float* HL, int hstride, int R, int NW, int gw,
-                                            int bar_id) {
-  constexpr int CW = 32 * TN;
-  const int lane = threadIdx.x & 31;
-  const int NB = m.Vp / CW;
-  const int items = ((R + 3) >> 2) * NB;
-  const bool active = gw < items;
-  const int rg = gw / NB, blk = gw % NB;
-  const int cbase = blk * CW;
-  int col[TN];
-#pragma unroll
-  for (int j = 0; j < TN; ++j) {
-    if constexpr (TN == 8) col[j] = cbase + (j < 4 ? lane * 4 + j : 128 + lane * 4 + (j - 4));
-    else col[j] = cbase + lane * TN + j;
-  }
-  float acc[4][TN];
-#pragma unroll
-  for (int j = 0; j < TN; ++j) {
-    const float b = active ? m.out_b[col[j]] : 0.0f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i][j] = b;
-  }
-  for (int32_t c = 0; c < p.nc; ++c, ++g) {
-    const uint32_t st = g & 1u;
-    mbar_wait(p.bar + st, (g >> 1) & 1u);
-    if (active) {
-      const uint32_t ws = smem_u32(p.stage[0]) + st * static_cast<uint32_t>(p.bk * m.Vp * 4);
-      const int kk_end = min(p.bk, m.J - c * p.bk);
-      const float* hp = HL + static_cast<int64_t>(c * p.bk) * hstride + rg * 4;
-#pragma unroll 4
-      for (int kk = 0; kk < kk_end; ++kk) {
-        const float4 h4 = *reinterpret_cast<const float4*>(hp + kk * hstride);
-        const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
-        float wv[TN];
-        const uint32_t wr = ws + static_cast<uint32_t>(kk * m.Vp) * 4u;
-        if constexpr (TN == 8) {
-          const float4 wa = lds128(wr + col[0] * 4u);
-          const float4 wb = lds128(wr + col[4] * 4u);
-          wv[0] = wa.x; wv[1] = wa.y; wv[2] = wa.z; wv[3] = wa.w;
-          wv[4] = wb.x; wv[5] = wb.y; wv[6] = wb.z; wv[7] = wb.w;
-        } else if constexpr (TN == 4) {
-          const float4 wa = lds128(wr + col[0] * 4u);
-          wv[0] = wa.x; wv[1] = wa.y; wv[2] = wa.z; wv[3] = wa.w;
-        } else {
-          const float2 wa = lds64(wr + col[0] * 4u);
-          wv[0] = wa.x; wv[1] = wa.y;
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j)
-            acc[i][j] = fadd(acc[i][j], fmul(wv[j], hv[i]));
-      }
-    }
-    nbar_sync(bar_id, NW * 32);  // the GEMM group is done with this stage
-    if (gw == 0 && lane == 0) wpipe_issue(p, m, g + 2);
-  }
-  if (active) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = rg * 4 + i;
-      if (r < R) {
-        float* lr = HL + static_cast<int64_t>(r) * m.Vp;
-        if constexpr (TN == 8) {
-          *reinterpret_cast<float4*>(lr + col[0]) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-          *reinterpret_cast<float4*>(lr + col[4]) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
-        } else if constexpr (TN == 4) {
-          *reinterpret_cast<float4*>(lr + col[0]) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-        } else {
-          *reinterpret_cast<float2*>(lr + col[0]) = make_float2(acc[i][0], acc[i][1]);
-        }
-      }
-    }
-  }
-}
-
-// Column-block width for R rows on NW warps: the largest item count that
-// fits the group, ties to the wider (more reuse) block.
-__device__ __forceinline__ void joiner_gemm_g(const ModelView& m, const WPipe& p, uint32_t& g,
-                                              float* HL, int hstride, int R, int NW, int gw,
-                                              int bar_id) {
-  const int rg = (R + 3) >> 2;
-  const int i8 = rg * (m.Vp >> 8), i4 = rg * (m.Vp >> 7), i2 = rg * (m.Vp >> 6);
-  int best = i8 <= NW ? i8 : 0, tn = 8;
-  if (i4 <= NW && i4 > best) best = i4, tn = 4;
-  if (i2 <= NW && i2 > best) best = i2, tn = 2;
-  if (best == 0) tn = 8;  // more items than warps cannot happen for R <= 4*NW/2
-  if (tn == 8) gemm_pass_g<8>(m, p, g, HL, hstride, R, NW, gw, bar_id);
-  else if (tn == 4) gemm_pass_g<4>(m, p, g, HL, hstride, R, NW, gw, bar_id);
-  else gemm_pass_g<2>(m, p, g, HL, hstride, R, NW, gw, bar_id);
-}
-
 // h tile for a thread group of nt threads (tid in [0, nt)), k-major stride.
 __device__ __forceinline__ void build_h_g(const ModelView& m, const float* pe, const int64_t* row_pe,
                                           const int32_t* row_ctx, int R, float* HL, int hstride,

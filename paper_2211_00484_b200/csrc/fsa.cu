@@ -55,6 +55,7 @@ struct FsaStream {
   int32_t n_act, num_nodes, nrows, row_base;
   int32_t n_raw, n_hot, n_sort, n_surv;
   int32_t bstar, arc_count, arc_off, flag;
+  unsigned long long m_first, m_keep;  // prune: first-occurrence / survivor masks over sorted entries
   double best, floor;
   int32_t act_ctx[kMaxStates], act_state[kMaxStates], act_node[kMaxStates], act_row[kMaxStates];
   double act_score[kMaxStates];
@@ -66,7 +67,7 @@ struct FsaStream {
   int32_t bins[kBins];
   uint64_t hkey[kHashCap];
   unsigned long long hval[kHashCap];
-  uint64_t s1[kHashCap], s2[kHashCap];  // sort keys
+  uint64_t s1[kHashCap], s2[kHashCap];  // compacted hot entries (~score, key)
   int32_t surv_ctx[kMaxStates], surv_state[kMaxStates];
   double surv_score[kMaxStates];
   uint64_t shkey[kSurvHash];
@@ -366,32 +367,38 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
 
     if (live) {
       // ---- expand_arcs ----
-      if (grp.tid == 0) {
-        // Segment offsets of the raw candidates and an upper bound on the
-        // frame's best candidate: tuple i scores at most
-        // score_i + max(0, max arc weight of its state) + max_k lp_i[k].
-        int off = 0;
-        double ub = -INFINITY;
-        for (int i = 0; i < S.n_act; ++i) {
+      // Segment offsets of the raw candidates (one thread per active tuple,
+      // group scan) and an upper bound on the frame's best candidate: tuple i
+      // scores at most score_i + max(0, max arc weight of its state) +
+      // max_k lp_i[k].
+      {
+        const int i = grp.tid;
+        int cnt = 0;
+        double bound = -INFINITY;
+        if (i < S.n_act) {
           const int st = S.act_state[i];
-          S.act_off[i] = off;
-          S.act_abase[i] = gsplits[st];
-          off += 1 + gsplits[st + 1] - gsplits[st];
-          const double bound =
-              S.act_score[i] + fmax(0.0, gmaxw[st]) + C.row_lpmax[S.row_base + S.act_row[i]];
-          ub = fmax(ub, bound);
+          const int a0 = gsplits[st], a1 = gsplits[st + 1];
+          S.act_abase[i] = a0;
+          cnt = 1 + a1 - a0;
+          bound = S.act_score[i] + fmax(0.0, gmaxw[st]) + C.row_lpmax[S.row_base + S.act_row[i]];
         }
-        S.act_off[S.n_act] = off;
-        S.n_raw = off;
-        S.ub = ub + 1e-9 * fabs(ub) + 1e-12;  // absorbs the rounding of the bound itself
-        if (off > kMaxRaw) atomicExch(error_flag, 6);
+        int total = 0;
+        const int off = group_scan(grp, S, cnt, &total);
+        if (i < S.n_act) S.act_off[i] = off;
+        const double ubm = group_max(grp, S, bound);
+        if (grp.tid == 0) {
+          S.act_off[S.n_act] = total;
+          S.n_raw = total;
+          S.ub = ubm + 1e-9 * fabs(ubm) + 1e-12;  // absorbs the rounding of the bound itself
+          if (total > kMaxRaw) atomicExch(error_flag, 6);
+        }
       }
       for (int b = grp.tid; b < kBins; b += nt) S.bins[b] = 0;
       for (int b = grp.tid; b < kHashCap; b += nt) {
         S.hkey[b] = kEmptyKey;
         S.hval[b] = 0ull;
       }
-      for (int w = grp.tid; w < kMaxRaw / 32; w += nt) S.mbits[w] = 0u;
+      for (int w = grp.tid; w < (min(S.n_raw, kMaxRaw) + 31) / 32; w += nt) S.mbits[w] = 0u;
       grp.sync();
       const int nraw = min(S.n_raw, kMaxRaw);
       const double ub = S.ub;
@@ -413,19 +420,37 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       const double best = group_max(grp, S, mx);
       const double floor = best - beam;  // prune_streams 247-248
       // Smallest prefix of bins lying wholly at or above the floor that holds
-      // M candidates; kBins = every candidate at or above the floor.
-      if (grp.tid == 0) {
-        int cum = 0, bstar = kBins;
-        for (int b = 0; b < kBins; ++b) {
-          if (ub - (b + 1) / scale < floor) break;
-          cum += S.bins[b];
-          if (cum >= M) {
-            bstar = b;
-            break;
+      // M candidates; kBins = every candidate at or above the floor.  The bins
+      // become inclusive prefix counts (a group scan over contiguous runs of
+      // bins); bin b qualifies if it lies above the floor and its prefix
+      // reaches M, and validity is monotone in b, so bstar = the smallest
+      // qualifying bin.
+      {
+        constexpr int kMaxRun = kBins / 128;  // nt >= 128
+        const int run = kBins / nt > 0 ? kBins / nt : 1;
+        const int b0 = grp.tid * run;
+        int loc[kMaxRun > 0 ? kMaxRun : 1];
+        int sum = 0;
+#pragma unroll
+        for (int j = 0; j < (kMaxRun > 0 ? kMaxRun : 1); ++j) {
+          loc[j] = (j < run && b0 + j < kBins) ? S.bins[b0 + j] : 0;
+          sum += loc[j];
+        }
+        if (grp.tid == 0) {
+          S.bstar = kBins;
+          S.n_hot = 0;
+        }
+        int total = 0;
+        int cum = group_scan(grp, S, sum, &total);
+#pragma unroll
+        for (int j = 0; j < (kMaxRun > 0 ? kMaxRun : 1); ++j) {
+          const int b = b0 + j;
+          if (j < run && b < kBins) {
+            cum += loc[j];
+            S.bins[b] = cum;
+            if (cum >= M && !(ub - (b + 1) / scale < floor)) atomicMin(&S.bstar, b);
           }
         }
-        S.bstar = bstar;
-        S.n_hot = 0;
       }
       grp.sync();
       // Pass B: hot candidates into the hash; widen the threshold if
@@ -461,21 +486,23 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         if (S.n_hot > kHashCap / 2) break;
         grp.sync();
         if (grp.tid == 0) {  // widen by another M candidates (max is idempotent)
-          int b = bstar + 1, cum = 0;
+          int b = bstar + 1;
           for (; b < kBins; ++b) {
             if (ub - (b + 1) / scale < floor) {
               b = kBins;
               break;
             }
-            cum += S.bins[b];
-            if (cum >= M) break;
+            if (S.bins[b] - S.bins[bstar] >= M) break;  // bins hold prefix counts
           }
           S.bstar = min(b, kBins);
         }
         grp.sync();
       }
       if (grp.tid == 0 && S.n_hot > kHashCap * 3 / 4) atomicExch(error_flag, 3);
-      // Compact the distinct keys and bitonic-sort by (score desc, key asc).
+      // Compact the distinct keys; the first min(K, D) of them in (score
+      // desc, key asc) order are found by rank (each entry counts the
+      // entries before it: keys are distinct, so ranks are too) and land in
+      // hkey / hval[rank] (the hash is no longer needed).
       if (grp.tid == 0) S.n_sort = 0;
       grp.sync();
       for (int b = grp.tid; b < kHashCap; b += nt)
@@ -486,32 +513,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         }
       grp.sync();
       const int D = S.n_sort;
-      int NP = 1;
-      while (NP < D) NP <<= 1;
-      for (int p = D + grp.tid; p < NP; p += nt) {
-        S.s1[p] = ~0ull;
-        S.s2[p] = ~0ull;
-      }
-      grp.sync();
-      for (int k2 = 2; k2 <= NP; k2 <<= 1)
-        for (int j = k2 >> 1; j > 0; j >>= 1) {
-          for (int p = grp.tid; p < NP; p += nt) {
-            const int q = p ^ j;
-            if (q > p) {
-              const bool up = (p & k2) == 0;
-              const uint64_t a1 = S.s1[p], a2 = S.s2[p], b1 = S.s1[q], b2 = S.s2[q];
-              const bool gt = a1 > b1 || (a1 == b1 && a2 > b2);
-              if (gt == up) {
-                S.s1[p] = b1;
-                S.s2[p] = b2;
-                S.s1[q] = a1;
-                S.s2[q] = a2;
-              }
-            }
-          }
-          grp.sync();
+      const int npass = min(K, D);  // all hot entries are >= floor
+      for (int p = grp.tid; p < D; p += nt) {
+        const uint64_t a1 = S.s1[p], a2 = S.s2[p];
+        int rk = 0;
+        for (int q = 0; q < D; ++q) {
+          const uint64_t b1 = S.s1[q], b2 = S.s2[q];
+          rk += (b1 < a1 || (b1 == a1 && b2 < a2)) ? 1 : 0;
         }
-      // ---- prune_streams ----
+        if (rk < npass) {
+          S.hkey[rk] = a2;
+          S.hval[rk] = ~a1;
+        }
+      }
       if (grp.tid == 0) {
         // max_states beyond the device cap binds when more than kMaxStates
         // distinct keys are at or above the floor: either the hash already
@@ -519,29 +533,41 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         // past the hot threshold were never scanned.
         if (max_states > kMaxStates && (D > kMaxStates || (D == kMaxStates && S.bstar < kBins)))
           atomicExch(error_flag, 4);
-        const int npass = min(K, D);  // all hot entries are >= floor
-        int kept[kMaxStates];
-        int nk = 0, nsurv = 0;
-        for (int p = 0; p < npass; ++p) {
-          const int32_t c = static_cast<int32_t>(S.s2[p] >> 32);
-          bool found = false;
-          for (int z = 0; z < nk; ++z) found = found || kept[z] == c;
-          if (!found && nk < max_contexts) kept[nk++] = c;
-        }
-        for (int p = 0; p < npass; ++p) {
-          const int32_t c = static_cast<int32_t>(S.s2[p] >> 32);
-          bool found = false;
-          for (int z = 0; z < nk; ++z) found = found || kept[z] == c;
-          if (found) {
-            S.surv_ctx[nsurv] = c;
-            S.surv_state[nsurv] = static_cast<int32_t>(S.s2[p] & 0xffffffffu);
-            S.surv_score[nsurv] = dbl_of(~S.s1[p]);
-            ++nsurv;
-          }
-        }
-        S.n_surv = nsurv;
+        S.m_first = 0ull;
+        S.m_keep = 0ull;
         S.best = best;
         S.floor = floor;
+      }
+      grp.sync();
+      // ---- prune_streams (fsa_search.hpp:240-283) ----
+      // In sorted order, the first max_contexts distinct contexts are kept;
+      // a passing entry survives iff its context is kept.  Entry p's context
+      // is kept iff at most max_contexts distinct contexts appear up to its
+      // first occurrence fo: popcount of the first-occurrence mask over
+      // [0, fo].  Survivors keep the sorted order (mask prefix counts).
+      {
+        const int p = grp.tid;
+        int fo = p;
+        if (p < npass) {
+          const int32_t c = static_cast<int32_t>(S.hkey[p] >> 32);
+          for (int q = 0; q < p; ++q)
+            if (static_cast<int32_t>(S.hkey[q] >> 32) == c) {
+              fo = q;
+              break;
+            }
+          if (fo == p) atomicOr(&S.m_first, 1ull << p);
+        }
+        grp.sync();
+        const bool keep = p < npass && __popcll(S.m_first & ((2ull << fo) - 1ull)) <= max_contexts;
+        if (keep) atomicOr(&S.m_keep, 1ull << p);
+        grp.sync();
+        if (keep) {
+          const int x = __popcll(S.m_keep & ((1ull << p) - 1ull));
+          S.surv_ctx[x] = static_cast<int32_t>(S.hkey[p] >> 32);
+          S.surv_state[x] = static_cast<int32_t>(S.hkey[p] & 0xffffffffu);
+          S.surv_score[x] = dbl_of(S.hval[p]);
+        }
+        if (p == 0) S.n_surv = __popcll(S.m_keep);
       }
       for (int b = grp.tid; b < kSurvHash; b += nt) S.shkey[b] = kEmptyKey;
       grp.sync();
@@ -597,8 +623,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       if (grp.tid == 0) {
         const unsigned long long off = atomicAdd(lat_count, static_cast<unsigned long long>(total));
         if (static_cast<int64_t>(off + total) > lat_cap) {
-          atomicExch(error_flag, 1);
+          atomicExch(error_flag, 1);  // the host regrows the pool and decodes again
           S.arc_off = -1;
+          S.flag |= 2;  // this stream's lattice is incomplete: no best path
         } else {
           S.arc_off = static_cast<int32_t>(off);
         }
@@ -642,7 +669,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         finfo[fbase + t] = make_int4(S.arc_off, S.arc_count, S.num_nodes, nsurv);
         S.n_act = nsurv;
         S.num_nodes += nsurv;
-        if (nsurv == 0) S.flag = 1;  // dead stream (233-238): cannot happen with finite scores
+        if (nsurv == 0) S.flag |= 1;  // dead stream (233-238): cannot happen with finite scores
       }
       grp.sync();
     }
@@ -657,7 +684,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
 
   // ---- lattice_to_best_seq(kMax) = best_path on the stream's lattice ----
   const long long cb0 = clock64();
-  if (have && grp.tid == 0) {
+  if (have && grp.tid == 0 && !(S.flag & 2)) {
     double* nb = nodebest + nbase;
     const int32_t nn = S.num_nodes;
     // Layer T nodes reach the super-final node by a score-0 arc.

@@ -132,3 +132,31 @@ def test_fsa_invalid_params(big):
         Graph(dec, 1, np.array([0, 1], np.int32), np.zeros(1, np.int32), np.zeros(1, np.int32), np.zeros(1))
     with pytest.raises(ValidationError):
         Graph(dec, 1, np.array([0, 1], np.int32), np.zeros(1, np.int32), np.array([500], np.int32), np.zeros(1))
+
+
+def test_lattice_pool_overflow_regrows_and_device_frames(big, monkeypatch):
+    """A lattice pool far too small for the call: every stream's lattice
+    overflows, best path is skipped for the incomplete lattices, the host
+    regrows the pool and decodes again — same tokens / scores as a call with
+    a large pool, for host and for device-resident frames."""
+    import torch
+
+    from paper_2211_00484_b200.api import FsaParams, Graph
+
+    m, dec = big
+    feats, enc, splits = H.frames(m, [60] * 40, seed0=61000)
+    g = Graph.trivial(dec)
+    want, want_sc = dec.fsa_beam_search(enc, splits, g, FsaParams(4.0, 8, 4))
+    monkeypatch.setenv("RNNTG_LAT_CAP", "1024")
+    got, sc = dec.fsa_beam_search(enc, splits, g, FsaParams(4.0, 8, 4))
+    assert got == want and np.array_equal(sc, want_sc)
+    d_enc = torch.from_numpy(enc).cuda()
+    tok = torch.zeros(int(splits[-1]), dtype=torch.int32, device="cuda")
+    dsc = torch.zeros(len(splits) - 1, dtype=torch.float64, device="cuda")
+    osp, tok, dsc = dec.fsa_beam_search(d_enc, splits, g, FsaParams(4.0, 8, 4), tok, dsc)
+    t = tok.cpu().numpy()
+    assert [t[osp[i] : osp[i + 1]].tolist() for i in range(len(splits) - 1)] == want
+    assert np.array_equal(dsc.cpu().numpy(), want_sc)
+    monkeypatch.delenv("RNNTG_LAT_CAP")
+    osp, tok, dsc = dec.fsa_beam_search(d_enc, splits, g, FsaParams(4.0, 8, 4), tok, dsc)
+    assert np.array_equal(dsc.cpu().numpy(), want_sc)

@@ -1,0 +1,76 @@
+"""FSA fast beam search on the BASELINE config 3 / config 4 workloads with
+frames resident in HBM: timing, occupancy counters and a roofline line per
+config; also the target of the ncu captures of fsa_kernel.
+
+    python tools/prof_fsa.py [3|4] [B] [T] [reps]
+
+Inputs: init_model(seed 0) weights (blank bias +0.4 for config 3, -1.4 for
+config 4), DetRng features through the GPU encoder; config 4's graph is the
+1,003,931-arc synthetic trigram graph built by the reference's ARPA reader
+(development tool: graph construction only)."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2211_00484_b200.api import (  # noqa: E402
+    Decoder, FsaParams, Graph, ModelWeights, gaussian_features, init_model_weights)
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+B = (int(sys.argv[2]) if len(sys.argv) > 2 else 0) or (512 if cfg == 3 else 256)
+T = int(sys.argv[3]) if len(sys.argv) > 3 else 500
+reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
+bias = 0.4 if cfg == 3 else -1.4
+w = init_model_weights(500, 80, 512, 512, 512, seed=0, blank_bias=bias)
+dec = Decoder(ModelWeights.from_dict(w))
+dec.set_encoder(w)
+splits = (np.arange(B + 1) * T).astype(np.int32)
+feats = torch.from_numpy(gaussian_features(30000 if cfg == 3 else 40000, B, T, 80)).cuda()
+enc = torch.empty((B * T, 512), dtype=torch.float32, device="cuda")
+dec.encoder_forward(feats, splits, enc)
+del feats
+if cfg == 3:
+    g = Graph.trivial(dec)
+    params = FsaParams(4.0, 8, 4)
+    arcs_in_graph = 499
+else:
+    from oracle.py_oracle import Reference, synthetic_arpa
+
+    rg = Reference().graph_from_arpa(synthetic_arpa(500), 500).g
+    g = Graph(dec, rg.num_states, rg.arc_splits, rg.dst, rg.label, rg.weight)
+    params = FsaParams(8.0, 64, 8)
+    arcs_in_graph = rg.num_arcs
+tok = torch.zeros(B * T, dtype=torch.int32, device="cuda")
+sc = torch.zeros(B, dtype=torch.float64, device="cuda")
+ms = []
+for r in range(reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    osp, _, _ = dec.fsa_beam_search(enc, splits, g, params, tok, sc)
+    e1.record()
+    torch.cuda.synchronize()
+    ms.append(e0.elapsed_time(e1))
+st = dec.stats()
+sf = st["stream_frames"]
+best = min(ms)
+dec_ms = st["decode_ms"]
+# algorithmic work: joiner 2*V*J per row + K1 2*J*D per stream-frame;
+# logical arc bytes 16 B per expanded arc + 24 B per lattice arc written
+flops = 2.0 * 500 * 512 * st["joiner_rows"]
+arc_bytes = 16.0 * st["arcs_expanded"] + 24.0 * st["lattice_arcs"]
+ph = st["phase_cycles"]
+tot = sum(ph[:3]) or 1
+print(json.dumps(dict(
+    config=cfg, B=B, T=T, params=[params.beam, params.max_states, params.max_contexts], graph_arcs=arcs_in_graph,
+    call_ms=ms, decode_ms=dec_ms, frames_per_s=B * T / (best * 1e-3),
+    rows_per_sf=st["joiner_rows"] / sf, arcs_per_sf=st["arcs_expanded"] / sf,
+    lattice_arcs_per_sf=st["lattice_arcs"] / sf, tokens_per_frame=int(osp[-1]) / (B * T),
+    joiner_tflops=flops / (dec_ms * 1e-3) / 1e12,
+    logical_arc_gbs=arc_bytes / (dec_ms * 1e-3) / 1e9,
+    phase_share={"h_build": round(ph[0] / tot, 3), "joiner_gemm": round(ph[1] / tot, 3),
+                 "lse_expand_prune": round(ph[2] / tot, 3)},
+    best_path_cycles=ph[3])))
