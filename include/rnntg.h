@@ -214,6 +214,17 @@ rnntg_status rnntg_fsa_lattice(rnntg_model_t model, int32_t stream,
                                int32_t capacity, int32_t* src, int32_t* dst,
                                int32_t* label, double* score);
 
+/* The lattice of `stream` as text, byte-identical to the reference's
+ * serialize_fsa_text (fsa.hpp:243-262) of that stream's fsa_beam_search
+ * lattice, prefixed with serialize_lattice's "# stream=S frames=T" line
+ * (fsa_search.hpp:429-435) when with_header != 0 -- the CLI's
+ * lattice_NNNN.txt (rnnt_main.cpp:303-307).  *length is always set (bytes,
+ * excluding the terminating NUL); call with capacity 0 to size, then with
+ * capacity >= *length + 1. */
+rnntg_status rnntg_fsa_lattice_text(rnntg_model_t model, int32_t stream,
+                                    int32_t with_header, char* buf,
+                                    int64_t capacity, int64_t* length);
+
 /* The reference's toy encoder on the GPU (encoder_forward, model.hpp:224-238;
  * SURVEY.md §8f "next" row 3): enc[t] = tanhf(b2 + W2 . tanhf(b1 + W1 . f[t])),
  * bit-exact with the reference (same sequential fp32 affine and glibc tanhf
@@ -276,6 +287,16 @@ rnntg_status rnntg_debug_joiner_logits(rnntg_model_t model, const float* enc,
 rnntg_status rnntg_debug_tanhf_chunk_hashes(int32_t device, int32_t first_chunk,
                                             int32_t num_chunks,
                                             uint64_t* hashes);
+
+/* The decoders' log-softmax normaliser over n rows of V fp32 logits:
+ * lse[r] = double(max) + log(sum_k exp(double(l_k) - max)), the reference's
+ * detail::log_softmax_row (model.hpp:115-125) bit for bit. */
+rnntg_status rnntg_debug_log_softmax_lse(int32_t device, const float* logits,
+                                         int32_t n, int32_t V, double* lse);
+/* The device ports of glibc's exp (op 0), log (1), log1p (2) and the
+ * decoders' branch-light exp (3) over x[0..n). */
+rnntg_status rnntg_debug_f64_math(int32_t device, int32_t op, const double* x,
+                                  int64_t n, double* y);
 
 #ifdef __cplusplus
 }

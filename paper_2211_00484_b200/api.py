@@ -125,11 +125,14 @@ def _load():
     lib.rnntg_fsa_beam_search.argtypes = [vp, f32p, i32p, i32, vp, C.POINTER(_FsaParams), i32, i32p, vp, f64p]
     lib.rnntg_fsa_lattice.argtypes = [vp, i32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), i32, vp, vp, vp, vp]
     lib.rnntg_fsa_lattice.restype = C.c_int
+    lib.rnntg_fsa_lattice_text.argtypes = [vp, i32, i32, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
     lib.rnntg_model_set_encoder.argtypes = [vp, C.POINTER(_EncDesc)]
     lib.rnntg_encoder_forward.argtypes = [vp, f32p, i32p, i32, i32, vp]
     lib.rnntg_debug_decoder_projection.argtypes = [vp, i32p, i32, f32p]
     lib.rnntg_debug_joiner_logits.argtypes = [vp, f32p, i32p, i32, f32p]
     lib.rnntg_debug_tanhf_chunk_hashes.argtypes = [i32, i32, i32, C.POINTER(C.c_uint64)]
+    lib.rnntg_debug_log_softmax_lse.argtypes = [i32, f32p, i32, i32, vp]
+    lib.rnntg_debug_f64_math.argtypes = [i32, i32, vp, C.c_int64, vp]
     lib.rnntg_init_model_weights.argtypes = [vp, vp]
     lib.rnntg_gaussian_features.argtypes = [C.c_uint64, i32, i32, i32, i32, vp]
     for f in (
@@ -143,11 +146,14 @@ def _load():
         "rnntg_graph_create",
         "rnntg_graph_destroy",
         "rnntg_fsa_beam_search",
+        "rnntg_fsa_lattice_text",
         "rnntg_model_set_encoder",
         "rnntg_encoder_forward",
         "rnntg_debug_decoder_projection",
         "rnntg_debug_joiner_logits",
         "rnntg_debug_tanhf_chunk_hashes",
+        "rnntg_debug_log_softmax_lse",
+        "rnntg_debug_f64_math",
         "rnntg_init_model_weights",
         "rnntg_gaussian_features",
     ):
@@ -457,6 +463,15 @@ class Decoder:
         )
         return dict(num_nodes=nn.value, src=src[:n], dst=dst[:n], label=lab[:n], score=sc[:n])
 
+    def fsa_lattice_text(self, stream: int, header: bool = False) -> str:
+        """serialize_fsa_text (or, with header, serialize_lattice) of
+        `stream`'s lattice from the last fsa_beam_search."""
+        n = C.c_int64()
+        _check(self._lib.rnntg_fsa_lattice_text(self.h, stream, int(header), None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        _check(self._lib.rnntg_fsa_lattice_text(self.h, stream, int(header), buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
     # ---- kernel-level parity ----
     def decoder_projection(self, ctxs):
         ctxs = np.ascontiguousarray(ctxs, np.int32)
@@ -526,3 +541,23 @@ def exported_symbols():
 
     hdr = open(os.path.join(_HERE, "..", "include", "rnntg.h")).read()
     return sorted(set(re.findall(r"\b(rnntg_[a-z_0-9]+)\s*\(", hdr)))
+
+
+def log_softmax_lse(logits, device=0):
+    """Device log-softmax normalisers of fp32 rows [n][V] (model.hpp:115-125)."""
+    x = np.ascontiguousarray(logits, np.float32)
+    n, V = x.shape
+    out = np.zeros(max(1, n), np.float64)
+    _check(_load().rnntg_debug_log_softmax_lse(device, _ptr(x), n, V, _ptr(out)))
+    return out[:n]
+
+
+F64_OPS = {"exp": 0, "log": 1, "log1p": 2, "exp_g": 3}
+
+
+def f64_math(op, x, device=0):
+    """Device glibc exp / log / log1p ports (glibc_f64.h) over x."""
+    a = np.ascontiguousarray(x, np.float64)
+    y = np.zeros(max(1, a.size), np.float64)
+    _check(_load().rnntg_debug_f64_math(device, F64_OPS[op], _ptr(a), a.size, _ptr(y)))
+    return y[: a.size]

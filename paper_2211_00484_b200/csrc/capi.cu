@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <charconv>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -343,6 +344,29 @@ rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
   return RNNTG_OK;
 }
 
+}  // namespace
+
+namespace {
+// Host in, host out through temporary device buffers (debug entry points).
+template <typename In, typename Out, typename F>
+rnntg_status debug_roundtrip(int32_t device, const In* in, size_t n_in, Out* out, size_t n_out, F launch) {
+  RNNTG_CUDA_TRY(cudaSetDevice(device));
+  In* di = nullptr;
+  Out* dout = nullptr;
+  cudaError_t e = cudaMalloc(&di, sizeof(In) * std::max<size_t>(1, n_in));
+  if (e == cudaSuccess) e = cudaMalloc(&dout, sizeof(Out) * std::max<size_t>(1, n_out));
+  if (e == cudaSuccess) e = cudaMemcpy(di, in, sizeof(In) * n_in, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch(di, dout);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(out, dout, sizeof(Out) * n_out, cudaMemcpyDeviceToHost);
+  cudaFree(di);
+  cudaFree(dout);
+  if (e != cudaSuccess) {
+    set_error(cudaGetErrorString(e));
+    return RNNTG_CUDA_ERROR;
+  }
+  return RNNTG_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -958,6 +982,56 @@ rnntg_status rnntg_fsa_lattice(rnntg_model_t h, int32_t s, int32_t* num_nodes, i
   return RNNTG_OK;
 }
 
+rnntg_status rnntg_fsa_lattice_text(rnntg_model_t h, int32_t s, int32_t with_header, char* buf,
+                                    int64_t capacity, int64_t* length) {
+  if (!h || !length) return invalid("null argument");
+  int32_t nn = 0, na = 0;
+  rnntg_status st = rnntg_fsa_lattice(h, s, &nn, &na, 0, nullptr, nullptr, nullptr, nullptr);
+  if (st) return st;
+  std::vector<int32_t> src(std::max(1, na)), dst(std::max(1, na)), lab(std::max(1, na));
+  std::vector<double> sc(std::max(1, na));
+  if ((st = rnntg_fsa_lattice(h, s, &nn, &na, na, src.data(), dst.data(), lab.data(), sc.data()))) return st;
+  // serialize_lattice (fsa_search.hpp:429-435) over serialize_fsa_text
+  // (fsa.hpp:243-262): "src dst label score" per arc, then "state score" per
+  // final, scores in the shortest round-trip form of std::to_chars
+  // (detail::format_score, fsa.hpp:127-131).
+  std::string out;
+  out.reserve(static_cast<size_t>(na) * 32 + 64);
+  auto score = [&out](double v) {
+    char b[64];
+    const auto r = std::to_chars(b, b + sizeof(b), v);
+    out.append(b, r.ptr);
+  };
+  if (with_header) {
+    int32_t T = 0;
+    {
+      std::lock_guard<std::mutex> lk(h->mu);
+      T = h->last_fsa_fs[s + 1] - h->last_fsa_fs[s];
+    }
+    out += "# stream=" + std::to_string(s) + " frames=" + std::to_string(T) + "\n";
+  }
+  for (int32_t i = 0; i < na; ++i) {
+    out += std::to_string(src[i]);
+    out += ' ';
+    out += std::to_string(dst[i]);
+    out += ' ';
+    out += std::to_string(lab[i]);
+    out += ' ';
+    score(sc[i]);
+    out += '\n';
+  }
+  out += std::to_string(nn - 1);  // the super-final node, final score 0
+  out += ' ';
+  score(0.0);
+  out += '\n';
+  *length = static_cast<int64_t>(out.size());
+  if (capacity == 0) return RNNTG_OK;
+  if (!buf || capacity < *length + 1) return invalid("lattice text capacity too small");
+  std::memcpy(buf, out.data(), out.size());
+  buf[out.size()] = '\0';
+  return RNNTG_OK;
+}
+
 rnntg_status rnntg_model_set_encoder(rnntg_model_t h, const rnntg_encoder_desc* e) {
   if (!h || !e) return invalid("null argument");
   if (e->feat_dim < 1) return invalid("model dims must be >= 1");
@@ -1071,6 +1145,25 @@ rnntg_status rnntg_debug_tanhf_chunk_hashes(int32_t device, int32_t first_chunk,
     return RNNTG_CUDA_ERROR;
   }
   return RNNTG_OK;
+}
+
+
+rnntg_status rnntg_debug_log_softmax_lse(int32_t device, const float* logits, int32_t n, int32_t V,
+                                         double* lse) {
+  if (n < 0 || V < 1 || V > rnntg::kMaxVocab || (n > 0 && (!logits || !lse)))
+    return invalid("bad log-softmax arguments");
+  if (n == 0) return RNNTG_OK;
+  return debug_roundtrip(device, logits, static_cast<size_t>(n) * V, lse, static_cast<size_t>(n),
+                         [&](const float* di, double* dout) {
+                           return rnntg::launch_log_softmax_rows(di, n, V, dout, nullptr);
+                         });
+}
+
+rnntg_status rnntg_debug_f64_math(int32_t device, int32_t op, const double* x, int64_t n, double* y) {
+  if (op < 0 || op > 3 || n < 0 || (n > 0 && (!x || !y))) return invalid("bad f64 math arguments");
+  if (n == 0) return RNNTG_OK;
+  return debug_roundtrip(device, x, static_cast<size_t>(n), y, static_cast<size_t>(n),
+                         [&](const double* di, double* dout) { return rnntg::launch_f64_math(op, di, n, dout, nullptr); });
 }
 
 }  // extern "C"

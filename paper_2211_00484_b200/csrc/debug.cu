@@ -1,6 +1,8 @@
 // Kernel-level parity entry points: an independent straight-line joiner row
 // kernel and the exhaustive tanhf sweep.  Not on the decode hot path.
+#include "decode_common.cuh"
 #include "exact_math.h"
+#include "glibc_f64.h"
 #include "internal.cuh"
 
 namespace rnntg {
@@ -64,7 +66,48 @@ __global__ void tanhf_hash_kernel(uint32_t first_chunk,
   if ((threadIdx.x & 31) == 0) atomicAdd(&hashes[blockIdx.y], acc);
 }
 
+// One warp per row: the decoders' exact log-softmax normaliser (row_lse:
+// index-order sum with glibc exp / log).
+__global__ void log_softmax_rows_kernel(const float* __restrict__ logits, int32_t n, int32_t V,
+                                        double* __restrict__ lse) {
+  __shared__ uint64_t etab[256];
+  __shared__ __align__(16) double scr[4 * dec::kLseScr];
+  dec::load_exp_table(etab);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  for (int r = blockIdx.x * 4 + warp; r < n; r += gridDim.x * 4) {
+    const double v = dec::row_lse(logits + static_cast<int64_t>(r) * V, V, scr + warp * dec::kLseScr, etab);
+    if ((threadIdx.x & 31) == 0) lse[r] = v;
+  }
+}
+
+// glibc exp / log / log1p ports over x[i] (op 0 / 1 / 2; op 3: exp_g, the
+// decoders' branch-light exp).
+__global__ void f64_math_kernel(int32_t op, const double* __restrict__ x, int64_t n, double* __restrict__ y) {
+  __shared__ uint64_t etab[256];
+  dec::load_exp_table(etab);
+  __syncthreads();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = x[i];
+    y[i] = op == 0 ? rnntg_f64::exp(v) : op == 1 ? rnntg_f64::log(v) : op == 2 ? rnntg_f64::log1p(v)
+                                                                                 : dec::exp_g(v, etab);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_log_softmax_rows(const float* logits, int32_t n, int32_t V, double* lse, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  log_softmax_rows_kernel<<<(n + 3) / 4, 128, 0, s>>>(logits, n, V, lse);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_f64_math(int32_t op, const double* x, int64_t n, double* y, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  f64_math_kernel<<<296, 256, 0, s>>>(op, x, n, y);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_joiner_rows_exact(const DeviceModel& m, const float* pe,
                                      const int32_t* ctxs, int32_t n,

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
                   unsigned long long* __restrict__ counters) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* HL = reinterpret_cast<float*>(smem_raw);
-  const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
+  const int hl_floats = hl_floats_of(m.J, m.Vp);
   float* W0 = HL + hl_floats;
   float* W1 = W0 + kBK * m.Vp;
   GreedySmem& S = *reinterpret_cast<GreedySmem*>(W1 + kBK * m.Vp);
@@ -224,6 +224,7 @@ struct BeamCand {  // stage-1 extension or stage-2 merged entry
 };
 
 struct BeamSmem {
+  uint64_t etab[256];  // glibc exp table (lse_exact)
   unsigned long long stat[16];  // per-CTA counters (layout of DecodeArgs::counters)
   WPipe pipe;
   uint64_t bar[2];
@@ -353,77 +354,13 @@ __device__ __forceinline__ int beam_rows(Hyps* H, int n, const int32_t* fsp, int
   return __shfl_sync(0xffffffffu, incl, 31);
 }
 
-// D. one logits row (one warp): lse, blank logit, top-`beam` tokens k >= 1
-// by (logit desc, token asc).  Each lane keeps a sorted local top-BCAP,
-// then `beam` warp-wide pops.
-template <int BCAP>
-__device__ __forceinline__ void beam_row_reduce(const float* L, int V, int beam, int r, RowRes rr) {
-  const int lane = threadIdx.x & 31;
-  const double lse = row_lse(L, V);
-  float tl[BCAP];
-  int tk[BCAP];
-#pragma unroll
-  for (int q = 0; q < BCAP; ++q) {
-    tl[q] = -FLT_MAX;
-    tk[q] = 0x7fffffff;
-  }
-  for (int k = (lane == 0 ? 32 : lane); k < V; k += 32) {
-    float cv = L[k];
-    int ck = k;
-    if (!tok_before(cv, ck, tl[BCAP - 1], tk[BCAP - 1])) continue;
-#pragma unroll
-    for (int q = 0; q < BCAP; ++q) {
-      if (tok_before(cv, ck, tl[q], tk[q])) {
-        const float tv = tl[q];
-        const int tkk = tk[q];
-        tl[q] = cv;
-        tk[q] = ck;
-        cv = tv;
-        ck = tkk;
-      }
-    }
-  }
-  for (int q = 0; q < beam; ++q) {
-    float bv = tl[0];
-    int bk = tk[0], bl = lane;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
-      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (tok_before(ov, ok, bv, bk)) {
-        bv = ov;
-        bk = ok;
-        bl = ol;
-      }
-    }
-    if (lane == 0) {
-      rr.tl[r][q] = bv;
-      rr.tk[r][q] = bk;
-    }
-    if (lane == bl) {
-#pragma unroll
-      for (int z = 0; z < BCAP - 1; ++z) {
-        tl[z] = tl[z + 1];
-        tk[z] = tk[z + 1];
-      }
-      tl[BCAP - 1] = -FLT_MAX;
-      tk[BCAP - 1] = 0x7fffffff;
-    }
-  }
-  if (lane == 0) {
-    rr.lse[r] = lse;
-    rr.l0[r] = L[0];
-  }
-}
-
 // D for NR rows per warp (rows r0 + 16 j), their dependency chains
 // interleaved.  Per row: each lane keeps a sorted top-BCAP of its columns
 // k >= 1 (k = lane + 32 i) as 64-bit keys (ordered logit << 32 | ~k: key
 // order is (logit desc, token asc)) by branch-free compare-exchange; `beam`
 // pops take the warp maximum with two redux.sync each; the row max M is the
-// larger of the first pop and the blank logit; then lse = M + log(sum of
-// exp(double(l) - M)) in row_lse's order.  Same results as beam_row_reduce.
+// larger of the first pop and the blank logit; then the exact lse
+// (lse_exact: the reference's index-order sum with glibc exp / log).
 __device__ __forceinline__ uint64_t tok_key(float v, int k) {
   return (static_cast<uint64_t>(ord_key(v + 0.0f)) << 32) | static_cast<uint32_t>(~k);  // -0 -> +0
 }
@@ -432,10 +369,6 @@ __device__ __forceinline__ uint64_t tok_key(float v, int k) {
 #define RNNTG_TOPK_UNROLL 2  // 0: compiler's choice
 #endif
 constexpr int kTopkUnroll = RNNTG_TOPK_UNROLL > 0 ? RNNTG_TOPK_UNROLL : 1;
-#ifndef RNNTG_LSE_UNROLL
-#define RNNTG_LSE_UNROLL 2
-#endif
-constexpr int kLseUnroll = RNNTG_LSE_UNROLL;  // exp-sum loop trips unrolled (row reduction)
 #ifndef RNNTG_MAIN_STEP_NI
 #define RNNTG_MAIN_STEP_NI 0
 #endif
@@ -449,8 +382,8 @@ constexpr int kLseUnroll = RNNTG_LSE_UNROLL;  // exp-sum loop trips unrolled (ro
 #define RNNTG_SL_RR_NI 1
 #endif
 template <int BCAP, int NR>
-__device__ __forceinline__ void beam_row_reduce_n(const float* HL, int Vp, int V, int beam, int r0,
-                                                  int R, RowRes rr, int rs = 16) {
+__device__ __forceinline__ void beam_row_reduce_n(float* HL, int Vp, int V, int beam, int r0,
+                                                  int R, RowRes rr, const uint64_t* etab, int rs = 16) {
   const int lane = threadIdx.x & 31;
   uint64_t t[NR][BCAP];
   const float* L[NR];
@@ -500,18 +433,12 @@ __device__ __forceinline__ void beam_row_reduce_n(const float* HL, int Vp, int V
       }
     }
   }
-  double s[NR];
-#pragma unroll
-  for (int j = 0; j < NR; ++j) s[j] = 0.0;
-#pragma unroll kLseUnroll
-  for (int k = lane; k < V; k += 32)
-#pragma unroll
-    for (int j = 0; j < NR; ++j) s[j] += exp_lse(static_cast<double>(L[j][k]) - static_cast<double>(M[j]));
+  double lse[NR];
+  lse_exact<NR>(L, M, V, lse_scratch(HL, Vp), etab, lse);
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
-    s[j] = warp_sum_d(s[j]);
     if (lane == 0 && live[j]) {
-      rr.lse[r0 + rs * j] = static_cast<double>(M[j]) + log(s[j]);
+      rr.lse[r0 + rs * j] = lse[j];
       rr.l0[r0 + rs * j] = L[j][0];
     }
   }
@@ -520,9 +447,9 @@ __device__ __forceinline__ void beam_row_reduce_n(const float* HL, int Vp, int V
 // Out-of-line copy for the time-sliced kernel instantiation (measured faster
 // there than inlined; the single-launch kernel inlines it).
 template <int BCAP, int NR>
-__device__ __noinline__ void beam_row_reduce_ni(const float* HL, int Vp, int V, int beam, int r0, int R,
-                                                RowRes rr) {
-  beam_row_reduce_n<BCAP, NR>(HL, Vp, V, beam, r0, R, rr);
+__device__ __noinline__ void beam_row_reduce_ni(float* HL, int Vp, int V, int beam, int r0, int R,
+                                                RowRes rr, const uint64_t* etab) {
+  beam_row_reduce_n<BCAP, NR>(HL, Vp, V, beam, r0, R, rr, etab);
 }
 
 // E. one stream's frame (one warp).  Reference order (search.hpp:223-259 at
@@ -630,14 +557,8 @@ __device__ void beam_stream_step(const ModelView& m, Hyps& h, BeamCand* cand, ui
     if (lane < nsel) {
       if (hit >= 0) {
         double& sc = merged[hit].score;
-        if (merge_log) {  // log_add, common.hpp:48-54
-          const double a = sc, b = e.score;
-          if (a == -INFINITY) {
-            sc = b;
-          } else if (b != -INFINITY) {
-            const double hi = a > b ? a : b, lo = a > b ? b : a;
-            sc = hi + log1p(exp(lo - hi));
-          }
+        if (merge_log) {  // log_add, common.hpp:48-54 (glibc exp / log1p bits)
+          sc = rnntg_f64::log_add(sc, e.score);
         } else {
           sc = sc > e.score ? sc : e.score;
         }
@@ -735,7 +656,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
                 unsigned long long* __restrict__ counters, DbgKnobs fp, BeamSlice sl) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* HL = reinterpret_cast<float*>(smem_raw);
-  const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
+  const int hl_floats = hl_floats_of(m.J, m.Vp);
   // weight stages: two kBK-row fp32 chunks, or (bf16 variant) kTcStages
   // 16 KB bf16 chunks = the area of two 16-row fp32 chunks
   const int wst = TC ? 16 * m.Vp : kBK * m.Vp;
@@ -783,6 +704,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     }
   }
   if (threadIdx.x < 16) S.stat[threadIdx.x] = 0;
+  load_exp_table(S.etab);
   if (threadIdx.x == 0) {
     if constexpr (TC) {
       for (int i = 0; i < kTcStages; ++i) {
@@ -864,15 +786,15 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     const RowRes rr{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
     if constexpr ((SL && RNNTG_SL_RR_NI) || (!SL && RNNTG_MAIN_RR_NI)) {
       if (R <= kWarps) {
-        if (warp < R) beam_row_reduce_ni<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr);
+        if (warp < R) beam_row_reduce_ni<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr, S.etab);
       } else if (warp < R - kWarps || warp < kWarps) {
-        beam_row_reduce_ni<BCAP, 2>(HL, m.Vp, m.V, beam, warp, R, rr);
+        beam_row_reduce_ni<BCAP, 2>(HL, m.Vp, m.V, beam, warp, R, rr, S.etab);
       }
     } else {
       if (R <= kWarps) {
-        if (warp < R) beam_row_reduce_n<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr);
+        if (warp < R) beam_row_reduce_n<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr, S.etab);
       } else if (warp < R - kWarps || warp < kWarps) {
-        beam_row_reduce_n<BCAP, 2>(HL, m.Vp, m.V, beam, warp, R, rr);
+        beam_row_reduce_n<BCAP, 2>(HL, m.Vp, m.V, beam, warp, R, rr, S.etab);
       }
     }
     __syncthreads();
@@ -973,6 +895,7 @@ struct MStream {
 };
 
 struct MultiSmem {
+  uint64_t etab[256];  // glibc exp table (lse_exact)
   unsigned long long stat[16];
   uint64_t bar[2];
   uint32_t wcur[2];
@@ -1012,14 +935,8 @@ __device__ __forceinline__ bool seq_before(double ka, int la, int na, int ta, do
 }
 
 __device__ __forceinline__ void nf_merge(NfEntry& e, double v, int merge_log) {
-  if (merge_log) {  // log_add, common.hpp:48-54
-    const double a = e.score, b = v;
-    if (a == -INFINITY) {
-      e.score = b;
-    } else if (b != -INFINITY) {
-      const double hi = a > b ? a : b, lo = a > b ? b : a;
-      e.score = hi + log1p(exp(lo - hi));
-    }
+  if (merge_log) {  // log_add, common.hpp:48-54 (glibc exp / log1p bits)
+    e.score = rnntg_f64::log_add(e.score, v);
   } else {
     e.score = e.score > v ? e.score : v;
   }
@@ -1070,7 +987,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
                       unsigned long long* __restrict__ counters) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* HL = reinterpret_cast<float*>(smem_raw);
-  const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
+  const int hl_floats = hl_floats_of(m.J, m.Vp);
   float* W0 = HL + hl_floats;
   float* W1 = W0 + kBKSmall * m.Vp;
   MultiSmem& S = *reinterpret_cast<MultiSmem*>(W1 + kBKSmall * m.Vp);
@@ -1100,6 +1017,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     pool[pb] = make_int2(0, 0);  // root
   }
   if (threadIdx.x < 16) S.stat[threadIdx.x] = 0;
+  load_exp_table(S.etab);
   if (threadIdx.x == 0) {
     mbar_init(&S.bar[0], 1);
     mbar_init(&S.bar[1], 1);
@@ -1140,9 +1058,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       joiner_gemm(m, pipe, g, HL, R);
       const RowRes rr{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
       if (R <= kWarps) {
-        if (warp < R) beam_row_reduce_n<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr);
+        if (warp < R) beam_row_reduce_n<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr, S.etab);
       } else if (warp < R - kWarps || warp < kWarps) {
-        beam_row_reduce_n<BCAP, 2>(HL, m.Vp, m.V, beam, warp, R, rr);
+        beam_row_reduce_n<BCAP, 2>(HL, m.Vp, m.V, beam, warp, R, rr, S.etab);
       }
       __syncthreads();
       for (int i = warp; i < ns; i += kWarps) {
@@ -1364,7 +1282,7 @@ cudaError_t launch_beam_cap3(const DecodeArgs& a, cudaStream_t s) {
     return e ? std::atoi(e) : 0;
   }();
   DbgKnobs fp{force_r};
-  const size_t hl = static_cast<size_t>(max(m.J * kHStride, kRowCap * m.Vp)) * 4;
+  const size_t hl = static_cast<size_t>(hl_floats_of(m.J, m.Vp)) * 4;
   size_t smem = hl + static_cast<size_t>(2) * (TC ? 16 : kBK) * m.Vp * 4 + sizeof(BeamSmem) + sizeof(Hyps) * G +
                 sizeof(BeamCand) * G * (BCAP * BCAP + 2 * BCAP);
   if (TC) smem += 1024 + static_cast<size_t>(kRowCap) * m.J * 2 + sizeof(TcBars);

@@ -7,6 +7,7 @@
 #include <math.h>
 
 #include "exact_math.h"
+#include "glibc_f64.h"
 #include "internal.cuh"
 #include "tc_common.cuh"
 
@@ -479,53 +480,104 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// exp(x) for the log-softmax sums, x = double(l) - double(max) <= 0: n =
-// rint(x / ln2), r = x - n ln2 (two-part ln2, |r| <= ln2/2), e^r by its
-// degree-13 Taylor polynomial in Horner form (truncation < 5e-18 relative),
-// times 2^n by an exponent add.  ~1-2 ulp, branch-free, ~22 instructions
-// against ~90 for the libdevice exp (whose range checks also split it into
-// basic blocks, so consecutive evaluations cannot interleave).  x < -700
-// gives 0 (e^-700 is far below an ulp of any sum it joins: the sum holds
-// e^0 = 1).
-__device__ __forceinline__ double exp_lse(double x) {
-  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round to nearest integer
-  const double t = __fma_rn(x, 1.4426950408889634, kMagic);
-  const double nd = t - kMagic;
-  const int n = __double2loint(t);
-  double r = __fma_rn(-nd, 6.93147180369123816490e-01, x);  // ln2 hi (n*hi exact for |n| < 2^20)
-  r = __fma_rn(-nd, 1.90821492927058770002e-10, r);          // ln2 lo
-  double p = 1.6059043836821614599e-10;                       // 1/13!
-  p = __fma_rn(p, r, 2.0876756987868098979e-09);              // 1/12!
-  p = __fma_rn(p, r, 2.5052108385441718775e-08);              // 1/11!
-  p = __fma_rn(p, r, 2.7557319223985890653e-07);              // 1/10!
-  p = __fma_rn(p, r, 2.7557319223985890653e-06);              // 1/9!
-  p = __fma_rn(p, r, 2.4801587301587301566e-05);              // 1/8!
-  p = __fma_rn(p, r, 1.9841269841269841253e-04);              // 1/7!
-  p = __fma_rn(p, r, 1.3888888888888889419e-03);              // 1/6!
-  p = __fma_rn(p, r, 8.3333333333333332177e-03);              // 1/5!
-  p = __fma_rn(p, r, 4.1666666666666664354e-02);              // 1/4!
-  p = __fma_rn(p, r, 1.6666666666666665741e-01);              // 1/3!
-  p = __fma_rn(p, r, 0.5);
-  p = __fma_rn(p, r, 1.0);
-  p = __fma_rn(p, r, 1.0);
-  const double y = __hiloint2double(__double2hiint(p) + (n << 20), __double2loint(p));
-  return x < -700.0 ? 0.0 : y;
+// Exact log-softmax normaliser (model.hpp:115-125): sum = Σ_k exp(double(l_k)
+// - max) in index order k = 0..V-1 starting from 0.0, lse = double(max) +
+// log(sum), with glibc's own exp / log (glibc_f64.h), so lse -- hence every
+// log-probability, score and lattice arc -- has the reference's bits.
+//
+// The exps are evaluated lane-parallel, 32 consecutive k at a time, and
+// staged in a per-warp scratch (kLseScr doubles); the sum is then the
+// reference's sequential chain, run by every lane on broadcast reads (two
+// doubles per LDS.128), so the result is warp-uniform.  NR rows share each
+// chunk so their chains interleave.  `etab` is a shared-memory copy of
+// glibc's exp table (a divergent index into constant memory serialises).
+constexpr int kLseScr = 64;  // doubles of scratch per warp (2 rows x 32)
+
+__host__ __device__ inline int hl_floats_of(int J, int Vp) {
+  const int a = J * kHStride, b = kRowCap * Vp + kWarps * kLseScr * 2;
+  return a > b ? a : b;
+}
+// The scratch sits behind the logits tile inside the h/logits buffer (the
+// k-major h tile is dead once the joiner GEMM has written the logits).
+__device__ __forceinline__ double* lse_scratch(float* HL, int Vp) {
+  return reinterpret_cast<double*>(HL + kRowCap * Vp) + (threadIdx.x >> 5) * kLseScr;
+}
+__device__ __forceinline__ void load_exp_table(uint64_t* etab) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) etab[i] = rnntg_f64::kExpTab[i];
 }
 
-// Log-softmax normaliser of one logits row (model.hpp:115-125): float max,
-// double sum of exp(double(l) - max), lse = max + log(sum).  The sum is a
-// warp tree instead of the reference's index-order loop; the two differ by a
-// few fp64 ulps (documented in DESIGN.md; scores are checked to 1e-9 rel).
-__device__ __forceinline__ double row_lse(const float* L, int V) {
+// exp for arguments in [-2^9, 2^9) evaluated branch-free (glibc's main
+// path); anything else (|x| < 2^-54: 1 + x; |x| >= 512) takes glibc's own
+// special-case code.
+__device__ __forceinline__ double exp_g(double x, const uint64_t* __restrict__ etab) {
+  using namespace rnntg_f64;
+  const uint32_t abstop = static_cast<uint32_t>(d2u(x) >> 52) & 0x7ffu;
+  const double kd0 = xfma(x, 0x1.71547652b82fep+7, 0x1.8p52);
+  const uint64_t ki = d2u(kd0);
+  const double kd = xsub(kd0, 0x1.8p52);
+  double r = xfma(kd, -0x1.62e42fefa0000p-8, x);
+  r = xfma(kd, -0x1.cf79abc9e3b3ap-47, r);
+  const uint32_t idx = 2u * static_cast<uint32_t>(ki & 0x7f);
+  const double tail = u2d(etab[idx]);
+  const double scale = u2d(etab[idx + 1] + (ki << 45));
+  const double p23 = xfma(r, 0x1.555555555543cp-3, 0x1.ffffffffffdbdp-2);
+  const double tr = xadd(r, tail);
+  const double r2 = xmul(r, r);
+  const double p45 = xfma(r, 0x1.1111167a4d017p-7, 0x1.55555cf172b91p-5);
+  const double t1 = xfma(p23, r2, tr);
+  const double tmp = xfma(xmul(r2, r2), p45, t1);
+  double y = xfma(scale, tmp, scale);
+  if (abstop - 0x3c9u > 0x3eu) y = static_cast<int32_t>(abstop - 0x3c9u) < 0 ? xadd(x, 1.0) : exp_t(x, etab);
+  return y;
+}
+
+template <int NR>
+__device__ __forceinline__ void lse_exact(const float* const* L, const float* M, int V,
+                                          double* __restrict__ scr, const uint64_t* __restrict__ etab,
+                                          double* lse) {
+  const int lane = threadIdx.x & 31;
+  double acc[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) acc[j] = 0.0;
+  for (int c = 0; c < V; c += 32) {
+    const int k = c + lane;
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+      scr[j * 32 + lane] =
+          k < V ? exp_g(rnntg_f64::xsub(static_cast<double>(L[j][k]), static_cast<double>(M[j])), etab) : 0.0;
+    __syncwarp();
+    // + 0.0 past the end of the row is exact (acc > 0 by then).
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const double2 p = reinterpret_cast<const double2*>(scr + j * 32)[q];
+        acc[j] = rnntg_f64::xadd(rnntg_f64::xadd(acc[j], p.x), p.y);
+      }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int j = 0; j < NR; ++j) lse[j] = rnntg_f64::xadd(static_cast<double>(M[j]), rnntg_f64::log(acc[j]));
+}
+
+// One row (one warp): float max, then lse_exact.
+__device__ __forceinline__ double row_lse(const float* L, int V, double* scr, const uint64_t* etab) {
   const int lane = threadIdx.x & 31;
   float mx = -FLT_MAX;
   for (int k = lane; k < V; k += 32) mx = fmaxf(mx, L[k]);
-  mx = warp_max_f(mx);
-  double s = 0.0;
-#pragma unroll 4
-  for (int k = lane; k < V; k += 32) s += exp_lse(static_cast<double>(L[k]) - static_cast<double>(mx));
-  s = warp_sum_d(s);
-  return static_cast<double>(mx) + log(s);
+  const float Ms[1] = {warp_max_f(mx)};
+  const float* const Ls[1] = {L};
+  double lse[1];
+  lse_exact<1>(Ls, Ms, V, scr, etab, lse);
+  return lse[0];
+}
+
+// log_add (common.hpp:48-54) with glibc's exp / log1p.
+__device__ __forceinline__ double log_add_g(double a, double b, const uint64_t* etab) {
+  if (a == -INFINITY) return b;
+  if (b == -INFINITY) return a;
+  const double mx = a > b ? a : b, mn = a > b ? b : a;
+  return rnntg_f64::xadd(mx, rnntg_f64::log1p(rnntg_f64::exp_t(rnntg_f64::xsub(mn, mx), etab)));
 }
 
 // (logit desc, token asc): the order of a hypothesis' extensions, whose
@@ -648,7 +700,7 @@ __device__ __forceinline__ void tc_gemm(const ModelView& m, const TcPipe& p, uin
 }
 
 inline size_t smem_common(const ModelView& m, int bk = kBK) {
-  const size_t hl = static_cast<size_t>(max(m.J * kHStride, kRowCap * m.Vp)) * 4;
+  const size_t hl = static_cast<size_t>(hl_floats_of(m.J, m.Vp)) * 4;
   return hl + static_cast<size_t>(2) * bk * m.Vp * 4;
 }
 

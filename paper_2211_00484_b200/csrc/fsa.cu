@@ -77,6 +77,7 @@ struct FsaStream {
 };
 
 struct FsaSmem {
+  uint64_t etab[256];            // glibc exp table (lse_exact)
   WPipe pipe;                    // in smem: no registers pinned across the frame loop
   unsigned long long rows_total;
   long long ph[3];               // thread 0: h build, joiner GEMM, lse + expand/prune
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
                unsigned long long* __restrict__ counters, int32_t* __restrict__ error_flag) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* HL = reinterpret_cast<float*>(smem_raw);
-  const int hl_floats = max(m.J * kHStride, kRowCap * m.Vp);
+  const int hl_floats = hl_floats_of(m.J, m.Vp);
   float* W0 = HL + hl_floats;
   float* W1 = W0 + bk * m.Vp;
   FsaSmem& C = *reinterpret_cast<FsaSmem*>(W1 + bk * m.Vp);
@@ -301,6 +302,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     fence_mbar_init();
   }
   if (have && grp.tid == 0) S.raw_total = S.lat_total = 0;
+  load_exp_table(C.etab);
   __syncthreads();
   if (threadIdx.x == 0) {
     wpipe_issue(pipe, m, 0);
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       for (int r = warp; r < R; r += kDecodeThreads / 32) {
         const float* L = HL + static_cast<int64_t>(r) * m.Vp;
-        const double lse = row_lse(L, m.V);
+        const double lse = row_lse(L, m.V, lse_scratch(HL, m.Vp), C.etab);
         float mx = -FLT_MAX;
         for (int k = lane; k < m.V; k += 32) mx = fmaxf(mx, L[k]);
         mx = warp_max_f(mx);

@@ -149,6 +149,8 @@ cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s);
 int decode_num_sms(int device);
 int decode_num_sms_current();
 
+cudaError_t launch_log_softmax_rows(const float* logits, int32_t n, int32_t V, double* lse, cudaStream_t s);
+cudaError_t launch_f64_math(int32_t op, const double* x, int64_t n, double* y, cudaStream_t s);
 cudaError_t launch_tanhf_hash(int32_t first_chunk, int32_t num_chunks,
                               unsigned long long* d_hashes, cudaStream_t s);
 cudaError_t launch_joiner_rows_exact(const DeviceModel& m, const float* pe,

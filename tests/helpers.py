@@ -62,3 +62,21 @@ def decoder_env(m, **env):
                 del os.environ[k]
             else:
                 os.environ[k] = v
+
+
+def assert_scores_equal(got, want):
+    """fp64 scores bit-equal to the reference's (exact log-softmax: the
+    reference's index-order sum with glibc exp / log, glibc_f64.h)."""
+    g = np.asarray(got, np.float64)
+    w = np.asarray(want, np.float64)
+    assert g.shape == w.shape, (g.shape, w.shape)
+    bad = np.flatnonzero(g.view(np.int64) != w.view(np.int64))
+    assert bad.size == 0, f"{bad.size} scores differ, first {bad[:4].tolist()}: {g[bad[:4]]} vs {w[bad[:4]]}"
+
+
+def ref_logits(m, n, seed=0):
+    """n real joiner rows of the reference (encoder frames x random contexts)."""
+    _, enc, _ = frames(m, [n], seed0=seed)
+    V = m.w.V
+    ctx = np.random.default_rng(seed).integers(0, V * V, n).astype(np.int32)
+    return m.joiner_logits(enc, ctx)

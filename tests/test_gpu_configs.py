@@ -12,10 +12,11 @@ through the reference encoder).
             (host DetRng generator + GPU encoder, exactly bench.py's), a
             stratified 64-stream sample compared against the reference
 
-Bars: tokens identical on every stream; beam scores within 1e-9 relative of
-the oracle restatement (the reference's beam_search returns tokens only);
-FSA best-path scores within 1e-9 relative of the reference's.  Exact-score
-ties resolved by the tie rules are counted by the device and reported.
+Bars: tokens identical on every stream; beam scores bit-equal to the oracle
+restatement's (the reference's beam_search returns tokens only); FSA
+best-path scores bit-equal to the reference's and every stream's lattice
+text (serialize_fsa_text) byte-identical.  Exact-score ties resolved by
+the tie rules are counted by the device and reported.
 """
 import os
 
@@ -27,13 +28,19 @@ from tests import helpers as H
 pytestmark = pytest.mark.gpu
 
 THREADS = os.cpu_count() or 1
-RTOL = 1e-9
 
 
 def _assert_tokens(got, want, what):
     bad = [i for i, (a, b) in enumerate(zip(got, want)) if a != b]
     assert len(got) == len(want)
     assert not bad, f"{what}: {len(bad)} streams differ, first {bad[:8]}"
+
+
+def _assert_texts(got, want, what):
+    """serialize_fsa_text of every stream's lattice, byte for byte."""
+    bad = [i for i, (a, b) in enumerate(zip(got, want)) if a != b]
+    assert len(got) == len(want)
+    assert not bad, f"{what}: {len(bad)} lattice texts differ, first {bad[:8]}"
 
 
 def test_config2_beam_256x500():
@@ -50,7 +57,7 @@ def test_config2_beam_256x500():
     want = m.beam(feats, splits, beam=4, threads=THREADS)
     _assert_tokens(got, want, "config 2")
     _, osc = H.orc().beam(m.w, enc, splits, beam=4, threads=THREADS)
-    np.testing.assert_allclose(sc, osc, rtol=RTOL, atol=0)
+    H.assert_scores_equal(sc, osc)
     tpf = sum(map(len, want)) / splits[-1]
     assert 0.15 < tpf < 0.35, tpf  # the reference's emission rate (seed 0, blank bias 0.4)
     print(f"config 2: 256 streams identical, tokens/frame {tpf:.3f}, exact-score ties resolved {ties}")
@@ -65,11 +72,13 @@ def test_config3_fsa_trivial_512x500():
     dec = Decoder(H.api_weights(m.w))
     try:
         got, sc = dec.fsa_beam_search(enc, splits, Graph.trivial(dec), FsaParams(4.0, 8, 4))
+        texts = [dec.fsa_lattice_text(i) for i in range(512)]
     finally:
         dec.close()
-    want, wsc, _ = m.fsa(feats, splits, rg, 4.0, 8, 4, threads=THREADS)
+    want, wsc, wtexts = m.fsa(feats, splits, rg, 4.0, 8, 4, threads=THREADS, lattice_texts=True)
     _assert_tokens(got, want, "config 3")
-    np.testing.assert_allclose(sc, wsc, rtol=RTOL, atol=0)
+    H.assert_scores_equal(sc, wsc)
+    _assert_texts(texts, wtexts, "config 3")
 
 
 def test_config4_fsa_ngram_256x500():
@@ -85,11 +94,13 @@ def test_config4_fsa_ngram_256x500():
     try:
         dg = Graph(dec, g.num_states, g.arc_splits, g.dst, g.label, g.weight)
         got, sc = dec.fsa_beam_search(enc, splits, dg, FsaParams(8.0, 64, 8))
+        texts = [dec.fsa_lattice_text(i) for i in range(256)]
     finally:
         dec.close()
-    want, wsc, _ = m.fsa(feats, splits, rg, 8.0, 64, 8, threads=THREADS)
+    want, wsc, wtexts = m.fsa(feats, splits, rg, 8.0, 64, 8, threads=THREADS, lattice_texts=True)
     _assert_tokens(got, want, "config 4")
-    np.testing.assert_allclose(sc, wsc, rtol=RTOL, atol=0)
+    H.assert_scores_equal(sc, wsc)
+    _assert_texts(texts, wtexts, "config 4")
     tpf = sum(map(len, want)) / splits[-1]
     assert tpf > 0.03, tpf
 
@@ -134,6 +145,6 @@ def test_config5_beam_1024x1000_bench_inputs_sample():
     want = m.beam(f_pick, s_pick, beam=4, threads=THREADS)
     _assert_tokens(got, want, "config 5 sample")
     _, osc = H.orc().beam(m.w, ref_enc, s_pick, beam=4, threads=THREADS)
-    np.testing.assert_allclose(got_sc, osc, rtol=RTOL, atol=0)
+    H.assert_scores_equal(got_sc, osc)
     tpf = sum(map(len, want)) / s_pick[-1]
     assert 0.15 < tpf < 0.35, tpf

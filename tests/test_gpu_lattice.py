@@ -1,7 +1,8 @@
 """FSA lattices from the GPU vs the reference's fsa_beam_search lattices
-(SURVEY.md §8f row 2): identical node numbering, arc order, labels and
-destinations; arc scores to 1e-12 relative (the log-softmax normaliser is
-summed in a different fp64 order); byte-identical text for the structure."""
+(SURVEY.md §8f row 2): identical node numbering, arc order, labels,
+destinations and fp64 arc scores (bit-equal: the device log-softmax is the
+reference's own arithmetic), hence byte-identical serialize_fsa_text /
+serialize_lattice output (fsa.hpp:243-262, fsa_search.hpp:429-435)."""
 import numpy as np
 import pytest
 
@@ -27,7 +28,10 @@ def _compare(dec, m, feats, enc, splits, rg, params):
         mine = list(zip(lat["src"].tolist(), lat["dst"].tolist(), lat["label"].tolist()))
         assert mine == [a[:3] for a in arcs]
         want = np.array([a[3] for a in arcs])
-        np.testing.assert_allclose(lat["score"], want, rtol=1e-12, atol=1e-15)
+        H.assert_scores_equal(lat["score"], want)
+        assert dec.fsa_lattice_text(s) == text
+        T = int(splits[s + 1] - splits[s])
+        assert dec.fsa_lattice_text(s, header=True) == f"# stream={s} frames={T}\n" + text
 
 
 def test_trivial_graph_lattices_match_reference():

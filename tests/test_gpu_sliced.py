@@ -30,7 +30,7 @@ def test_sliced_host_frames_match_oracle_and_device_path(T, B, first, cap):
         if B <= 300:
             want, want_sc = H.orc().beam(m.w, enc, splits, beam=4)
             assert got == want
-            np.testing.assert_allclose(sc, want_sc, rtol=1e-9, atol=0)
+            H.assert_scores_equal(sc, want_sc)
         d_enc = torch.from_numpy(enc).cuda()
         tok = torch.zeros(max(1, int(splits[-1])), dtype=torch.int32, device="cuda")
         dsc = torch.zeros(B, dtype=torch.float64, device="cuda")
@@ -56,7 +56,7 @@ def test_sliced_repeated_calls_and_beam_sizes():
             want, want_sc = H.orc().beam(m.w, enc, splits, beam=beam)
             got, sc = dec.beam_search_batch(enc, splits, BeamParams(beam_size=beam))
             assert got == want, beam
-            np.testing.assert_allclose(sc, want_sc, rtol=1e-9, atol=0)
+            H.assert_scores_equal(sc, want_sc)
     finally:
         dec.close()
 
@@ -117,7 +117,7 @@ def test_sliced_bench_scale_matches_single_launch_and_oracle_sample():
         assert np.array_equal(sc, dsc.cpu().numpy())
         want, want_sc = H.orc().beam(m.w, enc[: U * T], splits[: U + 1], beam=4)
         assert [tok[osp[i] : osp[i + 1]].tolist() for i in range(U)] == want
-        np.testing.assert_allclose(sc[:U], want_sc, rtol=1e-9, atol=0)
+        H.assert_scores_equal(sc[:U], want_sc)
     finally:
         sliced.close()
         plain.close()
