@@ -225,6 +225,7 @@ struct BeamCand {  // stage-1 extension or stage-2 merged entry
 
 struct BeamSmem {
   uint64_t etab[256];  // glibc exp table (lse_exact)
+  float row_m[kRowCap];  // row maxima (beam_reduce_cta)
   unsigned long long stat[16];  // per-CTA counters (layout of DecodeArgs::counters)
   WPipe pipe;
   uint64_t bar[2];
@@ -381,7 +382,7 @@ constexpr int kTopkUnroll = RNNTG_TOPK_UNROLL > 0 ? RNNTG_TOPK_UNROLL : 1;
 #ifndef RNNTG_SL_RR_NI
 #define RNNTG_SL_RR_NI 1
 #endif
-template <int BCAP, int NR>
+template <int BCAP, int NR, bool LSE = true>
 __device__ __forceinline__ void beam_row_reduce_n(float* HL, int Vp, int V, int beam, int r0,
                                                   int R, RowRes rr, const uint64_t* etab, int rs = 16) {
   const int lane = threadIdx.x & 31;
@@ -433,15 +434,103 @@ __device__ __forceinline__ void beam_row_reduce_n(float* HL, int Vp, int V, int 
       }
     }
   }
-  double lse[NR];
-  lse_exact<NR>(L, M, V, lse_scratch(HL, Vp), etab, lse);
+  if constexpr (LSE) {
+    double lse[NR];
+    lse_exact<NR>(L, M, V, lse_scratch(HL, Vp), etab, lse);
 #pragma unroll
-  for (int j = 0; j < NR; ++j) {
-    if (lane == 0 && live[j]) {
-      rr.lse[r0 + rs * j] = lse[j];
-      rr.l0[r0 + rs * j] = L[j][0];
+    for (int j = 0; j < NR; ++j) {
+      if (lane == 0 && live[j]) {
+        rr.lse[r0 + rs * j] = lse[j];
+        rr.l0[r0 + rs * j] = L[j][0];
+      }
     }
   }
+}
+
+// D for the whole CTA with the weight stages as scratch (WPipe::defer):
+//  (a) row maxima (model.hpp:117-118), one warp per row;
+//  (b) every exp(double(l_k) - max) of every row into E (row stride S, odd
+//      so the chain lanes below hit distinct banks), one column per thread
+//      -- all of the exp work spread over the 512 threads;
+//  (c) warp 0 runs the reference's sequential sums (model.hpp:119-121), one
+//      lane per row, while warps 1-15 pick the top-`beam` tokens.
+// The index-order fp64 chain is ~V dependent DADDs per row; here it costs
+// one warp V instructions for all rows, overlapped with the top-k.
+template <int BCAP>
+__device__ __forceinline__ void beam_reduce_cta(float* HL, double* E, int ecap, int Vp, int V, int beam, int R,
+                                                RowRes rr, const uint64_t* etab, float* row_m) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < R; r += kWarps) {
+    const float* L = HL + static_cast<int64_t>(r) * Vp;
+    float mx = -FLT_MAX;
+    for (int k = lane; k < V; k += 32) mx = fmaxf(mx, L[k]);
+    mx = warp_max_f(mx);
+    if (lane == 0) row_m[r] = mx;
+  }
+  __syncthreads();
+  // Rows are zero-padded to V8 = V rounded up to 8 (+ 0.0 is exact once the
+  // sum holds exp(0) = 1), so the chain below runs in whole groups of 8.
+  constexpr int G8 = 8;
+  const int V8 = (V + G8 - 1) / G8 * G8;
+  int S = V8 + 1;
+  if (S * R > ecap) S = V8;
+  const int k = threadIdx.x;  // V8 <= kDecodeThreads
+  auto arg = [&](int r) {
+    return k < V ? rnntg_f64::xsub(static_cast<double>(HL[static_cast<int64_t>(r) * Vp + k]),
+                                   static_cast<double>(row_m[r]))
+                 : -1.0;
+  };
+  for (int r = 0; r < R; r += 2) {  // two rows per trip: independent exp chains interleave
+    const int r1 = r + 1 < R ? r + 1 : r;
+    const double x0 = arg(r), x1 = arg(r1);
+    double y0 = exp_main(x0, etab), y1 = exp_main(x1, etab);
+    if (__any_sync(0xffffffffu, exp_big(x0) || exp_big(x1))) {
+      if (exp_big(x0)) y0 = rnntg_f64::exp_t(x0, etab);
+      if (exp_big(x1)) y1 = rnntg_f64::exp_t(x1, etab);
+    }
+    if (k < V8) {
+      E[r * S + k] = k < V ? y0 : 0.0;
+      E[r1 * S + k] = k < V ? y1 : 0.0;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane < R) {
+      // Software-pipelined: group q + 1's loads are in flight while group
+      // q's 8 dependent DADDs run.
+      const double* e = E + lane * S;
+      double acc = 0.0, cur[G8], nxt[G8];
+#pragma unroll
+      for (int u = 0; u < G8; ++u) cur[u] = e[u];
+      for (int q = G8; q < V8; q += G8) {
+#pragma unroll
+        for (int u = 0; u < G8; ++u) nxt[u] = e[q + u];
+#pragma unroll
+        for (int u = 0; u < G8; ++u) acc = rnntg_f64::xadd(acc, cur[u]);
+#pragma unroll
+        for (int u = 0; u < G8; ++u) cur[u] = nxt[u];
+      }
+#pragma unroll
+      for (int u = 0; u < G8; ++u) acc = rnntg_f64::xadd(acc, cur[u]);
+      rr.lse[lane] = rnntg_f64::xadd(static_cast<double>(row_m[lane]), rnntg_f64::log(acc));
+      rr.l0[lane] = HL[static_cast<int64_t>(lane) * Vp];
+    }
+  } else {
+    constexpr int kTw = kWarps - 1;  // top-k warps
+    const int w = warp - 1;
+    if (R <= kTw) {
+      if (w < R) beam_row_reduce_n<BCAP, 1, false>(HL, Vp, V, beam, w, R, rr, etab);
+    } else {
+      beam_row_reduce_n<BCAP, 2, false>(HL, Vp, V, beam, w, R, rr, etab, kTw);
+      if (w + 2 * kTw < R) beam_row_reduce_n<BCAP, 1, false>(HL, Vp, V, beam, w + 2 * kTw, R, rr, etab);
+    }
+  }
+  __syncthreads();
+}
+template <int BCAP>
+__device__ __noinline__ void beam_reduce_cta_ni(float* HL, double* E, int ecap, int Vp, int V, int beam, int R,
+                                                RowRes rr, const uint64_t* etab, float* row_m) {
+  beam_reduce_cta<BCAP>(HL, E, ecap, Vp, V, beam, R, rr, etab, row_m);
 }
 
 // Out-of-line copy for the time-sliced kernel instantiation (measured faster
@@ -679,7 +768,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   // chunk is waited for or issued instead of pinning ~14 registers across
   // every phase (register pressure here costs the GEMM its LDS prefetch).
   const WPipe& pipe = S.pipe;
-  if (threadIdx.x == 0) S.pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
+  if (threadIdx.x == 0) {
+    S.pipe = make_wpipe(W0, W1, S.bar, S.wcur, m);
+    // exact fp32 joiner: the row reduction borrows both weight stages
+    S.pipe.defer = (!TC && S.pipe.nc >= 2 && m.Vp <= kDecodeThreads) ? 1 : 0;
+  }
   TcPipe tp{smem_u32(W0), tb->full, tb->empty, &tb->done, smem_u32(hb), 0u, m.J / kTcBK};
 
   int32_t tmax = 0;
@@ -784,7 +877,13 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     // token asc).  Each lane keeps a sorted local top-kMaxBeam, then `beam`
     // warp-wide pops.
     const RowRes rr{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
-    if constexpr ((SL && RNNTG_SL_RR_NI) || (!SL && RNNTG_MAIN_RR_NI)) {
+    if (!TC && pipe.defer) {
+      if constexpr ((SL && RNNTG_SL_RR_NI) || (!SL && RNNTG_MAIN_RR_NI))
+        beam_reduce_cta_ni<BCAP>(HL, reinterpret_cast<double*>(W0), wst, m.Vp, m.V, beam, R, rr, S.etab, S.row_m);
+      else
+        beam_reduce_cta<BCAP>(HL, reinterpret_cast<double*>(W0), wst, m.Vp, m.V, beam, R, rr, S.etab, S.row_m);
+      wpipe_issue_next(pipe, m, g);
+    } else if constexpr ((SL && RNNTG_SL_RR_NI) || (!SL && RNNTG_MAIN_RR_NI)) {
       if (R <= kWarps) {
         if (warp < R) beam_row_reduce_ni<BCAP, 1>(HL, m.Vp, m.V, beam, warp, R, rr, S.etab);
       } else if (warp < R - kWarps || warp < kWarps) {

@@ -108,11 +108,14 @@ struct WPipe {
   const float* a_ptr;  // nullptr: no A passes
   int32_t a_nc, a_K;
   int32_t period;      // B passes per A pass
+  int32_t defer;       // 1: the next frame's first two chunks are issued by
+                       // wpipe_issue_next after the row reduction (which then
+                       // uses both stages as scratch), not by the GEMM
 };
 
 __device__ __forceinline__ WPipe make_wpipe(float* W0, float* W1, uint64_t* bar, uint32_t* cur,
                                             const ModelView& m, int bk = kBK) {
-  return WPipe{{W0, W1}, bar, cur, bk, (m.J + bk - 1) / bk, m.out_wt, m.J, m.Vp, nullptr, 0, 0, 1};
+  return WPipe{{W0, W1}, bar, cur, bk, (m.J + bk - 1) / bk, m.out_wt, m.J, m.Vp, nullptr, 0, 0, 1, 0};
 }
 
 // Issues chunk g (thread 0; chunks are issued strictly in sequence, so the
@@ -142,6 +145,16 @@ __device__ __forceinline__ void wpipe_issue(const WPipe& p, const ModelView& /*m
   fence_proxy_async();
   mbar_expect_tx(bar, bytes);
   bulk_g2s(p.stage[g & 1u], src, bytes, bar);
+}
+
+// The two refills a deferring GEMM skipped (chunks g, g + 1: the next
+// frame's first two), once the stages are free again.  Call after a CTA
+// barrier that retired every generic-proxy access of the stages.
+__device__ __forceinline__ void wpipe_issue_next(const WPipe& p, const ModelView& m, uint32_t g) {
+  if (threadIdx.x == kDecodeThreads - 32) {
+    wpipe_issue(p, m, g);
+    wpipe_issue(p, m, g + 1);
+  }
 }
 
 // C. logits[r][n] = out_b[n] + sum_k out_w[n][k] * h[r][k], sequential in k.
@@ -207,7 +220,7 @@ __device__ __forceinline__ void gemm_pass(const ModelView& m, const WPipe& p,
       }
     }
     __syncthreads();  // every warp is done with this stage
-    if (threadIdx.x == 0) wpipe_issue(p, m, g + 2);
+    if (threadIdx.x == 0 && !(p.defer && c + 2 >= p.nc)) wpipe_issue(p, m, g + 2);
   }
   // The last __syncthreads above also retired every read of Hs, so the logits
   // may overwrite it.
@@ -328,7 +341,7 @@ __device__ __forceinline__ void gemm_pass_bal(const ModelView& m, const WPipe& p
     if (threadIdx.x == 0 && g_wait_cycles) g_wait_cycles[1] += clock64() - b0;
     // The refill is issued by the last warp: idle or light for every R, so
     // the issue latency never delays a heavy warp into the next barrier.
-    if (threadIdx.x == kDecodeThreads - 32) wpipe_issue(p, m, g + 2);
+    if (threadIdx.x == kDecodeThreads - 32 && !(p.defer && c + 2 >= p.nc)) wpipe_issue(p, m, g + 2);
   }
   // The last __syncthreads above also retired every read of the h tile.
   if (tn != 0) {
@@ -491,7 +504,10 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // doubles per LDS.128), so the result is warp-uniform.  NR rows share each
 // chunk so their chains interleave.  `etab` is a shared-memory copy of
 // glibc's exp table (a divergent index into constant memory serialises).
-constexpr int kLseScr = 64;  // doubles of scratch per warp (2 rows x 32)
+constexpr int kLseScr = 64;
+#ifndef RNNTG_LSE_GROUP
+#define RNNTG_LSE_GROUP 8  // double2 scratch loads in flight per group (lse_exact)
+#endif  // doubles of scratch per warp (2 rows x 32)
 
 __host__ __device__ inline int hl_floats_of(int J, int Vp) {
   const int a = J * kHStride, b = kRowCap * Vp + kWarps * kLseScr * 2;
@@ -506,10 +522,14 @@ __device__ __forceinline__ void load_exp_table(uint64_t* etab) {
   for (int i = threadIdx.x; i < 256; i += blockDim.x) etab[i] = rnntg_f64::kExpTab[i];
 }
 
-// exp for arguments in [-2^9, 2^9) evaluated branch-free (glibc's main
-// path); anything else (|x| < 2^-54: 1 + x; |x| >= 512) takes glibc's own
-// special-case code.
-__device__ __forceinline__ double exp_g(double x, const uint64_t* __restrict__ etab) {
+// glibc exp, straight-line: the main path for |x| in [2^-54, 2^9) and
+// 1 + x below (the max of every log-softmax row gives x = 0); valid unless
+// exp_big(x), where glibc's special-case code (exp_t) must be used.
+__device__ __forceinline__ bool exp_big(double x) {
+  const uint32_t abstop = static_cast<uint32_t>(__double_as_longlong(x) >> 52) & 0x7ffu;
+  return abstop > 0x407u;
+}
+__device__ __forceinline__ double exp_main(double x, const uint64_t* __restrict__ etab) {
   using namespace rnntg_f64;
   const uint32_t abstop = static_cast<uint32_t>(d2u(x) >> 52) & 0x7ffu;
   const double kd0 = xfma(x, 0x1.71547652b82fep+7, 0x1.8p52);
@@ -526,38 +546,76 @@ __device__ __forceinline__ double exp_g(double x, const uint64_t* __restrict__ e
   const double p45 = xfma(r, 0x1.1111167a4d017p-7, 0x1.55555cf172b91p-5);
   const double t1 = xfma(p23, r2, tr);
   const double tmp = xfma(xmul(r2, r2), p45, t1);
-  double y = xfma(scale, tmp, scale);
-  if (abstop - 0x3c9u > 0x3eu) y = static_cast<int32_t>(abstop - 0x3c9u) < 0 ? xadd(x, 1.0) : exp_t(x, etab);
-  return y;
+  const double y = xfma(scale, tmp, scale);
+  return abstop < 0x3c9u ? xadd(x, 1.0) : y;
+}
+// Any argument (per-thread branch for the rare |x| >= 512).
+__device__ __forceinline__ double exp_g(double x, const uint64_t* __restrict__ etab) {
+  return exp_big(x) ? rnntg_f64::exp_t(x, etab) : exp_main(x, etab);
 }
 
 template <int NR>
 __device__ __forceinline__ void lse_exact(const float* const* L, const float* M, int V,
                                           double* __restrict__ scr, const uint64_t* __restrict__ etab,
                                           double* lse) {
+  static_assert(NR == 1 || NR == 2, "one or two rows per warp");
+  // Lanes [j*LPR, (j+1)*LPR) own row j; a chunk is LPR consecutive k.
+  // Software-pipelined over a double-buffered scratch (buffer b at
+  // scr + 32 b): iteration c loads chunk c's exps (broadcast within the
+  // row's lanes), evaluates chunk c+1's exps while chunk c's chain runs,
+  // then stores them into the other buffer.
+  constexpr int LPR = 32 / NR;
+  constexpr int NV = LPR / 2;
+  constexpr int kLseGroup = NV < RNNTG_LSE_GROUP ? NV : RNNTG_LSE_GROUP;
   const int lane = threadIdx.x & 31;
-  double acc[NR];
+  const int j = lane / LPR, p = lane % LPR;
+  const float* Lj = L[0];
+  float Mf = M[0];
 #pragma unroll
-  for (int j = 0; j < NR; ++j) acc[j] = 0.0;
-  for (int c = 0; c < V; c += 32) {
-    const int k = c + lane;
+  for (int q = 1; q < NR; ++q)
+    if (j == q) {
+      Lj = L[q];
+      Mf = M[q];
+    }
+  const double Mj = static_cast<double>(Mf);
+  // exp(double(l) - max) of column k (0.0 past the row end); the whole warp
+  // calls it: the rare |x| >= 512 fix-up is a warp-uniform branch, so the
+  // straight-line main path interleaves with the chain below.
+  auto arg = [&](int k) { return k < V ? rnntg_f64::xsub(static_cast<double>(Lj[k]), Mj) : -1.0; };
+  auto fix = [&](double x, double y, int k) {
+    if (__any_sync(0xffffffffu, exp_big(x)))
+      if (exp_big(x)) y = rnntg_f64::exp_t(x, etab);
+    return k < V ? y : 0.0;
+  };
+  {
+    const double x = arg(p);
+    scr[j * LPR + p] = fix(x, exp_main(x, etab), p);
+  }
+  __syncwarp();
+  double acc = 0.0;
+  const int nc = (V + LPR - 1) / LPR;
+  for (int c = 0; c < nc; ++c) {
+    const double2* src = reinterpret_cast<const double2*>(scr + (c & 1) * 32 + j * LPR);
+    const int kn = (c + 1) * LPR + p;
+    const double xn = arg(kn);
+    double e = exp_main(xn, etab);
+    // + 0.0 past the end of the row is exact (acc >= 1 by then).  Groups of
+    // 8 loads (16 values) bound the registers this phase adds.
 #pragma unroll
-    for (int j = 0; j < NR; ++j)
-      scr[j * 32 + lane] =
-          k < V ? exp_g(rnntg_f64::xsub(static_cast<double>(L[j][k]), static_cast<double>(M[j])), etab) : 0.0;
-    __syncwarp();
-    // + 0.0 past the end of the row is exact (acc > 0 by then).
+    for (int h = 0; h < NV; h += kLseGroup) {
+      double2 v[kLseGroup];
 #pragma unroll
-    for (int q = 0; q < 16; ++q)
+      for (int q = 0; q < kLseGroup; ++q) v[q] = src[h + q];
 #pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        const double2 p = reinterpret_cast<const double2*>(scr + j * 32)[q];
-        acc[j] = rnntg_f64::xadd(rnntg_f64::xadd(acc[j], p.x), p.y);
-      }
+      for (int q = 0; q < kLseGroup; ++q) acc = rnntg_f64::xadd(rnntg_f64::xadd(acc, v[q].x), v[q].y);
+    }
+    e = fix(xn, e, kn);
+    scr[((c + 1) & 1) * 32 + j * LPR + p] = e;
     __syncwarp();
   }
+  const double lj = rnntg_f64::xadd(Mj, rnntg_f64::log(acc));
 #pragma unroll
-  for (int j = 0; j < NR; ++j) lse[j] = rnntg_f64::xadd(static_cast<double>(M[j]), rnntg_f64::log(acc[j]));
+  for (int q = 0; q < NR; ++q) lse[q] = __shfl_sync(0xffffffffu, lj, q * LPR);
 }
 
 // One row (one warp): float max, then lse_exact.
