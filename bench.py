@@ -228,10 +228,26 @@ def cpu_baseline_and_parity(threads, streams, T, gpu_tokens, gpu_scores):
         "tokens_identical_streams": int(sum(same)),
         "tokens_identical": bool(all(same)),
         "max_score_rel_err": float(rel.max()) if len(rel) else 0.0,
-        "score_tolerance": 1e-9,
+        "scores_bit_equal": bool(np.array_equal(np.asarray(gpu_scores[:streams], np.float64).view(np.int64),
+                                                np.asarray(osc, np.float64).view(np.int64))),
+        "score_tolerance": 0.0,
         "reference_tokens_per_frame": sum(len(x) for x in want) / frames,
     }
     return base, parity
+
+
+def cxx_dropin(B, T, reps=2):
+    """The same workload through the C++ drop-in (include/rnnt_gpu.hpp,
+    tests/cpp/shim_bench): host acoustic features in, token sequences out,
+    the reference's call shape; GPU encoder + exact beam search."""
+    exe = os.path.join(ROOT, "tests", "cpp", "shim_bench")
+    if not os.path.exists(exe):
+        return {"unavailable": "tests/cpp/shim_bench not built"}
+    try:
+        r = subprocess.run([exe, str(B), str(T), str(reps)], capture_output=True, text=True, timeout=300)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": str(e)[:200]}
 
 
 def run_reference(args):
@@ -516,6 +532,8 @@ def main(argv=None):
             "model_prep_s": model_prep_s,
             "clocks": clk.summary(),
         }
+        if world == 1:
+            line["cxx_dropin"] = cxx_dropin(B, T)
         if not args.no_cpu_baseline and world == 1:
             threads = os.cpu_count() or 1
             try:

@@ -14,9 +14,13 @@
 //   rnnt::fsa_beam_search + lattice_to_best_seq(kMax)   fsa_search.hpp:326-409
 //     -> rnnt::gpu::fsa_best_sequences(ctx, m, batch, graph, params)
 //
-// Like the reference, each search takes acoustic features and runs the
-// reference's own encoder_forward on the host (model.hpp:224-238) before the
-// GPU decode; callers that already hold encoder frames use the C ABI directly.
+// Like the reference, each search takes acoustic features.  The encoder
+// (encoder_forward, model.hpp:224-238) runs on the GPU, bit-exact with the
+// reference's (RNNTG_MEM_HOST_FEATURES: features in, device-resident frames,
+// host results), so a call costs one H2D copy of the features and no host
+// compute; callers that already hold encoder frames use the C ABI directly.
+// Decoding graphs are uploaded once per Context and reused for every call
+// with the same graph content.
 // Errors map back to the reference's types: RNNTG_INVALID_ARGUMENT ->
 // rnnt::ValidationError, RNNTG_INTERNAL -> std::logic_error, anything else ->
 // std::runtime_error.
@@ -24,6 +28,8 @@
 #define RNNT_GPU_HPP_
 
 #include <cstdint>
+#include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -62,31 +68,93 @@ class Context {
     d.out_w = m.out_w.data.data();
     d.out_b = m.out_b.data.data();
     check(rnntg_model_create(&d, device, &h_));
+    rnntg_encoder_desc e{};
+    e.feat_dim = m.cfg.feat_dim;
+    e.enc_w1 = m.enc_w1.data.data();
+    e.enc_b1 = m.enc_b1.data.data();
+    e.enc_w2 = m.enc_w2.data.data();
+    e.enc_b2 = m.enc_b2.data.data();
+    const rnntg_status st = rnntg_model_set_encoder(h_, &e);
+    if (st != RNNTG_OK) {
+      rnntg_model_destroy(h_);
+      check(st);
+    }
   }
-  ~Context() { rnntg_model_destroy(h_); }
+  ~Context() {
+    for (Cached& c : graphs_) rnntg_graph_destroy(c.handle);
+    rnntg_model_destroy(h_);
+  }
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
   rnntg_model_t handle() const { return h_; }
 
+  // The device copy of `graph` (fsa.hpp:54-80), uploaded on first use and
+  // reused by content (a 64-bit hash of the CSR, confirmed by Fsa equality).
+  rnntg_graph_t graph(const Fsa& graph) {
+    const uint64_t key = hash(graph);
+    for (Cached& c : graphs_)
+      if (c.key == key && *c.copy == graph) return c.handle;
+    std::vector<int32_t> dst, label;
+    std::vector<double> w;
+    dst.reserve(graph.arcs.size());
+    label.reserve(graph.arcs.size());
+    w.reserve(graph.arcs.size());
+    for (const Arc& a : graph.arcs) {
+      dst.push_back(a.dst);
+      label.push_back(a.label);
+      w.push_back(a.score);
+    }
+    rnntg_graph_t g = nullptr;
+    check(rnntg_graph_create(h_, graph.num_states, graph.arc_splits.data(),
+                             static_cast<int32_t>(graph.arcs.size()), dst.data(), label.data(), w.data(), &g));
+    graphs_.push_back({key, std::make_unique<Fsa>(graph), g});
+    return g;
+  }
+
  private:
+  struct Cached {
+    uint64_t key;
+    std::unique_ptr<Fsa> copy;
+    rnntg_graph_t handle;
+  };
+  static uint64_t hash(const Fsa& g) {
+    uint64_t x = 0xcbf29ce484222325ull ^ static_cast<uint64_t>(g.num_states);
+    auto mix = [&x](uint64_t v) { x = (x ^ v) * 0x100000001b3ull; };
+    for (int32_t v : g.arc_splits) mix(static_cast<uint32_t>(v));
+    for (const Arc& a : g.arcs) {
+      uint64_t b;
+      std::memcpy(&b, &a.score, 8);
+      mix((static_cast<uint64_t>(static_cast<uint32_t>(a.dst)) << 32) | static_cast<uint32_t>(a.label));
+      mix(b);
+    }
+    return x;
+  }
   rnntg_model_t h_ = nullptr;
+  std::vector<Cached> graphs_;
 };
 
 namespace detail {
 
+// The batch's features, concatenated, with the reference encoder's
+// validation (model.hpp:226-228); the GPU runs the encoder itself.
 struct Frames {
-  std::vector<float> enc;
+  std::vector<float> enc;  // features [sum T][F] (RNNTG_MEM_HOST_FEATURES)
   std::vector<int32_t> splits;
 };
 
 inline Frames encode(const ToyTransducer& m, const std::vector<Mat<float>>& batch) {
+  check_model_shapes(m);
   Frames f;
   f.splits.push_back(0);
+  size_t n = 0;
+  for (const Mat<float>& x : batch) n += x.data.size();
+  f.enc.reserve(std::max<size_t>(1, n));
   for (const Mat<float>& x : batch) {
-    Mat<float> e = encoder_forward(m, x);
-    f.enc.insert(f.enc.end(), e.data.begin(), e.data.end());
-    f.splits.push_back(f.splits.back() + e.rows);
+    if (x.cols != m.cfg.feat_dim) throw ValidationError("features must have feat_dim columns");
+    f.enc.insert(f.enc.end(), x.data.begin(), x.data.end());
+    f.splits.push_back(f.splits.back() + x.rows);
   }
+  if (f.enc.empty()) f.enc.push_back(0.0f);
   return f;
 }
 
@@ -109,7 +177,7 @@ inline std::vector<std::vector<int32_t>> greedy_search_batch(
   const int32_t B = static_cast<int32_t>(batch.size());
   std::vector<int32_t> splits(B + 1), toks(std::max<int32_t>(1, f.splits.back()));
   check(rnntg_greedy_search_batch(ctx.handle(), f.enc.data(), f.splits.data(), B, max_symbols,
-                                  RNNTG_MEM_HOST, splits.data(), toks.data()));
+                                  RNNTG_MEM_HOST_FEATURES, splits.data(), toks.data()));
   return detail::unpack(splits, toks);
 }
 
@@ -125,7 +193,7 @@ inline std::vector<std::vector<int32_t>> greedy_search_batched(
   std::vector<int32_t> splits(B + 1), toks(std::max<int64_t>(1, f.splits.back() * cap));
   int64_t capped = 0;
   check(rnntg_greedy_search(ctx.handle(), f.enc.data(), f.splits.data(), B, max_symbols,
-                            RNNTG_MEM_HOST, splits.data(), toks.data(), &capped));
+                            RNNTG_MEM_HOST_FEATURES, splits.data(), toks.data(), &capped));
   if (capped_frames) *capped_frames = capped;
   return detail::unpack(splits, toks);
 }
@@ -150,7 +218,7 @@ inline std::vector<std::vector<int32_t>> beam_search_batch(
   std::vector<int32_t> splits(B + 1), toks(std::max<int64_t>(1, f.splits.back() * cap));
   std::vector<double> sc(std::max<int32_t>(1, B));
   check(rnntg_beam_search_batch(ctx.handle(), f.enc.data(), f.splits.data(), B, &p,
-                                RNNTG_MEM_HOST, splits.data(), toks.data(), sc.data()));
+                                RNNTG_MEM_HOST_FEATURES, splits.data(), toks.data(), sc.data()));
   if (scores) scores->assign(sc.begin(), sc.begin() + B);
   return detail::unpack(splits, toks);
 }
@@ -167,26 +235,14 @@ inline std::vector<std::vector<int32_t>> fsa_best_sequences(
     Context& ctx, const ToyTransducer& m, const std::vector<Mat<float>>& batch,
     const Fsa& graph, const FsaSearchParams& params,
     std::vector<double>* scores = nullptr) {
-  std::vector<int32_t> dst, label;
-  std::vector<double> w;
-  for (const Arc& a : graph.arcs) {
-    dst.push_back(a.dst);
-    label.push_back(a.label);
-    w.push_back(a.score);
-  }
-  rnntg_graph_t g = nullptr;
-  check(rnntg_graph_create(ctx.handle(), graph.num_states, graph.arc_splits.data(),
-                           static_cast<int32_t>(graph.arcs.size()), dst.data(), label.data(),
-                           w.data(), &g));
+  rnntg_graph_t g = ctx.graph(graph);
   detail::Frames f = detail::encode(m, batch);
   const int32_t B = static_cast<int32_t>(batch.size());
   rnntg_fsa_params p{params.beam, params.max_states, params.max_contexts};
   std::vector<int32_t> splits(B + 1), toks(std::max<int32_t>(1, f.splits.back()));
   std::vector<double> sc(std::max<int32_t>(1, B));
-  const rnntg_status st = rnntg_fsa_beam_search(ctx.handle(), f.enc.data(), f.splits.data(), B, g, &p,
-                                                RNNTG_MEM_HOST, splits.data(), toks.data(), sc.data());
-  rnntg_graph_destroy(g);
-  check(st);
+  check(rnntg_fsa_beam_search(ctx.handle(), f.enc.data(), f.splits.data(), B, g, &p,
+                              RNNTG_MEM_HOST_FEATURES, splits.data(), toks.data(), sc.data()));
   if (scores) scores->assign(sc.begin(), sc.begin() + B);
   return detail::unpack(splits, toks);
 }

@@ -57,7 +57,12 @@ typedef enum {
 /* Where the frame / result buffers of a decode call live. */
 typedef enum {
   RNNTG_MEM_HOST = 0,   /* host memory: H2D and D2H copies inside the call */
-  RNNTG_MEM_DEVICE = 1  /* device memory on the model's GPU */
+  RNNTG_MEM_DEVICE = 1, /* device memory on the model's GPU */
+  /* search inputs only: `enc` points to host ACOUSTIC FEATURES [sum T][F]
+   * (the reference API's input); the GPU encoder (rnntg_encoder_forward,
+   * bit-exact encoder_forward) turns them into device-resident frames first.
+   * Needs rnntg_model_set_encoder.  Outputs are host memory. */
+  RNNTG_MEM_HOST_FEATURES = 2
 } rnntg_mem;
 
 typedef enum { RNNTG_MERGE_MAX = 0, RNNTG_MERGE_LOG_ADD = 1 } rnntg_merge_op;

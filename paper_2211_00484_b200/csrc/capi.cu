@@ -52,7 +52,7 @@ struct rnntg_model_s {
   bool greedy_cluster = true;
   int32_t slot_mult = 1;  // token slots per frame of the current call (greedy S > 1)
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
-  Scratch finfo, nodebest, lattice, flag, feat, hid;
+  Scratch finfo, nodebest, lattice, flag, feat, hid, fenc;
   int64_t lat_cap_hint = 0;
   cudaStream_t cstream[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t done[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -105,6 +105,64 @@ rnntg_status check_frames(const float* enc, const int32_t* fs, int32_t B) {
   for (int32_t i = 0; i < B; ++i)
     if (fs[i + 1] < fs[i]) return invalid("frame_splits must be non-decreasing");
   if (B > 0 && fs[B] > 0 && enc == nullptr) return invalid("enc is null");
+  return RNNTG_OK;
+}
+
+rnntg_status encoder_impl(rnntg_model_t h, const float* feats, const int32_t* fs, int32_t B, int32_t mem,
+                          float* enc_out) {
+  const int64_t total = B > 0 ? fs[B] : 0;
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  const int32_t D = h->d.D, F = h->d.F, Dp = round_up(D, 128);
+  const float* x = feats;
+  float* y = enc_out;
+  // HOST: host in, host out; DEVICE: device in and out; HOST_FEATURES
+  // (internal, frames_from): host features in, device frames out.
+  if (mem != RNNTG_MEM_DEVICE) {
+    RNNTG_CUDA_TRY(h->feat.ensure(sizeof(float) * total * F));
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(h->feat.ptr, feats, sizeof(float) * total * F,
+                                   cudaMemcpyHostToDevice, h->stream));
+    x = h->feat.as<float>();
+  }
+  if (mem == RNNTG_MEM_HOST) {
+    RNNTG_CUDA_TRY(h->enc.ensure(sizeof(float) * total * D));
+    y = h->enc.as<float>();
+  }
+  RNNTG_CUDA_TRY(h->hid.ensure(sizeof(float) * total * D));
+  // encoder_forward (model.hpp:224-238): two affine + tanh layers per frame.
+  RNNTG_CUDA_TRY(rnntg::launch_gemm_exact(x, F, h->d.enc_w1t, Dp, h->d.enc_b1, h->hid.as<float>(), D,
+                                          total, D, F, true, nullptr, 0, 0, h->stream));
+  RNNTG_CUDA_TRY(rnntg::launch_gemm_exact(h->hid.as<float>(), D, h->d.enc_w2t, Dp, h->d.enc_b2, y, D,
+                                          total, D, D, true, nullptr, 0, 0, h->stream));
+  if (mem == RNNTG_MEM_HOST)
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(enc_out, y, sizeof(float) * total * D, cudaMemcpyDeviceToHost, h->stream));
+  RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return RNNTG_OK;
+}
+
+bool mem_ok(int32_t mem) {
+  return mem == RNNTG_MEM_HOST || mem == RNNTG_MEM_DEVICE || mem == RNNTG_MEM_HOST_FEATURES;
+}
+
+// RNNTG_MEM_HOST_FEATURES (the reference's own input, model.hpp:224-238):
+// the GPU encoder turns the host features into device-resident frames
+// (h->fenc); the search then runs on device frames and returns host
+// results.  On return `enc` / `mem` describe the frames, `out_mem` the
+// outputs.  Caller holds h->mu.
+rnntg_status frames_from(rnntg_model_t h, const float*& enc, const int32_t* fs, int32_t B, int32_t& mem,
+                         int32_t& out_mem) {
+  out_mem = mem;
+  if (mem != RNNTG_MEM_HOST_FEATURES) return RNNTG_OK;
+  if (h->d.F == 0) return invalid("no encoder weights (rnntg_model_set_encoder)");
+  const int64_t total = B > 0 ? fs[B] : 0;
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  RNNTG_CUDA_TRY(h->fenc.ensure(sizeof(float) * std::max<int64_t>(1, total) * h->d.D));
+  if (total > 0) {
+    rnntg_status st = encoder_impl(h, enc, fs, B, RNNTG_MEM_HOST_FEATURES, h->fenc.as<float>());
+    if (st) return st;
+  }
+  enc = h->fenc.as<float>();
+  mem = RNNTG_MEM_DEVICE;
+  out_mem = RNNTG_MEM_HOST;
   return RNNTG_OK;
 }
 
@@ -554,6 +612,9 @@ namespace {
 // unlimited).  Caller holds h->mu and has validated the arguments.
 rnntg_status greedy_impl(rnntg_model_t h, const float* enc, const int32_t* fs, int32_t B, int32_t cap,
                          bool count_capped, int32_t mem, int32_t* out_splits, int32_t* out_tokens) {
+  int32_t out_mem = mem;
+  rnntg_status st0 = frames_from(h, enc, fs, B, mem, out_mem);
+  if (st0) return st0;
   RNNTG_CUDA_TRY(cudaSetDevice(h->device));
   h->slot_mult = cap;
   rnntg_status st = prepare(h, fs, B, mem);
@@ -587,7 +648,7 @@ rnntg_status greedy_impl(rnntg_model_t h, const float* enc, const int32_t* fs, i
       return st;
     }
   }
-  st = finish(h, fs, B, mem, out_splits, out_tokens, nullptr, launches);
+  st = finish(h, fs, B, out_mem, out_splits, out_tokens, nullptr, launches);
   h->slot_mult = 1;
   return st;
 }
@@ -600,7 +661,7 @@ rnntg_status rnntg_greedy_search_batch(rnntg_model_t h, const float* enc,
   if (!h) return invalid("null model");
   // search.hpp:110-111.
   if (max_symbols != 1) return invalid("greedy_search_batch supports max_symbols = 1 only");
-  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
+  if (!mem_ok(mem)) return invalid("bad mem kind");
   rnntg_status st = check_frames(enc, fs, B);
   if (st) return st;
   if (!out_splits) return invalid("out_splits is null");
@@ -614,7 +675,7 @@ rnntg_status rnntg_greedy_search(rnntg_model_t h, const float* enc, const int32_
   if (!h) return invalid("null model");
   // search.hpp:80 and 31-34 (kNoSymbolLimit -> kMaxSymbolsPerFrameSafety = 10).
   if (max_symbols < 1) return invalid("max_symbols must be >= 1");
-  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
+  if (!mem_ok(mem)) return invalid("bad mem kind");
   rnntg_status st = check_frames(enc, fs, B);
   if (st) return st;
   if (!out_splits) return invalid("out_splits is null");
@@ -640,11 +701,13 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
     return RNNTG_UNSUPPORTED;
   }
   if (p->merge_op != RNNTG_MERGE_MAX && p->merge_op != RNNTG_MERGE_LOG_ADD) return invalid("bad merge_op");
-  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
+  if (!mem_ok(mem)) return invalid("bad mem kind");
   rnntg_status st = check_frames(enc, fs, B);
   if (st) return st;
   if (!out_splits) return invalid("out_splits is null");
   std::lock_guard<std::mutex> lk(h->mu);
+  int32_t out_mem = mem;
+  if ((st = frames_from(h, enc, fs, B, mem, out_mem))) return st;
   RNNTG_CUDA_TRY(cudaSetDevice(h->device));
   // S > 1 (search.hpp:228-235): up to `cap` sub-steps per frame, cap = 10
   // for kNoSymbolLimit (frames stopped by it counted in the stats).
@@ -686,7 +749,7 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       return rnntg::launch_decode_beam(a, cs);
     });
     if (st) return st;
-    return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+    return finish(h, fs, B, out_mem, out_splits, out_tokens, out_scores, launches);
   }
   if (B > 0) {
     const int64_t total = fs[B];
@@ -734,7 +797,7 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
         return rnntg::launch_decode_beam(a, cs);
       });
       if (st) return st;
-      return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+      return finish(h, fs, B, out_mem, out_splits, out_tokens, out_scores, launches);
     }
     st = run_pipeline(h, enc, fs, B, mem, G, &launches, [&](int32_t b0, int32_t b1, cudaStream_t cs) {
       rnntg::DecodeArgs a = args(b0, b1);
@@ -742,7 +805,7 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
     });
     if (st) return st;
   }
-  return finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+  return finish(h, fs, B, out_mem, out_splits, out_tokens, out_scores, launches);
 }
 
 rnntg_status rnntg_graph_create(rnntg_model_t h, int32_t num_states,
@@ -821,7 +884,7 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
   if (!(p->beam >= 0.0)) return invalid("fsa search beam must be >= 0");
   if (p->max_states < 1) return invalid("max_states must be >= 1");
   if (p->max_contexts < 1) return invalid("max_contexts must be >= 1");
-  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
+  if (!mem_ok(mem)) return invalid("bad mem kind");
   rnntg_status st = check_frames(enc, fs, B);
   if (st) return st;
   if (!out_splits) return invalid("out_splits is null");
@@ -829,6 +892,8 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
   // The lattice buffers are overwritten below; until this call succeeds there
   // is no exportable lattice (rnntg_fsa_lattice).
   h->last_fsa_fs.clear();
+  int32_t out_mem = mem;
+  if ((st = frames_from(h, enc, fs, B, mem, out_mem))) return st;
   RNNTG_CUDA_TRY(cudaSetDevice(h->device));
   if ((st = prepare(h, fs, B, mem))) return st;
   int64_t launches = 0;
@@ -921,7 +986,7 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
       break;
     }
   }
-  st = finish(h, fs, B, mem, out_splits, out_tokens, out_scores, launches);
+  st = finish(h, fs, B, out_mem, out_splits, out_tokens, out_scores, launches);
   if (st == RNNTG_OK) h->last_fsa_fs.assign(fs, fs + B + 1);
   return st;
 }
@@ -1061,29 +1126,9 @@ rnntg_status rnntg_encoder_forward(rnntg_model_t h, const float* feats, const in
   if (total == 0) return RNNTG_OK;
   if (!enc_out) return invalid("enc_out is null");
   std::lock_guard<std::mutex> lk(h->mu);
-  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
-  const int32_t D = h->d.D, F = h->d.F, Dp = round_up(D, 128);
-  const float* x = feats;
-  float* y = enc_out;
-  if (mem == RNNTG_MEM_HOST) {
-    RNNTG_CUDA_TRY(h->feat.ensure(sizeof(float) * total * F));
-    RNNTG_CUDA_TRY(h->enc.ensure(sizeof(float) * total * D));
-    RNNTG_CUDA_TRY(cudaMemcpyAsync(h->feat.ptr, feats, sizeof(float) * total * F,
-                                   cudaMemcpyHostToDevice, h->stream));
-    x = h->feat.as<float>();
-    y = h->enc.as<float>();
-  }
-  RNNTG_CUDA_TRY(h->hid.ensure(sizeof(float) * total * D));
-  // encoder_forward (model.hpp:224-238): two affine + tanh layers per frame.
-  RNNTG_CUDA_TRY(rnntg::launch_gemm_exact(x, F, h->d.enc_w1t, Dp, h->d.enc_b1, h->hid.as<float>(), D,
-                                          total, D, F, true, nullptr, 0, 0, h->stream));
-  RNNTG_CUDA_TRY(rnntg::launch_gemm_exact(h->hid.as<float>(), D, h->d.enc_w2t, Dp, h->d.enc_b2, y, D,
-                                          total, D, D, true, nullptr, 0, 0, h->stream));
-  if (mem == RNNTG_MEM_HOST)
-    RNNTG_CUDA_TRY(cudaMemcpyAsync(enc_out, y, sizeof(float) * total * D, cudaMemcpyDeviceToHost, h->stream));
-  RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
-  return RNNTG_OK;
+  return encoder_impl(h, feats, fs, B, mem, enc_out);
 }
+
 
 rnntg_status rnntg_debug_decoder_projection(rnntg_model_t h, const int32_t* ctxs,
                                             int32_t n, float* pd_out) {

@@ -373,6 +373,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       // group scan) and an upper bound on the frame's best candidate: tuple i
       // scores at most score_i + max(0, max arc weight of its state) +
       // max_k lp_i[k].
+      int n_raw_all = 0;  // every thread's copy of the group scan total
       {
         const int i = grp.tid;
         int cnt = 0;
@@ -386,6 +387,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         }
         int total = 0;
         const int off = group_scan(grp, S, cnt, &total);
+        n_raw_all = total;
         if (i < S.n_act) S.act_off[i] = off;
         const double ubm = group_max(grp, S, bound);
         if (grp.tid == 0) {
@@ -400,7 +402,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         S.hkey[b] = kEmptyKey;
         S.hval[b] = 0ull;
       }
-      for (int w = grp.tid; w < (min(S.n_raw, kMaxRaw) + 31) / 32; w += nt) S.mbits[w] = 0u;
+      // (the scan total, not S.n_raw: thread 0 may still be writing that)
+      for (int w = grp.tid; w < (min(n_raw_all, kMaxRaw) + 31) / 32; w += nt) S.mbits[w] = 0u;
       grp.sync();
       const int nraw = min(S.n_raw, kMaxRaw);
       const double ub = S.ub;

@@ -47,6 +47,10 @@ int main() {
   fp.max_states = 8;
   fp.max_contexts = 4;
   auto gf = gpu::fsa_best_sequences(ctx, m, batch, g, fp);
+  if (gpu::fsa_best_sequences(ctx, m, batch, trivial_graph(cfg.vocab_size), fp) != gf) {  // cached graph
+    std::printf("fsa (cached graph) mismatch\n");
+    ++bad;
+  }
   std::vector<Fsa> graphs(batch.size(), g);
   auto lats = fsa_beam_search(m, batch, graphs, fp);
   for (size_t i = 0; i < batch.size(); ++i)
@@ -54,17 +58,15 @@ int main() {
       std::printf("fsa mismatch %zu\n", i);
       ++bad;
     }
-  // Whole lattices through the reference-typed fsa_beam_search: same nodes,
-  // arcs and labels; scores to 1e-12 relative; same best sequences.
+  // Whole lattices through the reference-typed fsa_beam_search: equal Fsa
+  // objects (nodes, arcs, labels, fp64 scores bit for bit, finals) and
+  // byte-identical serialize_lattice text (the CLI's lattice files).
   auto glats = gpu::fsa_beam_search(ctx, m, batch, graphs, fp);
   for (size_t i = 0; i < batch.size(); ++i) {
     const Fsa& a = glats[i];
     const Fsa& b = lats[i];
-    bool same = a.num_states == b.num_states && a.arcs.size() == b.arcs.size() && a.finals == b.finals;
-    for (size_t k = 0; same && k < a.arcs.size(); ++k)
-      same = a.arcs[k].src == b.arcs[k].src && a.arcs[k].dst == b.arcs[k].dst &&
-             a.arcs[k].label == b.arcs[k].label &&
-             std::abs(a.arcs[k].score - b.arcs[k].score) <= 1e-12 * std::abs(b.arcs[k].score) + 1e-15;
+    const bool same = a == b && serialize_lattice(a, static_cast<int32_t>(i), batch[i].rows) ==
+                                    serialize_lattice(b, static_cast<int32_t>(i), batch[i].rows);
     if (!same || lattice_to_best_seq(a, MergeOp::kMax) != lattice_to_best_seq(b, MergeOp::kMax)) {
       std::printf("lattice mismatch %zu\n", i);
       ++bad;
