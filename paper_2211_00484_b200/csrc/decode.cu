@@ -447,7 +447,10 @@ __device__ __forceinline__ void beam_row_reduce_n(float* HL, int Vp, int V, int 
   }
 }
 
-// D for the whole CTA with the weight stages as scratch (WPipe::defer):
+// D for the whole CTA with the weight stages as scratch (WPipe::defer).
+// (The arithmetic of decode_common.cuh's lse_cta_exps / lse_cta_chain, kept
+// written out here: composed from those helpers ptxas allocates the beam
+// kernel's frame loop differently and its GEMM phase runs ~3% slower.)
 //  (a) row maxima (model.hpp:117-118), one warp per row;
 //  (b) every exp(double(l_k) - max) of every row into E (row stride S, odd
 //      so the chain lanes below hit distinct banks), one column per thread

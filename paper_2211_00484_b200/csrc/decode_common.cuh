@@ -618,6 +618,88 @@ __device__ __forceinline__ void lse_exact(const float* const* L, const float* M,
   for (int q = 0; q < NR; ++q) lse[q] = __shfl_sync(0xffffffffu, lj, q * LPR);
 }
 
+// Exact normalisers of R rows for the whole CTA, with `E` (>= ecap doubles;
+// the weight stages under WPipe::defer) as scratch:
+//  (a) row maxima (model.hpp:117-118), one warp per row -> row_m;
+//  (b) every exp(double(l_k) - max) of every row into E (row stride S, odd
+//      so the chain lanes below hit distinct banks), one column per thread:
+//      all the exp work spread over the CTA;
+//  (c) one warp runs the reference's sequential sums (model.hpp:119-121),
+//      one lane per row, while the other warps do other work.
+// The index-order fp64 chain is ~V dependent DADDs per row; here it costs
+// one warp V instructions for all rows.  Requires lse_cta_fits(R, V, ecap).
+__host__ __device__ inline int lse_cta_stride(int V, int R, int ecap) {
+  const int V8 = (V + 7) / 8 * 8;
+  return (V8 + 1) * R <= ecap ? V8 + 1 : V8;
+}
+__host__ __device__ inline bool lse_cta_fits(int R, int V, int ecap) {
+  return V <= kDecodeThreads && lse_cta_stride(V, R, ecap) * R <= ecap;
+}
+// (a) + (b): row maxima, then every exp into E.  Ends with a CTA barrier.
+__device__ __forceinline__ void lse_cta_exps(const float* HL, double* E, int ecap, int Vp, int V, int R,
+                                             const uint64_t* etab, float* row_m) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < R; r += kWarps) {
+    const float* L = HL + static_cast<int64_t>(r) * Vp;
+    float mx = -FLT_MAX;
+    for (int k = lane; k < V; k += 32) mx = fmaxf(mx, L[k]);
+    mx = warp_max_f(mx);
+    if (lane == 0) row_m[r] = mx;
+  }
+  __syncthreads();
+  // Rows are zero-padded to V8 = V rounded up to 8 (+ 0.0 is exact once the
+  // sum holds exp(0) = 1), so the chain runs in whole groups of 8.
+  const int V8 = (V + 7) / 8 * 8;
+  const int S = lse_cta_stride(V, R, ecap);
+  const int k = threadIdx.x;  // V8 <= kDecodeThreads
+  auto arg = [&](int r) {
+    return k < V ? rnntg_f64::xsub(static_cast<double>(HL[static_cast<int64_t>(r) * Vp + k]),
+                                   static_cast<double>(row_m[r]))
+                 : -1.0;
+  };
+  for (int r = 0; r < R; r += 2) {  // two rows per trip: independent exp chains interleave
+    const int r1 = r + 1 < R ? r + 1 : r;
+    const double x0 = arg(r), x1 = arg(r1);
+    double y0 = exp_main(x0, etab), y1 = exp_main(x1, etab);
+    if (__any_sync(0xffffffffu, exp_big(x0) || exp_big(x1))) {
+      if (exp_big(x0)) y0 = rnntg_f64::exp_t(x0, etab);
+      if (exp_big(x1)) y1 = rnntg_f64::exp_t(x1, etab);
+    }
+    if (k < V8) {
+      E[r * S + k] = k < V ? y0 : 0.0;
+      E[r1 * S + k] = k < V ? y1 : 0.0;
+    }
+  }
+  __syncthreads();
+}
+
+// (c) one warp (lane = row): the reference's sequential sums, software-
+// pipelined (group q + 1's loads in flight while group q's 8 dependent
+// DADDs run), then lse = max + log(sum).
+__device__ __forceinline__ void lse_cta_chain(const float* HL, const double* E, int ecap, int Vp, int V, int R,
+                                              const float* row_m, double* lse_out, float* l0_out) {
+  constexpr int G8 = 8;
+  const int lane = threadIdx.x & 31;
+  if (lane >= R) return;
+  const int V8 = (V + G8 - 1) / G8 * G8;
+  const double* e = E + lane * lse_cta_stride(V, R, ecap);
+  double acc = 0.0, cur[G8], nxt[G8];
+#pragma unroll
+  for (int u = 0; u < G8; ++u) cur[u] = e[u];
+  for (int q = G8; q < V8; q += G8) {
+#pragma unroll
+    for (int u = 0; u < G8; ++u) nxt[u] = e[q + u];
+#pragma unroll
+    for (int u = 0; u < G8; ++u) acc = rnntg_f64::xadd(acc, cur[u]);
+#pragma unroll
+    for (int u = 0; u < G8; ++u) cur[u] = nxt[u];
+  }
+#pragma unroll
+  for (int u = 0; u < G8; ++u) acc = rnntg_f64::xadd(acc, cur[u]);
+  lse_out[lane] = rnntg_f64::xadd(static_cast<double>(row_m[lane]), rnntg_f64::log(acc));
+  if (l0_out) l0_out[lane] = HL[static_cast<int64_t>(lane) * Vp];
+}
+
 // One row (one warp): float max, then lse_exact.
 __device__ __forceinline__ double row_lse(const float* L, int V, double* scr, const uint64_t* etab) {
   const int lane = threadIdx.x & 31;

@@ -87,6 +87,7 @@ struct FsaSmem {
   int32_t row_ctx[kRowCap];
   double row_lse[kRowCap];
   double row_lpmax[kRowCap];  // max_k lp[k] of the row
+  float row_m[kRowCap];       // row maxima (lse_rows_cta)
   int32_t nrows;
 };
 
@@ -342,6 +343,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         R = kRowCap;
       }
       C.nrows = R;
+      // the exact log-softmax borrows the weight stages when its scratch fits
+      C.pipe.defer = (C.pipe.nc >= 2 && lse_cta_fits(R, m.V, bk * m.Vp)) ? 1 : 0;
     }
     __syncthreads();
     const int R = C.nrows;
@@ -351,7 +354,16 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     const long long c1 = clock64();
     joiner_gemm(m, pipe, gch, HL, R);
     const long long c2 = clock64();
-    {
+    if (pipe.defer) {  // CTA-wide exact normalisers in the weight stages
+      double* E = reinterpret_cast<double*>(W0);
+      lse_cta_exps(HL, E, bk * m.Vp, m.Vp, m.V, R, C.etab, C.row_m);
+      if (threadIdx.x < 32) {
+        lse_cta_chain(HL, E, bk * m.Vp, m.Vp, m.V, R, C.row_m, C.row_lse, nullptr);
+        if (threadIdx.x < R) C.row_lpmax[threadIdx.x] = static_cast<double>(C.row_m[threadIdx.x]) - C.row_lse[threadIdx.x];
+      }
+      __syncthreads();
+      wpipe_issue_next(pipe, m, gch);
+    } else {
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
       for (int r = warp; r < R; r += kDecodeThreads / 32) {
         const float* L = HL + static_cast<int64_t>(r) * m.Vp;
@@ -688,56 +700,120 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   }
 
   // ---- lattice_to_best_seq(kMax) = best_path on the stream's lattice ----
+  // (fsa.hpp:311-376) by the group's first warp.  Backward: frame by frame,
+  // suffix maxima of the layer-t nodes from their arcs (lanes over arcs,
+  // shared-memory atomicMax on order-preserving bits: max is order
+  // independent), layer t+1's values in shared memory, every layer also in
+  // HBM for the trace.  Forward: from node 0, the first arc (lowest index)
+  // attaining the remainder -- lanes test 32 arcs at once, ballot, first set
+  // bit -- with the next frame's arcs and suffix values loaded while this
+  // frame's choice is made.
   const long long cb0 = clock64();
-  if (have && grp.tid == 0 && !(S.flag & 2)) {
+  __syncthreads();  // the frame loop's shared state is free from here on
+  if (have && grp.tid < 32) {
+    const int lane = grp.tid;
     double* nb = nodebest + nbase;
-    const int32_t nn = S.num_nodes;
-    // Layer T nodes reach the super-final node by a score-0 arc.
-    const int32_t lastb = T > 0 ? finfo[fbase + T - 1].z : 0;
-    for (int32_t n = lastb; n < nn; ++n) nb[n] = 0.0;
-    for (int32_t t = T - 1; t >= 0; --t) {
-      const int4 fi = finfo[fbase + t];
-      const int32_t lb = t > 0 ? finfo[fbase + t - 1].z : 0;
-      const int32_t le = t > 0 ? lb + finfo[fbase + t - 1].w : 1;
-      for (int32_t n = lb; n < le; ++n) nb[n] = -INFINITY;
-      for (int32_t a = 0; a < fi.y; ++a) {
-        const LatArc& e = lat[static_cast<int64_t>(fi.x) + a];
-        const double v = e.score + nb[e.dst];
-        if (nb[e.src] < v) nb[e.src] = v;
-      }
-    }
+    double* cur = S.act_score;                                      // layer t+1 suffix values
+    unsigned long long* nxt = reinterpret_cast<unsigned long long*>(S.hval);  // layer t (ordered bits)
     int32_t len = 0;
     double total = 0.0;
-    double remaining = nb[0];
-    if (remaining == -INFINITY || S.flag) {
-      total = -INFINITY;
-    } else {
-      int32_t n = 0;
-      for (int32_t t = 0; t < T; ++t) {
-        const int4 fi = finfo[fbase + t];
-        int32_t chosen = -1;
-        for (int32_t a = 0; a < fi.y; ++a) {
-          const LatArc& e = lat[static_cast<int64_t>(fi.x) + a];
-          if (e.src == n && e.score + nb[e.dst] == remaining) {
-            chosen = a;
+    if (!(S.flag & 2)) {
+      const int32_t nn = S.num_nodes;
+      const int32_t lastb = T > 0 ? finfo[fbase + T - 1].z : 0;
+      for (int32_t n = lastb + lane; n < nn; n += 32) {
+        nb[n] = 0.0;  // layer T reaches the super-final node by a score-0 arc
+        cur[n - lastb] = 0.0;
+      }
+      __syncwarp();
+      // frame t-1's info and first 32 arcs are loaded while frame t is reduced
+      int4 fi_p = T > 0 ? finfo[fbase + T - 1] : make_int4(0, 0, 0, 0);
+      LatArc e_p{};
+      if (T > 0 && lane < fi_p.y) e_p = lat[static_cast<int64_t>(fi_p.x) + lane];
+      for (int32_t t = T - 1; t >= 0; --t) {
+        const int4 fi = fi_p;
+        const LatArc e0 = e_p;
+        if (t > 0) {
+          fi_p = finfo[fbase + t - 1];
+          if (lane < fi_p.y) e_p = lat[static_cast<int64_t>(fi_p.x) + lane];
+        }
+        const int32_t lb = t > 0 ? fi_p.z : 0;
+        const int32_t ln = t > 0 ? fi_p.w : 1;
+        for (int32_t i = lane; i < ln; i += 32) nxt[i] = 0ull;  // below ord_of(-inf)
+        __syncwarp();
+        for (int32_t a = lane; a < fi.y; a += 32) {
+          const LatArc e = a < 32 ? e0 : lat[static_cast<int64_t>(fi.x) + a];
+          atomicMax(&nxt[e.src - lb], ord_of(e.score + cur[e.dst - fi.z]));
+        }
+        __syncwarp();
+        for (int32_t i = lane; i < ln; i += 32) {
+          const double v = nxt[i] ? dbl_of(nxt[i]) : -INFINITY;
+          cur[i] = v;
+          nb[lb + i] = v;
+        }
+        __syncwarp();
+      }
+      double remaining = T > 0 ? nb[0] : 0.0;
+      if (remaining == -INFINITY || S.flag) {
+        total = -INFINITY;
+      } else {
+        int32_t n = 0;
+        LatArc e_n{};
+        double v_n = 0.0;
+        int4 fi_n = T > 0 ? finfo[fbase] : make_int4(0, 0, 0, 0);
+        if (T > 0 && lane < fi_n.y) {
+          e_n = lat[static_cast<int64_t>(fi_n.x) + lane];
+          v_n = nb[e_n.dst];
+        }
+        for (int32_t t = 0; t < T; ++t) {
+          const int4 fi = fi_n;
+          const LatArc e0 = e_n;
+          const double v0 = v_n;
+          if (t + 1 < T) {  // prefetch frame t+1's first 32 arcs and their suffix values
+            fi_n = finfo[fbase + t + 1];
+            if (lane < fi_n.y) {
+              e_n = lat[static_cast<int64_t>(fi_n.x) + lane];
+              v_n = nb[e_n.dst];
+            }
+          }
+          int32_t chosen = -1;
+          LatArc ce{};
+          for (int32_t a0 = 0; a0 < fi.y && chosen < 0; a0 += 32) {
+            LatArc e = e0;
+            double v = v0;
+            if (a0 > 0 && a0 + lane < fi.y) {
+              e = lat[static_cast<int64_t>(fi.x) + a0 + lane];
+              v = nb[e.dst];
+            }
+            const bool hit = a0 + lane < fi.y && e.src == n && e.score + v == remaining;
+            const unsigned ball = __ballot_sync(0xffffffffu, hit);
+            if (ball) {
+              const int src_lane = __ffs(ball) - 1;
+              chosen = a0 + src_lane;
+              ce.dst = __shfl_sync(0xffffffffu, e.dst, src_lane);
+              ce.label = __shfl_sync(0xffffffffu, e.label, src_lane);
+              ce.score = __shfl_sync(0xffffffffu, e.score, src_lane);
+              remaining = __shfl_sync(0xffffffffu, v, src_lane);
+            }
+          }
+          if (chosen < 0) {  // best_path "inconsistent scores"
+            if (lane == 0) atomicExch(error_flag, 5);
             break;
           }
+          if (ce.label != 0) {
+            if (lane == 0) tokens[fs + len] = ce.label;
+            ++len;
+          }
+          total += ce.score;
+          n = ce.dst;
         }
-        if (chosen < 0) {  // best_path "inconsistent scores"
-          atomicExch(error_flag, 5);
-          break;
-        }
-        const LatArc& e = lat[static_cast<int64_t>(fi.x) + chosen];
-        if (e.label != 0) tokens[fs + len++] = e.label;
-        total += e.score;
-        remaining = nb[e.dst];
-        n = e.dst;
+        total += 0.0;  // the score-0 hop into the super-final node
+        total += 0.0;  // its final score
       }
-      total += 0.0;  // the score-0 hop into the super-final node
-      total += 0.0;  // its final score
     }
-    lengths[sidx] = len;
-    scores[sidx] = total;
+    if (lane == 0) {
+      lengths[sidx] = len;
+      scores[sidx] = (S.flag & 2) ? 0.0 : total;
+    }
   }
   if (grp.tid == 0 && have) atomicAdd(&counters[11], static_cast<unsigned long long>(clock64() - cb0));
   if (threadIdx.x == 0) {

@@ -63,7 +63,7 @@ def run(name, m, B, T, kind, params, graph=None, ref_graph=None, cpu_streams=Non
             return dec.greedy_search_batch(d_enc, splits, 1, tok)
         if kind == "beam":
             return dec.beam_search_batch(d_enc, splits, BeamParams(**params), tok, sc)
-        return dec.fsa_beam_search(enc, splits, g, FsaParams(*params))
+        return dec.fsa_beam_search(d_enc, splits, g, FsaParams(*params), tok, sc)
 
     ms, _ = timed(fn)
     st = dec.stats()
@@ -72,7 +72,7 @@ def run(name, m, B, T, kind, params, graph=None, ref_graph=None, cpu_streams=Non
                arcs_per_sf=st["arcs_expanded"] / max(1, st["stream_frames"]),
                lattice_arcs_per_sf=st["lattice_arcs"] / max(1, st["stream_frames"]),
                phase_cycles=st["phase_cycles"],
-               note="fsa timed through host frames (includes H2D)" if kind == "fsa" else "frames resident in HBM")
+               note="frames resident in HBM")
     if cpu_streams:
         n = min(cpu_streams, len(splits_u) - 1)
         f = feats[: n * T]
