@@ -219,6 +219,21 @@ rnntg_status rnntg_fsa_lattice(rnntg_model_t model, int32_t stream,
                                int32_t capacity, int32_t* src, int32_t* dst,
                                int32_t* label, double* score);
 
+/* lattice_to_best_seq(lattice, kLogAdd, nbest_n, seed) (fsa_search.hpp:
+ * 410-425) for every stream of the last rnntg_fsa_beam_search, on the GPU:
+ * n-best sampling with DetRng(seed) (fsa.hpp:390-448), blank-free
+ * deduplication (452-463), per-sequence total log-probability (533-540),
+ * argmax with the reference's tie rule.  Same results as the reference
+ * function on the same lattices (the CLI's `--merge log_add` decode,
+ * rnnt_main.cpp:302).  merge_op must be RNNTG_MERGE_LOG_ADD (kMax is the
+ * search's own output).  Host outputs: out_splits [B+1], out_tokens (<= sum
+ * T), out_logprob [B] (may be NULL): the winner's total, -inf if the
+ * lattice has no complete path (empty sequence). */
+rnntg_status rnntg_fsa_lattice_best(rnntg_model_t model, int32_t merge_op,
+                                    int32_t nbest_n, uint64_t seed,
+                                    int32_t* out_splits, int32_t* out_tokens,
+                                    double* out_logprob);
+
 /* The lattice of `stream` as text, byte-identical to the reference's
  * serialize_fsa_text (fsa.hpp:243-262) of that stream's fsa_beam_search
  * lattice, prefixed with serialize_lattice's "# stream=S frames=T" line

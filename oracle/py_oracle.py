@@ -354,6 +354,11 @@ class Reference:
             C.POINTER(C.c_void_p),
         ]
 
+        L.ref_fsa_logadd.argtypes = [
+            C.c_void_p, _f32p, _i32p, C.c_int32, C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_int,
+            C.c_int32, C.c_uint64, _i32p, _i32p, _f64p,
+        ]
+
     def _check(self, rc):
         if rc != 0:
             raise RuntimeError(f"reference error {rc}: {self.lib.ref_last_error().decode()}")
@@ -578,6 +583,26 @@ class RefModel:
                 out_texts.append(C.cast(texts[i], C.c_char_p).value.decode())
                 self.ref.lib.ref_free_string(texts[i])
         return unragged(osp, otk), osc, out_texts
+
+
+def _refmodel_fsa_logadd(self, feats, splits, graph, beam, max_states, max_contexts, nbest=100, seed=0,
+                         threads=8):
+    """lattice_to_best_seq(kLogAdd, nbest, seed) of each stream's reference
+    lattice, and that sequence's total log-probability."""
+    feats = np.ascontiguousarray(feats, np.float32)
+    splits = np.ascontiguousarray(splits, np.int32)
+    B = len(splits) - 1
+    osp = np.zeros(B + 1, np.int32)
+    otk = np.zeros(max(1, int(splits[-1])), np.int32)
+    olp = np.zeros(max(1, B), np.float64)
+    self.ref._check(
+        self.ref.lib.ref_fsa_logadd(self.h, _p(feats, _f32p), _p(splits, _i32p), B, graph.h, beam, max_states,
+                                    max_contexts, threads, nbest, seed, _p(osp, _i32p), _p(otk, _i32p),
+                                    _p(olp, _f64p)))
+    return unragged(osp, otk), olp[:B]
+
+
+RefModel.fsa_logadd = _refmodel_fsa_logadd
 
 
 def synthetic_arpa(V=500, n_bigrams=1500, n_trigrams=3000, seed=7):

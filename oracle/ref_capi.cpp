@@ -419,4 +419,40 @@ int ref_fsa_beam_search(void* mp, const float* feats, const int32_t* splits,
   }
 }
 
+// fsa_beam_search + lattice_to_best_seq(kLogAdd, nbest_n, seed) per stream
+// (the CLI's `--merge log_add` decode, rnnt_main.cpp:302), sharded like
+// ref_fsa_beam_search.  out_logprob[i] = sequence_total_logprob(lattice,
+// seq) of the returned sequence (-inf for an empty lattice).
+int ref_fsa_logadd(void* mp, const float* feats, const int32_t* splits, int32_t B, void* gp,
+                   double beam, int32_t max_states, int32_t max_contexts, int threads,
+                   int32_t nbest_n, uint64_t seed, int32_t* out_splits, int32_t* out_tokens,
+                   double* out_logprob) {
+  try {
+    auto* m = static_cast<rnnt::ToyTransducer*>(mp);
+    const rnnt::Fsa& g = *static_cast<rnnt::Fsa*>(gp);
+    auto batch = split_frames(feats, splits, B, m->cfg.feat_dim);
+    rnnt::FsaSearchParams p;
+    p.beam = beam;
+    p.max_states = max_states;
+    p.max_contexts = max_contexts;
+    std::vector<std::vector<int32_t>> ys(B);
+    int nshard = std::max(1, std::min<int>(threads, B));
+    parallel_for(nshard, nshard, [&](int64_t s) {
+      std::vector<rnnt::Fsa> one{g};
+      int64_t lo = B * s / nshard, hi = B * (s + 1) / nshard;
+      for (int64_t i = lo; i < hi; ++i) {
+        auto lats = rnnt::fsa_beam_search(*m, {batch[i]}, one, p);
+        ys[i] = rnnt::lattice_to_best_seq(lats[0], rnnt::MergeOp::kLogAdd, nbest_n, seed);
+        double lp = rnnt::kNegInf;
+        if (rnnt::total_logprob(lats[0]) != rnnt::kNegInf) lp = rnnt::sequence_total_logprob(lats[0], ys[i]);
+        out_logprob[i] = lp;
+      }
+    });
+    write_ragged(ys, out_splits, out_tokens);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 }  // extern "C"

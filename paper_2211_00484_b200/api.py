@@ -126,6 +126,7 @@ def _load():
     lib.rnntg_fsa_lattice.argtypes = [vp, i32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), i32, vp, vp, vp, vp]
     lib.rnntg_fsa_lattice.restype = C.c_int
     lib.rnntg_fsa_lattice_text.argtypes = [vp, i32, i32, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
+    lib.rnntg_fsa_lattice_best.argtypes = [vp, i32, i32, C.c_uint64, i32p, vp, vp]
     lib.rnntg_model_set_encoder.argtypes = [vp, C.POINTER(_EncDesc)]
     lib.rnntg_encoder_forward.argtypes = [vp, f32p, i32p, i32, i32, vp]
     lib.rnntg_debug_decoder_projection.argtypes = [vp, i32p, i32, f32p]
@@ -147,6 +148,7 @@ def _load():
         "rnntg_graph_destroy",
         "rnntg_fsa_beam_search",
         "rnntg_fsa_lattice_text",
+        "rnntg_fsa_lattice_best",
         "rnntg_model_set_encoder",
         "rnntg_encoder_forward",
         "rnntg_debug_decoder_projection",
@@ -299,6 +301,7 @@ class Decoder:
         _check(lib.rnntg_model_create(C.byref(desc), device, C.byref(h)))
         self.h = h
         self.device = device
+        self._last_fsa_splits = None
 
     def close(self):
         if getattr(self, "h", None):
@@ -444,6 +447,7 @@ class Decoder:
                 self.h, p, _i32p(splits), B, graph.h, C.byref(fp), mem, _i32p(osp), tokp, scp
             )
         )
+        self._last_fsa_splits = np.array(splits, np.int32)
         if mem == MEM_DEVICE:
             return osp, out_tokens, out_scores
         return _ragged(osp, tok), sc[:B].copy()
@@ -462,6 +466,17 @@ class Decoder:
             )
         )
         return dict(num_nodes=nn.value, src=src[:n], dst=dst[:n], label=lab[:n], score=sc[:n])
+
+    def fsa_lattice_best(self, nbest: int = 100, seed: int = 0, merge_op: int = MERGE_LOG_ADD):
+        """lattice_to_best_seq(lattice, kLogAdd, nbest, seed) of every stream
+        of the last fsa_beam_search (fsa_search.hpp:410-425), on the GPU:
+        (token lists, total log-probabilities of the chosen sequences)."""
+        B = len(self._last_fsa_splits) - 1 if self._last_fsa_splits is not None else 0
+        osp = np.zeros(B + 1, np.int32)
+        tok = np.zeros(max(1, int(self._last_fsa_splits[-1]) if B else 1), np.int32)
+        lp = np.zeros(max(1, B), np.float64)
+        _check(self._lib.rnntg_fsa_lattice_best(self.h, merge_op, nbest, seed, _i32p(osp), _ptr(tok), _ptr(lp)))
+        return _ragged(osp, tok), lp[:B].copy()
 
     def fsa_lattice_text(self, stream: int, header: bool = False) -> str:
         """serialize_fsa_text (or, with header, serialize_lattice) of

@@ -16,7 +16,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librnntg.so")
-SOURCES = ["capi.cu", "gemm_exact.cu", "decode.cu", "fsa.cu", "cluster.cu", "debug.cu", "synth.cpp"]
+SOURCES = ["capi.cu", "gemm_exact.cu", "decode.cu", "fsa.cu", "logadd.cu", "cluster.cu", "debug.cu", "synth.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode",

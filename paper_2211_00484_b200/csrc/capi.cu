@@ -53,6 +53,10 @@ struct rnntg_model_s {
   int32_t slot_mult = 1;  // token slots per frame of the current call (greedy S > 1)
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
   Scratch finfo, nodebest, lattice, flag, feat, hid, fenc;
+  Scratch nodectx, ladd_u, ladd_tot, ladd_narc, ladd_paths, ladd_cells, ladd_pos;  // log-add best sequences
+  int32_t last_fsa_K = 0;
+  uint64_t ladd_seed = 0;
+  int64_t ladd_n = 0, ladd_cell_cap = 4096;
   int64_t lat_cap_hint = 0;
   cudaStream_t cstream[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t done[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -565,7 +569,8 @@ rnntg_status rnntg_model_destroy(rnntg_model_t h) {
   for (Scratch* s : {&h->enc, &h->pe, &h->splits, &h->tok, &h->len, &h->score, &h->bp,
                      &h->counters, &h->ctx, &h->out_tok, &h->out_splits, &h->logits,
                      &h->finfo, &h->nodebest, &h->lattice, &h->flag, &h->feat, &h->hid,
-                     &h->hstate, &h->pool})
+                     &h->hstate, &h->pool, &h->fenc, &h->nodectx, &h->ladd_u, &h->ladd_tot,
+                     &h->ladd_narc, &h->ladd_paths, &h->ladd_cells, &h->ladd_pos})
     s->release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -906,6 +911,7 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
     while (G * 2 <= want) G *= 2;
     RNNTG_CUDA_TRY(h->finfo.ensure(sizeof(int32_t) * 4 * (total + B)));
     RNNTG_CUDA_TRY(h->nodebest.ensure(sizeof(double) * (total * K + B)));
+    RNNTG_CUDA_TRY(h->nodectx.ensure(sizeof(int32_t) * (total * K + B)));
     RNNTG_CUDA_TRY(h->flag.ensure(16));
     // Lattice pool: sized so one decode suffices at the measured occupancy
     // (config 3: ~6.3, config 4: ~13 kept arcs per stream-frame against
@@ -946,6 +952,7 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
         // per-(stream, frame) and per-node tables are indexed (frame offset + stream index)
         a.lat_frame_info = h->finfo.as<int32_t>() + 4 * static_cast<int64_t>(b0);
         a.node_best = h->nodebest.as<double>() + b0;
+        a.node_ctx = h->nodectx.as<int32_t>() + b0;
         return rnntg::launch_decode_fsa(a, cs);
       });
       if (st) return st;
@@ -987,7 +994,10 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
     }
   }
   st = finish(h, fs, B, out_mem, out_splits, out_tokens, out_scores, launches);
-  if (st == RNNTG_OK) h->last_fsa_fs.assign(fs, fs + B + 1);
+  if (st == RNNTG_OK) {
+    h->last_fsa_fs.assign(fs, fs + B + 1);
+    h->last_fsa_K = std::min(p->max_states, rnntg::kFsaMaxStates);
+  }
   return st;
 }
 
@@ -1044,6 +1054,105 @@ rnntg_status rnntg_fsa_lattice(rnntg_model_t h, int32_t s, int32_t* num_nodes, i
     label[k] = 0;
     score[k] = 0.0;
   }
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_fsa_lattice_best(rnntg_model_t h, int32_t merge_op, int32_t nbest_n, uint64_t seed,
+                                    int32_t* out_splits, int32_t* out_tokens, double* out_logprob) {
+  if (!h || !out_splits) return invalid("null argument");
+  if (merge_op != RNNTG_MERGE_LOG_ADD)
+    return invalid("rnntg_fsa_lattice_best: kMax best sequences are rnntg_fsa_beam_search's own output");
+  if (nbest_n < 1) return invalid("nbest_n must be >= 1");  // fsa_search.hpp:411
+  if (nbest_n > 1024) {
+    set_error("nbest_n > 1024 is beyond this build's per-stream path cap");
+    return RNNTG_UNSUPPORTED;
+  }
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->last_fsa_fs.empty()) return invalid("no fsa_beam_search has run on this handle");
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  const std::vector<int32_t>& fs = h->last_fsa_fs;
+  const int32_t B = static_cast<int32_t>(fs.size()) - 1;
+  const int64_t total = fs[B];
+  int32_t tmax = 0;
+  for (int32_t i = 0; i < B; ++i) tmax = std::max(tmax, fs[i + 1] - fs[i]);
+  const int32_t K = h->last_fsa_K;
+  out_splits[0] = 0;
+  if (B == 0) return RNNTG_OK;
+  // DetRng(seed).uniform01() stream: nbest paths x (T + 2) draws (every
+  // complete path of these layered lattices visits T + 2 states).
+  const int64_t nu = static_cast<int64_t>(nbest_n) * (tmax + 2);
+  if (h->ladd_seed != seed || h->ladd_n < nu) {
+    RNNTG_CUDA_TRY(h->ladd_u.ensure(sizeof(double) * nu));
+    RNNTG_CUDA_TRY(rnntg::launch_mt19937_64_uniforms(seed, nu, h->ladd_u.as<double>(), h->stream));
+    h->ladd_seed = seed;
+    h->ladd_n = nu;
+  }
+  RNNTG_CUDA_TRY(h->splits.ensure(sizeof(int32_t) * (B + 1)));
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(h->splits.ptr, fs.data(), sizeof(int32_t) * (B + 1), cudaMemcpyHostToDevice,
+                                 h->stream));
+  RNNTG_CUDA_TRY(h->ladd_tot.ensure(sizeof(double) * (total * K + B)));
+  RNNTG_CUDA_TRY(h->ladd_narc.ensure(sizeof(int2) * (total * K + B)));
+  RNNTG_CUDA_TRY(h->ladd_paths.ensure(sizeof(int32_t) * nbest_n * (total + B)));
+  RNNTG_CUDA_TRY(h->ladd_pos.ensure(sizeof(int32_t) * B * rnntg::kLogAddWarps * 3 * (tmax + 2)));
+  RNNTG_CUDA_TRY(h->tok.ensure(sizeof(int32_t) * std::max<int64_t>(1, total)));
+  RNNTG_CUDA_TRY(h->len.ensure(sizeof(int32_t) * B));
+  RNNTG_CUDA_TRY(h->score.ensure(sizeof(double) * B));
+  RNNTG_CUDA_TRY(h->flag.ensure(16));
+  for (int attempt = 0;; ++attempt) {
+    RNNTG_CUDA_TRY(h->ladd_cells.ensure(sizeof(double) * B * rnntg::kLogAddWarps * 2 * h->ladd_cell_cap));
+    RNNTG_CUDA_TRY(cudaMemsetAsync(h->flag.ptr, 0, 16, h->stream));
+    rnntg::LogAddArgs a{};
+    a.B = B;
+    a.V = h->d.V;
+    a.K = K;
+    a.nbest = nbest_n;
+    a.frame_splits = h->splits.as<int32_t>();
+    a.lattice = h->lattice.ptr;
+    a.lat_frame_info = h->finfo.as<int32_t>();
+    a.node_ctx = h->nodectx.as<int32_t>();
+    a.uniforms = h->ladd_u.as<double>();
+    a.tot = h->ladd_tot.as<double>();
+    a.node_arcs = h->ladd_narc.as<int2>();
+    a.paths = h->ladd_paths.as<int32_t>();
+    a.cells = h->ladd_cells.as<double>();
+    a.pos = h->ladd_pos.as<int32_t>();
+    a.cell_cap = h->ladd_cell_cap;
+    a.tmax = tmax;
+    a.tokens = h->tok.as<int32_t>();
+    a.lengths = h->len.as<int32_t>();
+    a.logprob = h->score.as<double>();
+    a.error_flag = h->flag.as<int32_t>();
+    RNNTG_CUDA_TRY(rnntg::launch_lattice_logadd(a, h->stream));
+    int32_t flag = 0;
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(&flag, h->flag.ptr, sizeof(flag), cudaMemcpyDeviceToHost, h->stream));
+    RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (flag == 0) break;
+    if (attempt >= 6) {
+      set_error("log-add product DP scratch could not be sized");
+      return RNNTG_INTERNAL;
+    }
+    h->ladd_cell_cap *= 4;  // a layer of the intersection held more cells: regrow and rerun
+  }
+  std::vector<int32_t> lens(B);
+  RNNTG_CUDA_TRY(cudaMemcpy(lens.data(), h->len.ptr, sizeof(int32_t) * B, cudaMemcpyDeviceToHost));
+  for (int32_t i = 0; i < B; ++i) out_splits[i + 1] = out_splits[i] + lens[i];
+  const int64_t ntok = out_splits[B];
+  if (ntok > 0) {
+    if (!out_tokens) return invalid("out_tokens is null");
+    RNNTG_CUDA_TRY(h->out_splits.ensure(sizeof(int32_t) * (B + 1)));
+    RNNTG_CUDA_TRY(h->out_tok.ensure(sizeof(int32_t) * ntok));
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(h->out_splits.ptr, out_splits, sizeof(int32_t) * (B + 1),
+                                   cudaMemcpyHostToDevice, h->stream));
+    compact_tokens_kernel<<<B, 128, 0, h->stream>>>(h->tok.as<int32_t>(), h->splits.as<int32_t>(),
+                                                    h->out_splits.as<int32_t>(), B, 1, h->out_tok.as<int32_t>());
+    RNNTG_CUDA_TRY(cudaGetLastError());
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(out_tokens, h->out_tok.ptr, sizeof(int32_t) * ntok, cudaMemcpyDeviceToHost,
+                                   h->stream));
+  }
+  if (out_logprob)
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(out_logprob, h->score.ptr, sizeof(double) * B, cudaMemcpyDeviceToHost,
+                                   h->stream));
+  RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
   return RNNTG_OK;
 }
 

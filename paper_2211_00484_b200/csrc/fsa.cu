@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
                double beam, int32_t max_states,
                int32_t max_contexts, LatArc* __restrict__ lat, int64_t lat_cap,
                unsigned long long* __restrict__ lat_count, int4* __restrict__ finfo,
-               double* __restrict__ nodebest, int32_t* __restrict__ tokens,
+               double* __restrict__ nodebest, int32_t* __restrict__ node_ctx, int32_t* __restrict__ tokens,
                int32_t* __restrict__ lengths, double* __restrict__ scores,
                unsigned long long* __restrict__ counters, int32_t* __restrict__ error_flag) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   int32_t tmax = 0;
   for (int i = 0; i < ns; ++i) tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
   if (have && grp.tid == 0) {  // init_streams (95-120): ((0,0), state 0, 0.0, node 0)
+    node_ctx[nbase] = 0;
     S.n_act = 1;
     S.num_nodes = 1;
     S.act_ctx[0] = 0;
@@ -676,6 +677,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       grp.sync();
       // New active set, sorted by (ctx, state).
       if (my_rank >= 0) {
+        node_ctx[nbase + S.num_nodes + my_rank] = my_ctx;
         S.act_ctx[my_rank] = my_ctx;
         S.act_state[my_rank] = my_state;
         S.act_score[my_rank] = my_score;
@@ -854,7 +856,7 @@ cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s) {
   fsa_kernel<<<grid, kDecodeThreads, smem, s>>>(
       m, a.pe, a.frame_splits, a.B, G, bk, static_cast<const ArcRec*>(a.graph_arcs), a.graph_splits,
       a.graph_maxw, a.fsa_beam, a.max_states, a.max_contexts, static_cast<LatArc*>(a.lattice), a.lattice_cap,
-      a.lattice_count, reinterpret_cast<int4*>(a.lat_frame_info), a.node_best, a.tokens, a.lengths,
+      a.lattice_count, reinterpret_cast<int4*>(a.lat_frame_info), a.node_best, a.node_ctx, a.tokens, a.lengths,
       a.scores, a.counters, a.error_flag);
   return cudaGetLastError();
 }

@@ -135,6 +135,7 @@ struct DecodeArgs {
   unsigned long long* lattice_count; // device arc pool bump counter
   int32_t* lat_frame_info;  // device int4 per (stream, frame): off, count, node base, nodes
   double* node_best;        // device per-node suffix scores (best_path)
+  int32_t* node_ctx;        // device per-node packed context (lattice_to_best_seq(kLogAdd), logadd.cu)
   int32_t* error_flag;      // device
 };
 
@@ -146,6 +147,31 @@ bool greedy_cluster_fits(const DeviceModel& d, int32_t B);
 cudaError_t launch_decode_greedy_cluster(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s);
+
+// lattice_to_best_seq(kLogAdd) (fsa_search.hpp:410-425) on the device
+// lattices of the last FSA decode (logadd.cu).
+struct LogAddArgs {
+  int32_t B, V, K, nbest;
+  const int32_t* frame_splits;   // device [B+1]
+  const void* lattice;           // device LatArc pool
+  const int32_t* lat_frame_info; // device int4 per (stream, frame)
+  const int32_t* node_ctx;       // device, indexed like node_best
+  const double* uniforms;        // device [nbest * (Tmax + 2)]: DetRng(seed).uniform01() in order
+  double* tot;                   // scratch, indexed like node_best: log-semiring suffix totals
+  int2* node_arcs;               // scratch, indexed like node_best: {first arc, count} (-1: the super-final hop)
+  int32_t* paths;                // scratch [nbest * (sum T + B)] sampled blank-free label sequences
+  double* cells;                 // scratch [B * kLogAddWarps * 2 * cell_cap] DP layers
+  int32_t* pos;                  // scratch [B * kLogAddWarps * 3 * (Tmax + 2)] sorted positions
+  int64_t cell_cap;
+  int32_t tmax;
+  int32_t* tokens;               // device [sum T]: best sequence at frame_splits[i]
+  int32_t* lengths;              // device [B]
+  double* logprob;               // device [B]: its total log-probability (-inf: no path)
+  int32_t* error_flag;           // device: 1 = cell scratch too small
+};
+constexpr int kLogAddWarps = 8;
+cudaError_t launch_mt19937_64_uniforms(uint64_t seed, int64_t n, double* out, cudaStream_t s);
+cudaError_t launch_lattice_logadd(const LogAddArgs& a, cudaStream_t s);
 int decode_num_sms(int device);
 int decode_num_sms_current();
 

@@ -81,6 +81,41 @@ def test_config3_fsa_trivial_512x500():
     _assert_texts(texts, wtexts, "config 3")
 
 
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_config34_logadd_best_sequences(cfg):
+    """lattice_to_best_seq(kLogAdd, nbest 100, seeds 0 and 7) of config 3 / 4
+    at full shape on the GPU, every stream compared against the reference's
+    own function on its own lattices: identical sequences, bit-equal
+    sequence totals."""
+    from oracle.py_oracle import synthetic_arpa
+    from paper_2211_00484_b200.api import Decoder, FsaParams, Graph
+
+    if cfg == 3:
+        B, bias, seed0, params, step = 512, 0.4, 30000, (4.0, 8, 4), 1
+    else:
+        B, bias, seed0, params, step = 256, -1.4, 40000, (8.0, 64, 8), 1
+    m = H.model(V=500, seed=0, blank_bias=bias)
+    feats, enc, splits = H.frames(m, [500] * B, seed0=seed0)
+    rg = H.ref().graph_trivial(500) if cfg == 3 else H.ref().graph_from_arpa(synthetic_arpa(500), 500)
+    dec = Decoder(H.api_weights(m.w))
+    try:
+        g = Graph.trivial(dec) if cfg == 3 else Graph(dec, rg.g.num_states, rg.g.arc_splits, rg.g.dst, rg.g.label,
+                                                      rg.g.weight)
+        dec.fsa_beam_search(enc, splits, g, FsaParams(*params))
+        got = {seed: dec.fsa_lattice_best(nbest=100, seed=seed) for seed in (0, 7)}
+    finally:
+        dec.close()
+    pick = np.arange(0, B, step)
+    T = 500
+    f_pick = np.concatenate([feats[i * T : (i + 1) * T] for i in pick])
+    s_pick = (np.arange(len(pick) + 1) * T).astype(np.int32)
+    for seed in (0, 7):
+        want, wlp = m.fsa_logadd(f_pick, s_pick, rg, *params, nbest=100, seed=seed, threads=THREADS)
+        toks, lp = got[seed]
+        _assert_tokens([toks[i] for i in pick], want, f"config {cfg} log-add seed {seed}")
+        H.assert_scores_equal(lp[pick], wlp)
+
+
 def test_config4_fsa_ngram_256x500():
     from oracle.py_oracle import synthetic_arpa
     from paper_2211_00484_b200.api import Decoder, FsaParams, Graph

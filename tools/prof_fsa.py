@@ -55,6 +55,14 @@ for r in range(reps):
     torch.cuda.synchronize()
     ms.append(e0.elapsed_time(e1))
 st = dec.stats()
+lms = []
+for seed in (0, 7):  # lattice_to_best_seq(kLogAdd, 100, seed) on the device lattices
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    dec.fsa_lattice_best(nbest=100, seed=seed)
+    e1.record()
+    torch.cuda.synchronize()
+    lms.append(e0.elapsed_time(e1))
 sf = st["stream_frames"]
 best = min(ms)
 dec_ms = st["decode_ms"]
@@ -66,7 +74,7 @@ ph = st["phase_cycles"]
 tot = sum(ph[:3]) or 1
 print(json.dumps(dict(
     config=cfg, B=B, T=T, params=[params.beam, params.max_states, params.max_contexts], graph_arcs=arcs_in_graph,
-    call_ms=ms, decode_ms=dec_ms, frames_per_s=B * T / (best * 1e-3),
+    call_ms=ms, decode_ms=dec_ms, frames_per_s=B * T / (best * 1e-3), logadd_best_ms=lms,
     rows_per_sf=st["joiner_rows"] / sf, arcs_per_sf=st["arcs_expanded"] / sf,
     lattice_arcs_per_sf=st["lattice_arcs"] / sf, tokens_per_frame=int(osp[-1]) / (B * T),
     joiner_tflops=flops / (dec_ms * 1e-3) / 1e12,
