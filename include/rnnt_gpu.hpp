@@ -247,6 +247,26 @@ inline std::vector<std::vector<int32_t>> fsa_best_sequences(
   return detail::unpack(splits, toks);
 }
 
+// fsa_beam_search followed by lattice_to_best_seq(method, nbest_n, seed)
+// for every stream (fsa_search.hpp:394-426; the CLI's decode with --merge,
+// rnnt_main.cpp:302): kMax is the search's own best path, kLogAdd runs the
+// n-best sampling / dedup / per-sequence totals on the GPU lattices.
+inline std::vector<std::vector<int32_t>> fsa_best_sequences(
+    Context& ctx, const ToyTransducer& m, const std::vector<Mat<float>>& batch,
+    const Fsa& graph, const FsaSearchParams& params, MergeOp method, int32_t nbest_n = 100,
+    uint64_t seed = 0) {
+  if (method == MergeOp::kMax) return fsa_best_sequences(ctx, m, batch, graph, params);
+  if (nbest_n < 1) throw ValidationError("nbest_n must be >= 1");
+  fsa_best_sequences(ctx, m, batch, graph, params);
+  const int32_t B = static_cast<int32_t>(batch.size());
+  int64_t total = 0;
+  for (const Mat<float>& x : batch) total += x.rows;
+  std::vector<int32_t> splits(B + 1), toks(std::max<int64_t>(1, total));
+  check(rnntg_fsa_lattice_best(ctx.handle(), RNNTG_MERGE_LOG_ADD, nbest_n, seed, splits.data(), toks.data(),
+                               nullptr));
+  return detail::unpack(splits, toks);
+}
+
 // fsa_beam_search (fsa_search.hpp:326-387) with the reference's signature
 // and return type: one lattice per stream, node numbering and arc order as
 // build_lattice + make_fsa produce them.  Streams sharing a graph (by

@@ -82,6 +82,15 @@ int main() {
         ++bad;
       }
   }
+  // ... and computed on the GPU (rnntg_fsa_lattice_best)
+  for (uint64_t seed : {0ull, 7ull}) {
+    auto gl = gpu::fsa_best_sequences(ctx, m, batch, g, fp, MergeOp::kLogAdd, 100, seed);
+    for (size_t i = 0; i < batch.size(); ++i)
+      if (gl[i] != lattice_to_best_seq(lats[i], MergeOp::kLogAdd, 100, seed)) {
+        std::printf("GPU log-add mismatch %zu seed %llu\n", i, static_cast<unsigned long long>(seed));
+        ++bad;
+      }
+  }
   // greedy_search with S = 3 and S unlimited (search.hpp:76-100)
   for (int32_t S : {3, kNoSymbolLimit}) {
     int64_t gcap = 0;
