@@ -50,6 +50,9 @@ struct rnntg_model_s {
   // Small-batch greedy on thread-block clusters (cluster.cu);
   // RNNTG_GREEDY_CLUSTER=0 disables.
   bool greedy_cluster = true;
+  // Small-batch beam search on thread-block clusters (decode.cu);
+  // RNNTG_BEAM_CLUSTER=0 disables.
+  bool beam_cluster = true;
   int32_t slot_mult = 1;  // token slots per frame of the current call (greedy S > 1)
   Scratch enc, pe, splits, tok, len, score, bp, counters, ctx, out_tok, out_splits, logits;
   Scratch finfo, nodebest, lattice, flag, feat, hid, fenc;
@@ -482,6 +485,7 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
   if (const char* e = std::getenv("RNNTG_SLICE_OVERLAP")) h->slice_overlap = std::atoi(e);
   if (const char* e = std::getenv("RNNTG_SLICE_THROTTLE")) h->slice_throttle = std::atoi(e);
   if (const char* gc = std::getenv("RNNTG_GREEDY_CLUSTER")) h->greedy_cluster = std::atoi(gc) != 0;
+  if (const char* bc = std::getenv("RNNTG_BEAM_CLUSTER")) h->beam_cluster = std::atoi(bc) != 0;
   rnntg::DeviceModel& d = h->d;
   d.V = V;
   d.D = D;
@@ -791,6 +795,18 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       a.joiner_bf16 = h->joiner_mode == RNNTG_JOINER_BF16;
       return a;
     };
+    // Small batches: the thread-block-cluster kernel (out_w column slices
+    // resident in shared memory, decode.cu beam_cluster_kernel), one launch.
+    const int Gc = exact && h->beam_cluster ? rnntg::beam_cluster_streams(h->d, B, p->beam_size, h->num_sms) : 0;
+    if (Gc > 0) {
+      st = run_pipeline(h, enc, fs, B, mem, B, &launches, [&](int32_t b0, int32_t b1, cudaStream_t cs) {
+        rnntg::DecodeArgs a = args(b0, b1);
+        a.streams_per_cta = Gc;  // streams per cluster
+        return rnntg::launch_decode_beam_cluster(a, cs);
+      });
+      if (st) return st;
+      return finish(h, fs, B, out_mem, out_splits, out_tokens, out_scores, launches);
+    }
     const bool sliced = exact && uniform && fs[1] - fs[0] > h->slice_first &&
                         ((mem == RNNTG_MEM_HOST && h->sliced > 0) || (mem == RNNTG_MEM_DEVICE && h->sliced > 1));
     if (sliced) {

@@ -26,6 +26,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "decode_common.cuh"
 
 namespace rnntg {
@@ -1346,6 +1348,325 @@ cudaError_t launch_beam_multi(const DecodeArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Small-batch modified beam search on thread-block clusters (beam_search at
+// S = 1, search.hpp:206-277).  With fewer streams than a
+// few per SM the persistent kernel is latency bound: each SM streams all of
+// out_w (1 MB) from L2 per frame for ~4 joiner rows and pays the fixed
+// per-frame phases (h build, exact normaliser chain, beam step) for one or
+// two streams.  Here a cluster of kBc = 8 CTAs serves G <= 64 / beam
+// streams:
+//  - CTA c keeps out_w columns [64c, 64c+64) resident in shared memory for
+//    the whole utterance (no weight traffic after the first frame);
+//  - every CTA builds the h rows of the cluster's joiner rows (<= 64, in
+//    passes of 32) and computes its column slice of their logits (thread =
+//    column x 4 rows, sequential FMUL/FADD in k, the reference's order);
+//  - row r's slices are pushed into CTA (r mod 8)'s shared memory (DSMEM),
+//    which reduces it: exact normaliser (lse_cta_exps / lse_cta_chain) with
+//    the top-`beam` tokens picked meanwhile, results pushed to CTA 0;
+//  - CTA 0 runs the beam steps (warp per stream: the persistent kernel's
+//    beam_stream_step) and the next frame's rows; the others read the row
+//    table back through DSMEM.
+// Three cluster barriers per frame.  Same arithmetic as the persistent
+// kernel (identical tokens, bit-equal scores).
+// ---------------------------------------------------------------------------
+constexpr int kBc = 8;            // CTAs per cluster (portable maximum)
+constexpr int kBcCols = 64;       // out_w columns per CTA (Vp = 512)
+constexpr int kBcRows = 64;       // joiner rows per cluster frame
+constexpr int kBcPass = 32;       // rows per h / GEMM pass
+constexpr int kBcLocal = kBcRows / kBc;  // rows reduced per CTA
+
+struct BcSmem {
+  uint64_t etab[256];
+  unsigned long long stat[8];
+  int32_t R;
+  int64_t row_pe[kBcRows];
+  int32_t row_ctx[kBcRows];
+  // CTA 0: every row's reduction results (the beam steps' RowRes)
+  double row_lse[kBcRows];
+  float row_l0[kBcRows];
+  float row_tl[kBcRows][kMaxBeam];
+  int32_t row_tk[kBcRows][kMaxBeam];
+  // the rows this CTA reduces (local index r / kBc)
+  double loc_lse[kBcLocal];
+  float loc_l0[kBcLocal];
+  float loc_tl[kBcLocal][kMaxBeam];
+  int32_t loc_tk[kBcLocal][kMaxBeam];
+  float loc_m[kBcLocal];
+};
+
+template <int BCAP>
+__global__ void __launch_bounds__(kDecodeThreads, 1)
+    beam_cluster_kernel(ModelView m, const float* __restrict__ pe, const int32_t* __restrict__ frame_splits,
+                        int32_t B, int32_t G, int32_t beam, int32_t merge_log, int32_t length_norm,
+                        int32_t max_total, uint32_t* __restrict__ backptr, int32_t* __restrict__ tokens,
+                        int32_t* __restrict__ lengths, double* __restrict__ scores,
+                        unsigned long long* __restrict__ counters) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int cl = blockIdx.x / kBc;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* Ws = reinterpret_cast<float*>(smem_raw);      // [J][64] k-major out_w slice
+  float* Hs = Ws + m.J * kBcCols;                      // [J][32] k-major h rows (scratch after the GEMM)
+  float* recv = Hs + m.J * kBcPass;                    // [kBcLocal][Vp] logits of the rows reduced here
+  BcSmem& S = *reinterpret_cast<BcSmem*>(recv + kBcLocal * m.Vp);
+  Hyps* H = reinterpret_cast<Hyps*>(&S + 1);            // CTA 0: [G]
+  BcSmem& S0 = *cluster.map_shared_rank(&S, 0);
+  constexpr int kCandPerStream = BCAP * BCAP + 2 * BCAP;
+  BeamCand* C = reinterpret_cast<BeamCand*>(Hs);       // CTA 0, during the beam steps
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s0 = cl * G;
+  const int ns = max(0, min(G, B - s0));
+  const int c0 = rank * kBcCols;
+  for (int x = threadIdx.x; x < m.J * kBcCols; x += kDecodeThreads) {
+    const int k = x / kBcCols, c = x - k * kBcCols;
+    Ws[x] = m.out_wt[static_cast<int64_t>(k) * m.Vp + c0 + c];
+  }
+  load_exp_table(S.etab);
+  if (threadIdx.x < 8) S.stat[threadIdx.x] = 0;
+  int32_t tmax = 0;
+  for (int i = 0; i < ns; ++i) tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
+  if (rank == 0) {
+    for (int i = threadIdx.x; i < ns; i += kDecodeThreads) {
+      Hyps& h = H[i];
+      h.nh = 1;
+      h.score[0] = 0.0;
+      h.ctx[0] = 0;
+      h.len[0] = 0;
+      h.last[0] = -1;
+      h.h1[0] = 0x243f6a8885a308d3ull;
+      h.h2[0] = 0x13198a2e03707344ull;
+      h.p1[0] = h.p2[0] = 0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int R0 = beam_rows(H, ns, frame_splits + s0, 0, S.row_pe, S.row_ctx);
+      if (lane == 0) S.R = R0;
+    }
+  }
+  cluster.sync();
+  const RowRes rr0{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
+  const RowRes rloc{S.loc_lse, S.loc_l0, S.loc_tl, S.loc_tk};
+  long long ph[4] = {0, 0, 0, 0};  // thread 0: h + GEMM + push, reduce, beam step, cluster-barrier waits
+  for (int32_t t = 0; t < tmax; ++t) {
+    const long long ca = clock64();
+    // row table from CTA 0
+    if (rank != 0) {
+      if (threadIdx.x == 0) S.R = S0.R;
+      for (int r = threadIdx.x; r < kBcRows; r += kDecodeThreads) {
+        S.row_pe[r] = S0.row_pe[r];
+        S.row_ctx[r] = S0.row_ctx[r];
+      }
+    }
+    __syncthreads();
+    const int R = S.R;
+    // the next frame's encoder projections (one row per live stream) into L2
+    for (int i = threadIdx.x; i < ns; i += kDecodeThreads) {
+      const int32_t f = frame_splits[s0 + i];
+      if (t + 1 < frame_splits[s0 + i + 1] - f)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pe + static_cast<int64_t>(f + t + 1) * m.J + c0));
+    }
+    // h rows and this CTA's column slice of their logits, 32 rows a pass.
+    // h: CTA c builds k in [64c, 64c+64) of every row of the pass (unit = 4
+    // rows at one k: scalar gathers, four tanhf, one 16-byte store into each
+    // CTA's Hs) -- the gathers and tanhf are split 8 ways, not replicated.
+    // Hs slot of pass row lr: (lr % 8) * 4 + lr / 8, so thread group q's
+    // rows q, q+8, q+16, q+24 are one 16-byte load.  GEMM: thread = column
+    // c x group q (all 16 warps busy for R >= 8); row r's logit slice goes
+    // to CTA r % 8 (local row r / 8).
+    const int c = threadIdx.x & (kBcCols - 1), q = threadIdx.x / kBcCols;
+    for (int p0 = 0; p0 < R; p0 += kBcPass) {
+      const int Rp = min(kBcPass, R - p0);
+      if (p0 > 0) cluster.sync();  // every CTA is done reading the previous pass's Hs
+      {
+        const int units = kBcCols * min(8, Rp);  // (k, slot group g: rows g, g+8, g+16, g+24)
+        for (int x = threadIdx.x; x < units; x += kDecodeThreads) {
+          const int g = x / kBcCols, kk = c0 + (x - g * kBcCols);  // slots 4g .. 4g+3
+          float v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int lr = (4 * g + j) % 4 * 8 + (4 * g + j) / 4;  // slot -> pass row
+            if (lr < Rp) {
+              const int r = p0 + lr;
+              v[j] = fadd(fadd(pe[S.row_pe[r] * m.J + kk], m.pd[static_cast<int64_t>(S.row_ctx[r]) * m.J + kk]),
+                          m.j_b[kk]);
+            } else {
+              v[j] = 0.0f;
+            }
+          }
+          float z[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) z[j] = rnntg_exact::tanhf_main(v[j]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (!rnntg_exact::tanhf_main_path(v[j])) z[j] = rnntg_exact::tanhf_glibc(v[j]);
+          const float4 z4 = make_float4(z[0], z[1], z[2], z[3]);
+#pragma unroll
+          for (int d = 0; d < kBc; ++d)
+            *reinterpret_cast<float4*>(cluster.map_shared_rank(Hs, d) + kk * kBcPass + 4 * g) = z4;
+        }
+      }
+      cluster.sync();  // every h piece in place
+      if (threadIdx.x == 0) S.stat[5] += clock64() - ca;
+      const int nr = q < Rp ? (Rp - q + 7) / 8 : 0;  // rows q, q+8, ... of this pass
+      if (nr > 0) {
+        float acc[4];
+        const float bias = m.out_b[c0 + c];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = bias;
+        const float* hq = Hs + 4 * q;
+        if (nr == 4) {
+#pragma unroll 4
+          for (int k = 0; k < m.J; ++k) {
+            const float w = Ws[k * kBcCols + c];
+            const float4 h4 = *reinterpret_cast<const float4*>(hq + k * kBcPass);
+            acc[0] = fadd(acc[0], fmul(w, h4.x));
+            acc[1] = fadd(acc[1], fmul(w, h4.y));
+            acc[2] = fadd(acc[2], fmul(w, h4.z));
+            acc[3] = fadd(acc[3], fmul(w, h4.w));
+          }
+        } else if (nr == 3) {
+#pragma unroll 4
+          for (int k = 0; k < m.J; ++k) {
+            const float w = Ws[k * kBcCols + c];
+            const float4 h4 = *reinterpret_cast<const float4*>(hq + k * kBcPass);
+            acc[0] = fadd(acc[0], fmul(w, h4.x));
+            acc[1] = fadd(acc[1], fmul(w, h4.y));
+            acc[2] = fadd(acc[2], fmul(w, h4.z));
+          }
+        } else if (nr == 2) {
+#pragma unroll 4
+          for (int k = 0; k < m.J; ++k) {
+            const float w = Ws[k * kBcCols + c];
+            const float2 h2 = *reinterpret_cast<const float2*>(hq + k * kBcPass);
+            acc[0] = fadd(acc[0], fmul(w, h2.x));
+            acc[1] = fadd(acc[1], fmul(w, h2.y));
+          }
+        } else {
+#pragma unroll 4
+          for (int k = 0; k < m.J; ++k) acc[0] = fadd(acc[0], fmul(Ws[k * kBcCols + c], hq[k * kBcPass]));
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j < nr) {
+            const int r = p0 + q + 8 * j;
+            float* dst = cluster.map_shared_rank(recv, r % kBc);
+            dst[(r / kBc) * m.Vp + c0 + c] = acc[j];
+          }
+        }
+      }
+    }
+    const long long cb = clock64();
+    if (threadIdx.x == 0) S.stat[6] += cb - ca;
+    cluster.sync();  // every slice delivered
+    const long long cc = clock64();
+    // reduce the rows r = rank + 8 i
+    const int nloc = R > rank ? (R - rank + kBc - 1) / kBc : 0;
+    double* E = reinterpret_cast<double*>(Hs);
+    lse_cta_exps(recv, E, kBcPass * m.J / 2, m.Vp, m.V, nloc, S.etab, S.loc_m);
+    if (warp == 0) {
+      lse_cta_chain(recv, E, kBcPass * m.J / 2, m.Vp, m.V, nloc, S.loc_m, S.loc_lse, S.loc_l0);
+    } else if (warp - 1 < nloc) {
+      beam_row_reduce_n<BCAP, 1, false>(recv, m.Vp, m.V, beam, warp - 1, nloc, rloc, S.etab);
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < nloc * (2 + 2 * kMaxBeam); x += kDecodeThreads) {
+      const int i = x / (2 + 2 * kMaxBeam), f = x - i * (2 + 2 * kMaxBeam);
+      const int r = rank + kBc * i;
+      if (f == 0) S0.row_lse[r] = S.loc_lse[i];
+      else if (f == 1) S0.row_l0[r] = S.loc_l0[i];
+      else if (f < 2 + kMaxBeam) S0.row_tl[r][f - 2] = S.loc_tl[i][f - 2];
+      else S0.row_tk[r][f - 2 - kMaxBeam] = S.loc_tk[i][f - 2 - kMaxBeam];
+    }
+    const long long cd = clock64();
+    cluster.sync();  // every row reduced
+    const long long ce = clock64();
+    if (rank == 0) {
+      for (int i = warp; i < ns; i += kWarps) {
+        const int32_t fs = frame_splits[s0 + i];
+        const int32_t T = frame_splits[s0 + i + 1] - fs;
+        if (t >= T) continue;
+        beam_stream_step<BCAP>(m, H[i], C + static_cast<int64_t>(i) * kCandPerStream,
+                               backptr + static_cast<int64_t>(fs + s0 + i) * kMaxBeam, t, T, fs, beam, merge_log,
+                               length_norm, max_total, rr0, tokens, lengths + s0 + i, scores + s0 + i, &S.stat[4]);
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const int Rn = beam_rows(H, ns, frame_splits + s0, t + 1, S.row_pe, S.row_ctx);
+        if (lane == 0) {
+          S.R = Rn;
+          S.stat[1] += R;
+        }
+        // the next frame's decoder-table rows into L2 (each CTA gathers a
+        // 256-byte segment of every row): a head start on the h build
+        for (int x = lane; x < Rn * (m.J / 32); x += 32) {
+          const int r = x / (m.J / 32), l = x - r * (m.J / 32);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(m.pd + static_cast<int64_t>(S.row_ctx[r]) * m.J + l * 32));
+        }
+      }
+    }
+    const long long cf = clock64();
+    cluster.sync();  // next frame's rows published
+    if (threadIdx.x == 0) {
+      ph[0] += cb - ca;
+      ph[1] += cd - cc;
+      ph[2] += cf - ce;
+      ph[3] += (cc - cb) + (ce - cd) + (clock64() - cf);
+    }
+  }
+  // Zero-frame streams: empty result, score 0.
+  if (rank == 0)
+    for (int i = threadIdx.x; i < ns; i += kDecodeThreads)
+      if (frame_splits[s0 + i + 1] == frame_splits[s0 + i]) {
+        lengths[s0 + i] = 0;
+        scores[s0 + i] = 0.0;
+      }
+  if (rank == 0 && threadIdx.x == 0) {
+    unsigned long long sf = 0;
+    for (int i = 0; i < ns; ++i) sf += frame_splits[s0 + i + 1] - frame_splits[s0 + i];
+    atomicAdd(&counters[0], sf);
+    atomicAdd(&counters[1], S.stat[1]);
+    atomicAdd(&counters[4], S.stat[4]);
+    for (int i = 0; i < 4; ++i) atomicAdd(&counters[8 + i], static_cast<unsigned long long>(ph[i]));
+    atomicAdd(&counters[6], S.stat[5]);  // h build (diagnostic, gather_cycles slot)
+  }
+  cluster.sync();  // no CTA leaves while others may still read its shared memory
+}
+
+template <int BCAP>
+size_t beam_cluster_smem(const ModelView& m, int G) {
+  return static_cast<size_t>(m.J) * (kBcCols + kBcPass) * 4 + static_cast<size_t>(kBcLocal) * m.Vp * 4 +
+         sizeof(BcSmem) + sizeof(Hyps) * G;
+}
+
+template <int BCAP>
+cudaError_t launch_beam_cluster_cap(const DecodeArgs& a, cudaStream_t s) {
+  const ModelView m = view_of(*a.m);
+  const int G = a.streams_per_cta;
+  const int nclusters = (a.B + G - 1) / G;
+  const size_t smem = beam_cluster_smem<BCAP>(m, G);
+  cudaError_t e = cudaFuncSetAttribute(beam_cluster_kernel<BCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nclusters * kBc, 1, 1);
+  cfg.blockDim = dim3(kDecodeThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kBc;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, beam_cluster_kernel<BCAP>, m, a.pe, a.frame_splits, a.B, G, a.beam_size,
+                            a.merge_op, a.length_norm, a.max_total, a.backptr, a.tokens, a.lengths, a.scores,
+                            a.counters);
+}
+
 }  // namespace
 
 int decode_num_sms_current() {
@@ -1420,6 +1741,50 @@ cudaError_t launch_beam_mode(const DecodeArgs& a, cudaStream_t s) {
 // registers); the runtime beam_size selects the smallest capacity >= it.
 // a.joiner_bf16 selects the tcgen05 joiner variant.
 size_t beam_state_bytes() { return sizeof(Hyps); }
+
+int beam_cluster_streams(const DeviceModel& d, int32_t B, int32_t beam_size, int num_sms) {
+  // streams per cluster when the cluster kernel serves this batch, else 0
+  if (d.Vp != kBc * kBcCols || d.V > kDecodeThreads || B <= 0 || beam_size > kMaxBeam) return 0;
+  // clusters that can be resident at once (8 co-scheduled SMs of one GPC each)
+  static int resident = -1;
+  if (resident < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kBc * 64, 1, 1);
+    cfg.blockDim = dim3(kDecodeThreads, 1, 1);
+    cfg.dynamicSmemBytes = beam_cluster_smem<4>(view_of(d), 16);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kBc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    cudaFuncSetAttribute(beam_cluster_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(cfg.dynamicSmemBytes));
+    if (cudaOccupancyMaxActiveClusters(&n, beam_cluster_kernel<4>, &cfg) != cudaSuccess) n = 0;
+    cudaGetLastError();
+    resident = n > 0 ? n : num_sms / kBc;
+  }
+  const int nmax = std::min(resident, num_sms / kBc);
+  // up to 12 streams a cluster: beyond, the one-CTA beam steps of CTA 0 and
+  // the second h / GEMM pass make the persistent kernel faster (measured:
+  // B = 64 / 128 / 192 / 240 at T = 1000: 27.3 / 31.6 / 38.9 / 49.3 ms
+  // against 33.4 / 33.5 / 40.4 / 40.2 ms)
+  const int gmax = std::min(12, kBcRows / std::max(1, beam_size));
+  if (B > nmax * gmax) return 0;
+  const int G = (B + nmax - 1) / nmax;
+  const ModelView m = view_of(d);
+  const size_t smem = beam_size <= 4 ? beam_cluster_smem<4>(m, G) : beam_cluster_smem<8>(m, G);
+  return smem <= 227 * 1024 ? G : 0;
+}
+
+cudaError_t launch_decode_beam_cluster(const DecodeArgs& a, cudaStream_t s) {
+  if (a.beam_size <= 1) return launch_beam_cluster_cap<1>(a, s);
+  if (a.beam_size <= 2) return launch_beam_cluster_cap<2>(a, s);
+  if (a.beam_size <= 4) return launch_beam_cluster_cap<4>(a, s);
+  return launch_beam_cluster_cap<8>(a, s);
+}
 
 cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s) {
   if (a.symbol_cap > 1) {  // S > 1: sub-steps within a frame

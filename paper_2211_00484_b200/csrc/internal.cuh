@@ -146,6 +146,11 @@ size_t beam_state_bytes();  // per-stream hypothesis set carried between time-sl
 bool greedy_cluster_fits(const DeviceModel& d, int32_t B);
 cudaError_t launch_decode_greedy_cluster(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s);
+// small batches (<= num_sms / 8 * 64 / beam streams): thread-block clusters
+// with out_w column slices resident in shared memory (decode.cu); returns
+// the streams per cluster, or 0 when the batch does not fit
+int beam_cluster_streams(const DeviceModel& d, int32_t B, int32_t beam_size, int num_sms);
+cudaError_t launch_decode_beam_cluster(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s);
 
 // lattice_to_best_seq(kLogAdd) (fsa_search.hpp:410-425) on the device
