@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.cuh"
 
 namespace rnntg {
@@ -82,6 +84,15 @@ struct rnntg_graph_s {
 namespace {
 
 int32_t round_up(int32_t x, int32_t m) { return (x + m - 1) / m * m; }
+
+// NVTX ranges around every C-ABI decode call and its phases (SURVEY.md §5
+// tracing): visible in Nsight Systems / ncu --nvtx without any code change.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 rnntg_status invalid(const std::string& msg) {
   set_error(msg);
@@ -175,6 +186,7 @@ rnntg_status frames_from(rnntg_model_t h, const float*& enc, const int32_t* fs, 
 
 // Common front half of a decode call: buffers, splits, counters.
 rnntg_status prepare(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem) {
+  Nvtx nvtx_range("rnntg: prepare (buffers, splits)");
   const int64_t total = B > 0 ? fs[B] : 0;
   const int32_t D = h->d.D, J = h->d.J;
   RNNTG_CUDA_TRY(h->splits.ensure(sizeof(int32_t) * (B + 1)));
@@ -336,6 +348,7 @@ __global__ void compact_tokens_kernel(const int32_t* __restrict__ slot_tokens,
 rnntg_status finish(rnntg_model_t h, const int32_t* fs, int32_t B, int32_t mem,
                     int32_t* out_splits, int32_t* out_tokens, double* out_scores,
                     int64_t launches) {
+  Nvtx nvtx_range("rnntg: results (compact + read back)");
   RNNTG_CUDA_TRY(cudaEventRecord(h->ev[2], h->stream));
   const int64_t total = B > 0 ? static_cast<int64_t>(fs[B]) * h->slot_mult : 0;
   std::vector<int32_t> lens(std::max(1, B));
@@ -441,6 +454,7 @@ const char* rnntg_version(void) { return "rnntg 0.1 (sm_100a)"; }
 
 rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
                                 rnntg_model_t* out) {
+  Nvtx nvtx_range("rnntg_model_create");
   if (!desc || !out) return invalid("null argument");
   *out = nullptr;
   // check_config (model.hpp:174-182).
@@ -667,6 +681,7 @@ rnntg_status rnntg_greedy_search_batch(rnntg_model_t h, const float* enc,
                                        const int32_t* fs, int32_t B,
                                        int32_t max_symbols, int32_t mem,
                                        int32_t* out_splits, int32_t* out_tokens) {
+  Nvtx nvtx_range("rnntg_greedy_search_batch");
   if (!h) return invalid("null model");
   // search.hpp:110-111.
   if (max_symbols != 1) return invalid("greedy_search_batch supports max_symbols = 1 only");
@@ -681,6 +696,7 @@ rnntg_status rnntg_greedy_search_batch(rnntg_model_t h, const float* enc,
 rnntg_status rnntg_greedy_search(rnntg_model_t h, const float* enc, const int32_t* fs, int32_t B,
                                  int32_t max_symbols, int32_t mem, int32_t* out_splits,
                                  int32_t* out_tokens, int64_t* capped_frames) {
+  Nvtx nvtx_range("rnntg_greedy_search");
   if (!h) return invalid("null model");
   // search.hpp:80 and 31-34 (kNoSymbolLimit -> kMaxSymbolsPerFrameSafety = 10).
   if (max_symbols < 1) return invalid("max_symbols must be >= 1");
@@ -701,6 +717,7 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
                                      const rnntg_beam_params* p, int32_t mem,
                                      int32_t* out_splits, int32_t* out_tokens,
                                      double* out_scores) {
+  Nvtx nvtx_range("rnntg_beam_search_batch");
   if (!h || !p) return invalid("null argument");
   // beam_search validation, search.hpp:210-212.
   if (p->max_symbols < 1) return invalid("max_symbols must be >= 1");
@@ -833,6 +850,7 @@ rnntg_status rnntg_graph_create(rnntg_model_t h, int32_t num_states,
                                 const int32_t* arc_splits, int32_t num_arcs,
                                 const int32_t* dst, const int32_t* label,
                                 const double* weight, rnntg_graph_t* out) {
+  Nvtx nvtx_range("rnntg_graph_create");
   if (!h || !out) return invalid("null argument");
   *out = nullptr;
   if (num_states < 1) return invalid("fsa must have at least one state");
@@ -899,6 +917,7 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
                                    const rnntg_fsa_params* p, int32_t mem,
                                    int32_t* out_splits, int32_t* out_tokens,
                                    double* out_scores) {
+  Nvtx nvtx_range("rnntg_fsa_beam_search");
   if (!h || !p || !graph) return invalid("null argument");
   if (graph->model != h) return invalid("graph belongs to another model handle");
   // check_fsa_search_params, fsa_search.hpp:83-90.
@@ -1075,6 +1094,7 @@ rnntg_status rnntg_fsa_lattice(rnntg_model_t h, int32_t s, int32_t* num_nodes, i
 
 rnntg_status rnntg_fsa_lattice_best(rnntg_model_t h, int32_t merge_op, int32_t nbest_n, uint64_t seed,
                                     int32_t* out_splits, int32_t* out_tokens, double* out_logprob) {
+  Nvtx nvtx_range("rnntg_fsa_lattice_best");
   if (!h || !out_splits) return invalid("null argument");
   if (merge_op != RNNTG_MERGE_LOG_ADD)
     return invalid("rnntg_fsa_lattice_best: kMax best sequences are rnntg_fsa_beam_search's own output");
@@ -1242,6 +1262,7 @@ rnntg_status rnntg_model_set_encoder(rnntg_model_t h, const rnntg_encoder_desc* 
 
 rnntg_status rnntg_encoder_forward(rnntg_model_t h, const float* feats, const int32_t* fs,
                                    int32_t B, int32_t mem, float* enc_out) {
+  Nvtx nvtx_range("rnntg_encoder_forward");
   if (!h) return invalid("null model");
   if (h->d.F == 0) return invalid("no encoder weights (rnntg_model_set_encoder)");
   if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");

@@ -1,6 +1,11 @@
 // Measures the non-fused fp32 multiply+add rate the exact joiner is bound by
 // (FMUL then FADD per MAC, as the reference's sequential affine requires),
 // beside the FFMA rate, on this GPU.  Prints one JSON line.
+//
+// Every fp32 pipe instruction of the timed loop is counted: per iteration 32
+// MACs (64 FMUL/FADD, or 32 FFMA) plus the 4 FADDs that keep the
+// multipliers loop-variant (so ptxas cannot hoist the products).  The
+// instruction rate is what the nominal peak (SMs x 128 lanes x clock) bounds.
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -50,12 +55,15 @@ int main() {
       cudaEventSynchronize(b);
       float ms = 0;
       cudaEventElapsedTime(&ms, a, b);
-      const double macs = double(sms) * 2 * 512 * iters * 32.0;
-      res[f] = macs / (ms * 1e-3);
+      // fp32 pipe instructions: 64 FMUL/FADD (or 32 FFMA) + 4 FADD per iteration
+      const double inst = double(sms) * 2 * 512 * iters * (f ? 36.0 : 68.0);
+      res[f] = inst / (ms * 1e-3);
     }
   }
-  printf("{\"sms\": %d, \"clock_khz_attr\": %d, \"nonfused_mac_per_s\": %.4e, \"ffma_mac_per_s\": %.4e, "
-         "\"nonfused_tflops\": %.3f, \"ffma_tflops\": %.3f}\n",
-         sms, clk, res[0], res[1], 2 * res[0] / 1e12, 2 * res[1] / 1e12);
+  const double nominal = double(sms) * 128 * clk * 1e3;  // fp32 lane-instructions / s at the attribute clock
+  printf("{\"sms\": %d, \"clock_khz_attr\": %d, \"nonfused_fp32_inst_per_s\": %.4e, \"ffma_fp32_inst_per_s\": %.4e, "
+         "\"nominal_fp32_inst_per_s\": %.4e, \"nonfused_tflops\": %.3f, \"nonfused_frac_of_nominal\": %.3f, "
+         "\"ffma_frac_of_nominal\": %.3f}\n",
+         sms, clk, res[0], res[1], nominal, res[0] / 1e12, res[0] / nominal, res[1] / nominal);
   return 0;
 }
