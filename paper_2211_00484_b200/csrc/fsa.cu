@@ -159,9 +159,28 @@ struct Raw {
   double arc_score, score;
 };
 
-__device__ __forceinline__ Raw raw_cand(const FsaStream& S, int q, const ArcRec* __restrict__ arcs,
-                                        const int32_t* __restrict__ splits, const float* L,
-                                        const double* row_lse, int Vp, int V) {
+// Where a candidate's log-probability comes from: the joiner's logits in
+// shared memory and the row's exact normaliser (the decoder), or the
+// caller's log-prob rows (the step API, expand_arcs' plug-in point,
+// fsa_search.hpp:59-61).  lp(row, label) = double(l) - lse, as
+// log_softmax_row writes it (model.hpp:115-125).
+struct LpJoiner {
+  const float* L;
+  const double* lse;
+  int Vp;
+  __device__ __forceinline__ double lp(int row, int label) const {
+    return static_cast<double>(L[static_cast<int64_t>(row) * Vp + label]) - lse[row];
+  }
+};
+struct LpRows {
+  const double* P;
+  int V;
+  __device__ __forceinline__ double lp(int row, int label) const { return P[static_cast<int64_t>(row) * V + label]; }
+};
+
+template <class Src>
+__device__ __forceinline__ Raw raw_cand(const FsaStream& S, int q, const ArcRec* __restrict__ arcs, const Src& src,
+                                        int V) {
   int lo = 0, hi = S.n_act - 1;  // last i with act_off[i] <= q
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -170,22 +189,20 @@ __device__ __forceinline__ Raw raw_cand(const FsaStream& S, int q, const ArcRec*
   }
   Raw r;
   r.i = lo;
-  const int row = S.act_row[lo];
-  const float* Lr = L + static_cast<int64_t>(S.row_base + row) * Vp;
-  const double lse = row_lse[S.row_base + row];
+  const int row = S.row_base + S.act_row[lo];
   const double sc = S.act_score[lo];
   const int j = q - S.act_off[lo];
   if (j == 0) {
     r.ctx = S.act_ctx[lo];
     r.state = S.act_state[lo];
     r.label = 0;
-    r.arc_score = static_cast<double>(Lr[0]) - lse;
+    r.arc_score = src.lp(row, 0);
   } else {
     const ArcRec a = arcs[S.act_abase[lo] + j - 1];
     r.ctx = (S.act_ctx[lo] % V) * V + a.label;
     r.state = a.dst;
     r.label = a.label;
-    r.arc_score = a.w + (static_cast<double>(Lr[a.label]) - lse);
+    r.arc_score = a.w + src.lp(row, a.label);
   }
   r.score = sc + r.arc_score;
   return r;
@@ -195,9 +212,9 @@ __device__ __forceinline__ Raw raw_cand(const FsaStream& S, int q, const ArcRec*
 // all (independent) 16-byte arc loads, then the arithmetic, so a thread has
 // kU L2 requests in flight instead of one.
 constexpr int kU = 4;
+template <class Src>
 __device__ __forceinline__ void raw_batch(const FsaStream& S, int q0, int stride, int nraw,
-                                          const ArcRec* __restrict__ arcs, const float* L,
-                                          const double* row_lse, int Vp, int V, Raw (&r)[kU],
+                                          const ArcRec* __restrict__ arcs, const Src& src, int V, Raw (&r)[kU],
                                           bool (&ok)[kU]) {
   int ii[kU], jj[kU];
   ArcRec a[kU];
@@ -221,19 +238,17 @@ __device__ __forceinline__ void raw_batch(const FsaStream& S, int q0, int stride
   for (int u = 0; u < kU; ++u) {
     const int lo = ii[u];
     const int row = S.row_base + S.act_row[lo];
-    const float* Lr = L + static_cast<int64_t>(row) * Vp;
-    const double lse = row_lse[row];
     r[u].i = lo;
     if (jj[u] == 0) {
       r[u].ctx = S.act_ctx[lo];
       r[u].state = S.act_state[lo];
       r[u].label = 0;
-      r[u].arc_score = static_cast<double>(Lr[0]) - lse;
+      r[u].arc_score = src.lp(row, 0);
     } else {
       r[u].ctx = (S.act_ctx[lo] % V) * V + a[u].label;
       r[u].state = a[u].dst;
       r[u].label = a[u].label;
-      r[u].arc_score = a[u].w + (static_cast<double>(Lr[a[u].label]) - lse);
+      r[u].arc_score = a[u].w + src.lp(row, a[u].label);
     }
     r[u].score = S.act_score[lo] + r[u].arc_score;
   }
@@ -246,141 +261,22 @@ __device__ __forceinline__ int ub_bin(double ub, double score, double scale) {
   return d < 0.0 ? 0 : (d < kBins ? static_cast<int>(d) : kBins);
 }
 
-__global__ void __launch_bounds__(kDecodeThreads, 1)
-    fsa_kernel(ModelView m, const float* __restrict__ pe, const int32_t* __restrict__ frame_splits,
-               int32_t B, int32_t G, int32_t bk, const ArcRec* __restrict__ arcs,
-               const int32_t* __restrict__ gsplits, const double* __restrict__ gmaxw,
-               double beam, int32_t max_states,
-               int32_t max_contexts, LatArc* __restrict__ lat, int64_t lat_cap,
-               unsigned long long* __restrict__ lat_count, int4* __restrict__ finfo,
-               double* __restrict__ nodebest, int32_t* __restrict__ node_ctx, int32_t* __restrict__ tokens,
-               int32_t* __restrict__ lengths, double* __restrict__ scores,
-               unsigned long long* __restrict__ counters, int32_t* __restrict__ error_flag) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* HL = reinterpret_cast<float*>(smem_raw);
-  const int hl_floats = hl_floats_of(m.J, m.Vp);
-  float* W0 = HL + hl_floats;
-  float* W1 = W0 + bk * m.Vp;
-  FsaSmem& C = *reinterpret_cast<FsaSmem*>(W1 + bk * m.Vp);
-  FsaStream* SS = reinterpret_cast<FsaStream*>(&C + 1);
-
-  const int s0 = blockIdx.x * G;
-  const int ns = min(G, B - s0);
-  if (ns <= 0) return;
-  const WPipe& pipe = C.pipe;
-  const int nt = kDecodeThreads / G;
-  const Group grp{static_cast<int>(threadIdx.x) / nt, static_cast<int>(threadIdx.x) % nt, nt};
-  const bool have = grp.id < ns;
-  FsaStream& S = SS[grp.id < ns ? grp.id : 0];
-  const int sidx = s0 + grp.id;
-  const int32_t fs = have ? frame_splits[sidx] : 0;
-  const int32_t T = have ? frame_splits[sidx + 1] - fs : 0;
-  const int K = min(max_states, kMaxStates);
-  const int64_t fbase = static_cast<int64_t>(fs) + sidx;          // frame info base
-  const int64_t nbase = static_cast<int64_t>(fs) * K + sidx;       // node-best base
-  // Histogram range below the upper bound: the beam (capped at 8 nats) plus
-  // 2 nats of slack for the gap between the bound and the true best.
-  const double scale = kBins / ((beam < 8.0 ? beam : 8.0) + 2.0);
-  const int M = K + 32;  // hot-candidate target
-
-  int32_t tmax = 0;
-  for (int i = 0; i < ns; ++i) tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
-  if (have && grp.tid == 0) {  // init_streams (95-120): ((0,0), state 0, 0.0, node 0)
-    node_ctx[nbase] = 0;
-    S.n_act = 1;
-    S.num_nodes = 1;
-    S.act_ctx[0] = 0;
-    S.act_state[0] = 0;
-    S.act_score[0] = 0.0;
-    S.act_node[0] = 0;
-    S.flag = 0;
-  }
-  if (threadIdx.x == 0) {
-    C.pipe = make_wpipe(W0, W1, C.bar, C.wcur, m, bk);
-    C.rows_total = 0;
-    C.ph[0] = C.ph[1] = C.ph[2] = 0;
-    mbar_init(&C.bar[0], 1);
-    mbar_init(&C.bar[1], 1);
-    fence_mbar_init();
-  }
-  if (have && grp.tid == 0) S.raw_total = S.lat_total = 0;
-  load_exp_table(C.etab);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    wpipe_issue(pipe, m, 0);
-    wpipe_issue(pipe, m, 1);
-  }
-  uint32_t gch = 0;
-
-  for (int32_t t = 0; t < tmax; ++t) {
-    const bool live = have && t < T;
-    // get_contexts: distinct contexts in order; each tuple's row.
-    if (live && grp.tid == 0) {
-      int nr = 0;
-      for (int i = 0; i < S.n_act; ++i) {
-        if (nr == 0 || S.row_ctx[nr - 1] != S.act_ctx[i]) S.row_ctx[nr++] = S.act_ctx[i];
-        S.act_row[i] = nr - 1;
-      }
-      S.nrows = nr;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int R = 0;
-      for (int g2 = 0; g2 < ns; ++g2) {
-        FsaStream& X = SS[g2];
-        const int32_t f2 = frame_splits[s0 + g2];
-        if (t >= frame_splits[s0 + g2 + 1] - f2) continue;
-        X.row_base = R;
-        for (int r = 0; r < X.nrows; ++r) {
-          if (R < kRowCap) {
-            C.row_pe[R] = f2 + t;
-            C.row_ctx[R] = X.row_ctx[r];
-          }
-          ++R;
-        }
-      }
-      if (R > kRowCap) {
-        atomicExch(error_flag, 2);  // more joiner rows than the CTA tile holds
-        R = kRowCap;
-      }
-      C.nrows = R;
-      // the exact log-softmax borrows the weight stages when its scratch fits
-      C.pipe.defer = (C.pipe.nc >= 2 && lse_cta_fits(R, m.V, bk * m.Vp)) ? 1 : 0;
-    }
-    __syncthreads();
-    const int R = C.nrows;
-    if (threadIdx.x == 0) C.rows_total += R;
-    const long long c0 = clock64();
-    build_h(m, pe, C.row_pe, C.row_ctx, R, HL);
-    const long long c1 = clock64();
-    joiner_gemm(m, pipe, gch, HL, R);
-    const long long c2 = clock64();
-    if (pipe.defer) {  // CTA-wide exact normalisers in the weight stages
-      double* E = reinterpret_cast<double*>(W0);
-      lse_cta_exps(HL, E, bk * m.Vp, m.Vp, m.V, R, C.etab, C.row_m);
-      if (threadIdx.x < 32) {
-        lse_cta_chain(HL, E, bk * m.Vp, m.Vp, m.V, R, C.row_m, C.row_lse, nullptr);
-        if (threadIdx.x < R) C.row_lpmax[threadIdx.x] = static_cast<double>(C.row_m[threadIdx.x]) - C.row_lse[threadIdx.x];
-      }
-      __syncthreads();
-      wpipe_issue_next(pipe, m, gch);
-    } else {
-      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      for (int r = warp; r < R; r += kDecodeThreads / 32) {
-        const float* L = HL + static_cast<int64_t>(r) * m.Vp;
-        const double lse = row_lse(L, m.V, lse_scratch(HL, m.Vp), C.etab);
-        float mx = -FLT_MAX;
-        for (int k = lane; k < m.V; k += 32) mx = fmaxf(mx, L[k]);
-        mx = warp_max_f(mx);
-        if (lane == 0) {
-          C.row_lse[r] = lse;
-          C.row_lpmax[r] = static_cast<double>(mx) - lse;
-        }
-      }
-    }
-    __syncthreads();
-
-    if (live) {
+// One frame of expand_arcs + prune_streams (fsa_search.hpp:161-297) for the
+// stream of thread group `grp`, its active tuples in S (their joiner rows
+// S.row_base + act_row), log-probs from `src`, row_lpmax[r] = max_k lp(r, k):
+// the new active set in S, the frame's lattice arcs in the pool, its frame
+// info in *finfo_t, the new nodes' contexts in nctx.  Shared by the decoder
+// (fsa_kernel, LpJoiner) and the step API (fsa_step_kernel, LpRows).
+template <class Src>
+__device__ __forceinline__ void fsa_frame(FsaStream& S, const Group& grp, const Src& src,
+                                          const double* __restrict__ row_lpmax, int V,
+                                          const ArcRec* __restrict__ arcs, const int32_t* __restrict__ gsplits,
+                                          const double* __restrict__ gmaxw, double beam, int K, int max_states,
+                                          int max_contexts, int M, double scale, LatArc* __restrict__ lat,
+                                          int64_t lat_cap, unsigned long long* __restrict__ lat_count,
+                                          int4* __restrict__ finfo_t, int32_t* __restrict__ nctx,
+                                          int32_t* __restrict__ error_flag) {
+  const int nt = grp.nt;
       // ---- expand_arcs ----
       // Segment offsets of the raw candidates (one thread per active tuple,
       // group scan) and an upper bound on the frame's best candidate: tuple i
@@ -396,7 +292,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
           const int a0 = gsplits[st], a1 = gsplits[st + 1];
           S.act_abase[i] = a0;
           cnt = 1 + a1 - a0;
-          bound = S.act_score[i] + fmax(0.0, gmaxw[st]) + C.row_lpmax[S.row_base + S.act_row[i]];
+          bound = S.act_score[i] + fmax(0.0, gmaxw[st]) + row_lpmax[S.row_base + S.act_row[i]];
         }
         int total = 0;
         const int off = group_scan(grp, S, cnt, &total);
@@ -426,7 +322,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       for (int q0 = grp.tid; q0 < nraw; q0 += kU * nt) {
         Raw rc[kU];
         bool ok[kU];
-        raw_batch(S, q0, nt, nraw, arcs, HL, C.row_lse, m.Vp, m.V, rc, ok);
+        raw_batch(S, q0, nt, nraw, arcs, src, V, rc, ok);
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           if (!ok[u]) continue;
@@ -478,7 +374,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         for (int q0 = grp.tid; q0 < nraw; q0 += kU * nt) {
           Raw rc[kU];
           bool ok[kU];
-          raw_batch(S, q0, nt, nraw, arcs, HL, C.row_lse, m.Vp, m.V, rc, ok);
+          raw_batch(S, q0, nt, nraw, arcs, src, V, rc, ok);
 #pragma unroll
           for (int u = 0; u < kU; ++u) {
             if (!ok[u] || rc[u].score < floor) continue;
@@ -615,7 +511,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       for (int q0 = grp.tid; q0 < nraw; q0 += kU * nt) {
         Raw rc[kU];
         bool ok[kU];
-        raw_batch(S, q0, nt, nraw, arcs, HL, C.row_lse, m.Vp, m.V, rc, ok);
+        raw_batch(S, q0, nt, nraw, arcs, src, V, rc, ok);
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           if (!ok[u]) continue;
@@ -660,7 +556,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
           while (bits) {
             const int q = (w << 5) + __ffs(bits) - 1;
             bits &= bits - 1;
-            const Raw rc = raw_cand(S, q, arcs, gsplits, HL, C.row_lse, m.Vp, m.V);
+            const Raw rc = raw_cand(S, q, arcs, src, V);
             const uint64_t k = key_of(rc.ctx, rc.state);
             uint32_t slot = hash_slot(k, kSurvHash);
             while (S.shkey[slot] != k) slot = (slot + 1) & (kSurvHash - 1);
@@ -677,7 +573,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       grp.sync();
       // New active set, sorted by (ctx, state).
       if (my_rank >= 0) {
-        node_ctx[nbase + S.num_nodes + my_rank] = my_ctx;
+        nctx[S.num_nodes + my_rank] = my_ctx;
         S.act_ctx[my_rank] = my_ctx;
         S.act_state[my_rank] = my_state;
         S.act_score[my_rank] = my_score;
@@ -685,13 +581,151 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
       }
       grp.sync();
       if (grp.tid == 0) {
-        finfo[fbase + t] = make_int4(S.arc_off, S.arc_count, S.num_nodes, nsurv);
+        *finfo_t = make_int4(S.arc_off, S.arc_count, S.num_nodes, nsurv);
         S.n_act = nsurv;
         S.num_nodes += nsurv;
         if (nsurv == 0) S.flag |= 1;  // dead stream (233-238): cannot happen with finite scores
       }
       grp.sync();
+}
+
+__global__ void __launch_bounds__(kDecodeThreads, 1)
+    fsa_kernel(ModelView m, const float* __restrict__ pe, const int32_t* __restrict__ frame_splits,
+               int32_t B, int32_t G, int32_t bk, const ArcRec* __restrict__ arcs,
+               const int32_t* __restrict__ gsplits, const double* __restrict__ gmaxw,
+               double beam, int32_t max_states,
+               int32_t max_contexts, LatArc* __restrict__ lat, int64_t lat_cap,
+               unsigned long long* __restrict__ lat_count, int4* __restrict__ finfo,
+               double* __restrict__ nodebest, int32_t* __restrict__ node_ctx, int32_t* __restrict__ tokens,
+               int32_t* __restrict__ lengths, double* __restrict__ scores,
+               unsigned long long* __restrict__ counters, int32_t* __restrict__ error_flag) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* HL = reinterpret_cast<float*>(smem_raw);
+  const int hl_floats = hl_floats_of(m.J, m.Vp);
+  float* W0 = HL + hl_floats;
+  float* W1 = W0 + bk * m.Vp;
+  FsaSmem& C = *reinterpret_cast<FsaSmem*>(W1 + bk * m.Vp);
+  FsaStream* SS = reinterpret_cast<FsaStream*>(&C + 1);
+
+  const int s0 = blockIdx.x * G;
+  const int ns = min(G, B - s0);
+  if (ns <= 0) return;
+  const WPipe& pipe = C.pipe;
+  const int nt = kDecodeThreads / G;
+  const Group grp{static_cast<int>(threadIdx.x) / nt, static_cast<int>(threadIdx.x) % nt, nt};
+  const bool have = grp.id < ns;
+  FsaStream& S = SS[grp.id < ns ? grp.id : 0];
+  const int sidx = s0 + grp.id;
+  const int32_t fs = have ? frame_splits[sidx] : 0;
+  const int32_t T = have ? frame_splits[sidx + 1] - fs : 0;
+  const int K = min(max_states, kMaxStates);
+  const int64_t fbase = static_cast<int64_t>(fs) + sidx;          // frame info base
+  const int64_t nbase = static_cast<int64_t>(fs) * K + sidx;       // node-best base
+  // Histogram range below the upper bound: the beam (capped at 8 nats) plus
+  // 2 nats of slack for the gap between the bound and the true best.
+  const double scale = kBins / ((beam < 8.0 ? beam : 8.0) + 2.0);
+  const int M = K + 32;  // hot-candidate target
+
+  int32_t tmax = 0;
+  for (int i = 0; i < ns; ++i) tmax = max(tmax, frame_splits[s0 + i + 1] - frame_splits[s0 + i]);
+  if (have && grp.tid == 0) {  // init_streams (95-120): ((0,0), state 0, 0.0, node 0)
+    node_ctx[nbase] = 0;
+    S.n_act = 1;
+    S.num_nodes = 1;
+    S.act_ctx[0] = 0;
+    S.act_state[0] = 0;
+    S.act_score[0] = 0.0;
+    S.act_node[0] = 0;
+    S.flag = 0;
+  }
+  if (threadIdx.x == 0) {
+    C.pipe = make_wpipe(W0, W1, C.bar, C.wcur, m, bk);
+    C.rows_total = 0;
+    C.ph[0] = C.ph[1] = C.ph[2] = 0;
+    mbar_init(&C.bar[0], 1);
+    mbar_init(&C.bar[1], 1);
+    fence_mbar_init();
+  }
+  if (have && grp.tid == 0) S.raw_total = S.lat_total = 0;
+  load_exp_table(C.etab);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    wpipe_issue(pipe, m, 0);
+    wpipe_issue(pipe, m, 1);
+  }
+  uint32_t gch = 0;
+
+  for (int32_t t = 0; t < tmax; ++t) {
+    const bool live = have && t < T;
+    // get_contexts: distinct contexts in order; each tuple's row.
+    if (live && grp.tid == 0) {
+      int nr = 0;
+      for (int i = 0; i < S.n_act; ++i) {
+        if (nr == 0 || S.row_ctx[nr - 1] != S.act_ctx[i]) S.row_ctx[nr++] = S.act_ctx[i];
+        S.act_row[i] = nr - 1;
+      }
+      S.nrows = nr;
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int R = 0;
+      for (int g2 = 0; g2 < ns; ++g2) {
+        FsaStream& X = SS[g2];
+        const int32_t f2 = frame_splits[s0 + g2];
+        if (t >= frame_splits[s0 + g2 + 1] - f2) continue;
+        X.row_base = R;
+        for (int r = 0; r < X.nrows; ++r) {
+          if (R < kRowCap) {
+            C.row_pe[R] = f2 + t;
+            C.row_ctx[R] = X.row_ctx[r];
+          }
+          ++R;
+        }
+      }
+      if (R > kRowCap) {
+        atomicExch(error_flag, 2);  // more joiner rows than the CTA tile holds
+        R = kRowCap;
+      }
+      C.nrows = R;
+      // the exact log-softmax borrows the weight stages when its scratch fits
+      C.pipe.defer = (C.pipe.nc >= 2 && lse_cta_fits(R, m.V, bk * m.Vp)) ? 1 : 0;
+    }
+    __syncthreads();
+    const int R = C.nrows;
+    if (threadIdx.x == 0) C.rows_total += R;
+    const long long c0 = clock64();
+    build_h(m, pe, C.row_pe, C.row_ctx, R, HL);
+    const long long c1 = clock64();
+    joiner_gemm(m, pipe, gch, HL, R);
+    const long long c2 = clock64();
+    if (pipe.defer) {  // CTA-wide exact normalisers in the weight stages
+      double* E = reinterpret_cast<double*>(W0);
+      lse_cta_exps(HL, E, bk * m.Vp, m.Vp, m.V, R, C.etab, C.row_m);
+      if (threadIdx.x < 32) {
+        lse_cta_chain(HL, E, bk * m.Vp, m.Vp, m.V, R, C.row_m, C.row_lse, nullptr);
+        if (threadIdx.x < R) C.row_lpmax[threadIdx.x] = static_cast<double>(C.row_m[threadIdx.x]) - C.row_lse[threadIdx.x];
+      }
+      __syncthreads();
+      wpipe_issue_next(pipe, m, gch);
+    } else {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int r = warp; r < R; r += kDecodeThreads / 32) {
+        const float* L = HL + static_cast<int64_t>(r) * m.Vp;
+        const double lse = row_lse(L, m.V, lse_scratch(HL, m.Vp), C.etab);
+        float mx = -FLT_MAX;
+        for (int k = lane; k < m.V; k += 32) mx = fmaxf(mx, L[k]);
+        mx = warp_max_f(mx);
+        if (lane == 0) {
+          C.row_lse[r] = lse;
+          C.row_lpmax[r] = static_cast<double>(mx) - lse;
+        }
+      }
+    }
+    __syncthreads();
+
+    if (live)
+      fsa_frame(S, grp, LpJoiner{HL, C.row_lse, m.Vp}, C.row_lpmax, m.V, arcs, gsplits, gmaxw, beam, K, max_states,
+                max_contexts, M, scale, lat, lat_cap, lat_count, finfo + fbase + t, node_ctx + nbase, error_flag);
     __syncthreads();
     if (threadIdx.x == 0) {
       const long long c4 = clock64();
