@@ -219,6 +219,44 @@ rnntg_status rnntg_fsa_lattice(rnntg_model_t model, int32_t stream,
                                int32_t capacity, int32_t* src, int32_t* dst,
                                int32_t* label, double* score);
 
+/* The Algorithm-1 step API (fsa_search.hpp:95-297; Algorithm 1):
+ * the caller runs its own decoder + joiner between the context query and the
+ * expansion, and hands in the log-prob rows -- expand_arcs' plug-in point
+ * (fsa_search.hpp:59-61).  One open decode per model handle:
+ *
+ *   rnntg_fsa_stream_begin     init_streams (95-120) over B streams sharing
+ *                              `graph` (which must outlive the decode, as
+ *                              DecodeStream::graph; destroying it ends the
+ *                              decode); num_frames[i] = frames stream i will
+ *                              consume (the driver's DecodeStream::num_frames)
+ *   rnntg_fsa_stream_contexts  get_contexts (124-154): per stream its distinct
+ *                              active contexts in ascending packed order
+ *                              (a*V + b); streams past their last frame (or
+ *                              dead) contribute none.  out_row_splits [B+1]
+ *                              is always written; contexts when capacity >=
+ *                              out_row_splits[B] (call with 0 to size)
+ *   rnntg_fsa_stream_step      expand_arcs (161-223) + prune_streams
+ *                              (230-297) on the GPU with logprobs
+ *                              [out_row_splits[B]][V] fp64 (host or device,
+ *                              `mem`), row r = log p(. | context r); a step
+ *                              without a fresh contexts call is the
+ *                              reference's "stale get_contexts data"
+ *                              (RNNTG_INTERNAL)
+ *   rnntg_fsa_stream_end       finish_stream + lattice_to_best_seq(kMax) of
+ *                              every stream: as rnntg_fsa_beam_search's
+ *                              outputs; afterwards rnntg_fsa_lattice /
+ *                              _text / _best read these lattices. */
+rnntg_status rnntg_fsa_stream_begin(rnntg_model_t model, rnntg_graph_t graph,
+                                    const rnntg_fsa_params* params, int32_t B,
+                                    const int32_t* num_frames);
+rnntg_status rnntg_fsa_stream_contexts(rnntg_model_t model,
+                                       int32_t* out_row_splits,
+                                       int32_t capacity, int32_t* out_contexts);
+rnntg_status rnntg_fsa_stream_step(rnntg_model_t model, const double* logprobs,
+                                   int32_t mem);
+rnntg_status rnntg_fsa_stream_end(rnntg_model_t model, int32_t* out_splits,
+                                  int32_t* out_tokens, double* out_scores);
+
 /* lattice_to_best_seq(lattice, kLogAdd, nbest_n, seed) (fsa_search.hpp:
  * 410-425) for every stream of the last rnntg_fsa_beam_search, on the GPU:
  * n-best sampling with DetRng(seed) (fsa.hpp:390-448), blank-free

@@ -354,6 +354,12 @@ class Reference:
             C.POINTER(C.c_void_p),
         ]
 
+        L.ref_steps_begin.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_int32, _i32p]
+        L.ref_steps_begin.restype = C.c_void_p
+        L.ref_steps_contexts.argtypes = [C.c_void_p, _i32p, _i32p]
+        L.ref_steps_step.argtypes = [C.c_void_p, _f64p, C.c_int32, C.c_int32]
+        L.ref_steps_end.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), _i32p, _i32p, _f64p]
+        L.ref_steps_free.argtypes = [C.c_void_p]
         L.ref_fsa_logadd.argtypes = [
             C.c_void_p, _f32p, _i32p, C.c_int32, C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_int,
             C.c_int32, C.c_uint64, _i32p, _i32p, _f64p,
@@ -603,6 +609,46 @@ def _refmodel_fsa_logadd(self, feats, splits, graph, beam, max_states, max_conte
 
 
 RefModel.fsa_logadd = _refmodel_fsa_logadd
+
+
+class RefSteps:
+    """The reference's Algorithm-1 step API (init_streams / get_contexts /
+    expand_arcs + prune_streams / finish), driven like fsa_beam_search."""
+
+    def __init__(self, ref: "Reference", graph: "RefGraph", params, V, num_frames):
+        self.ref, self.V = ref, V
+        nf = np.ascontiguousarray(num_frames, np.int32)
+        self.B, self.total = len(nf), int(nf.sum())
+        self.h = ref.lib.ref_steps_begin(graph.h, len(nf), params[0], params[1], params[2], V, _p(nf, _i32p))
+        if not self.h:
+            raise RuntimeError(ref.lib.ref_last_error().decode())
+
+    def contexts(self):
+        rs = np.zeros(self.B + 1, np.int32)
+        ctx = np.zeros(max(1, self.B * 64 * 2), np.int32)
+        self.ref._check(self.ref.lib.ref_steps_contexts(self.h, _p(rs, _i32p), _p(ctx, _i32p)))
+        return rs, ctx[: rs[-1]].copy()
+
+    def step(self, logprobs):
+        lp = np.ascontiguousarray(logprobs, np.float64).reshape(-1, self.V)
+        self.ref._check(self.ref.lib.ref_steps_step(self.h, _p(lp, _f64p), lp.shape[0], self.V))
+
+    def end(self):
+        texts = (C.c_void_p * self.B)()
+        osp = np.zeros(self.B + 1, np.int32)
+        otk = np.zeros(max(1, self.total), np.int32)
+        osc = np.zeros(max(1, self.B), np.float64)
+        self.ref._check(self.ref.lib.ref_steps_end(self.h, texts, _p(osp, _i32p), _p(otk, _i32p), _p(osc, _f64p)))
+        out = []
+        for i in range(self.B):
+            out.append(C.cast(texts[i], C.c_char_p).value.decode())
+            self.ref.lib.ref_free_string(texts[i])
+        return unragged(osp, otk), osc[: self.B], out
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ref.lib.ref_steps_free(self.h)
+            self.h = None
 
 
 def synthetic_arpa(V=500, n_bigrams=1500, n_trigrams=3000, seed=7):

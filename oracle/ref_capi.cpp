@@ -455,4 +455,92 @@ int ref_fsa_logadd(void* mp, const float* feats, const int32_t* splits, int32_t 
   }
 }
 
+// ---- the Algorithm-1 step API (fsa_search.hpp:95-297), driven like the
+// reference's fsa_beam_search (326-387): num_frames per stream, streams
+// finished (finish_stream) when they reach it; for the GPU step-API tests.
+struct RefSteps {
+  std::vector<rnnt::Fsa> graphs;  // DecodeStream::graph points in here
+  std::vector<rnnt::DecodeStream> streams;
+  rnnt::RaggedShape shape;
+};
+
+void* ref_steps_begin(void* gp, int32_t B, double beam, int32_t max_states, int32_t max_contexts, int32_t V,
+                      const int32_t* num_frames) {
+  try {
+    auto* r = new RefSteps();
+    r->graphs.assign(B, *static_cast<rnnt::Fsa*>(gp));
+    rnnt::FsaSearchParams p;
+    p.beam = beam;
+    p.max_states = max_states;
+    p.max_contexts = max_contexts;
+    r->streams = rnnt::init_streams(r->graphs, p, V);
+    for (int32_t i = 0; i < B; ++i) {
+      r->streams[i].num_frames = num_frames[i];
+      if (num_frames[i] == 0) rnnt::detail::finish_stream(r->streams[i]);
+    }
+    return r;
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+// get_contexts: row splits [B+1] and packed contexts a*V+b.
+int ref_steps_contexts(void* hp, int32_t* out_row_splits, int32_t* out_ctx) {
+  try {
+    auto* r = static_cast<RefSteps*>(hp);
+    auto [shape, ctx] = rnnt::get_contexts(r->streams);
+    r->shape = shape;
+    for (size_t i = 0; i < shape.row_splits.size(); ++i) out_row_splits[i] = shape.row_splits[i];
+    const int32_t V = r->streams.empty() ? 2 : r->streams[0].vocab_size;
+    for (int32_t k = 0; k < ctx.rows; ++k) out_ctx[k] = ctx.at(k, 0) * V + ctx.at(k, 1);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// expand_arcs + prune_streams with the caller's rows, then finish_stream
+// for the streams that reached their last frame.
+int ref_steps_step(void* hp, const double* logprobs, int32_t rows, int32_t V) {
+  try {
+    auto* r = static_cast<RefSteps*>(hp);
+    rnnt::Mat<double> lp(rows, V);
+    for (int32_t k = 0; k < rows * V; ++k) lp.data[k] = logprobs[k];
+    rnnt::expand_arcs(r->streams, r->shape, lp);
+    rnnt::prune_streams(r->streams);
+    for (rnnt::DecodeStream& s : r->streams)
+      if (!s.done && s.t == s.num_frames) rnnt::detail::finish_stream(s);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// Per stream: serialize_fsa_text of its lattice, lattice_to_best_seq(kMax)
+// tokens and best_path score (-inf without a complete path).
+int ref_steps_end(void* hp, char** texts, int32_t* out_splits, int32_t* out_tokens, double* out_scores) {
+  try {
+    auto* r = static_cast<RefSteps*>(hp);
+    std::vector<std::vector<int32_t>> ys;
+    for (size_t i = 0; i < r->streams.size(); ++i) {
+      rnnt::Fsa lat = rnnt::detail::build_lattice(r->streams[i]);
+      texts[i] = strdup(rnnt::serialize_fsa_text(lat).c_str());
+      ys.push_back(rnnt::lattice_to_best_seq(lat, rnnt::MergeOp::kMax));
+      double sc = rnnt::kNegInf;
+      try {
+        sc = rnnt::best_path(lat).score;
+      } catch (const rnnt::ValidationError&) {
+      }
+      out_scores[i] = sc;
+    }
+    write_ragged(ys, out_splits, out_tokens);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+void ref_steps_free(void* hp) { delete static_cast<RefSteps*>(hp); }
+
 }  // extern "C"

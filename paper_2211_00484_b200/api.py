@@ -127,6 +127,10 @@ def _load():
     lib.rnntg_fsa_lattice.restype = C.c_int
     lib.rnntg_fsa_lattice_text.argtypes = [vp, i32, i32, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)]
     lib.rnntg_fsa_lattice_best.argtypes = [vp, i32, i32, C.c_uint64, i32p, vp, vp]
+    lib.rnntg_fsa_stream_begin.argtypes = [vp, vp, C.POINTER(_FsaParams), i32, i32p]
+    lib.rnntg_fsa_stream_contexts.argtypes = [vp, i32p, i32, i32p]
+    lib.rnntg_fsa_stream_step.argtypes = [vp, vp, i32]
+    lib.rnntg_fsa_stream_end.argtypes = [vp, i32p, vp, vp]
     lib.rnntg_model_set_encoder.argtypes = [vp, C.POINTER(_EncDesc)]
     lib.rnntg_encoder_forward.argtypes = [vp, f32p, i32p, i32, i32, vp]
     lib.rnntg_debug_decoder_projection.argtypes = [vp, i32p, i32, f32p]
@@ -149,6 +153,10 @@ def _load():
         "rnntg_fsa_beam_search",
         "rnntg_fsa_lattice_text",
         "rnntg_fsa_lattice_best",
+        "rnntg_fsa_stream_begin",
+        "rnntg_fsa_stream_contexts",
+        "rnntg_fsa_stream_step",
+        "rnntg_fsa_stream_end",
         "rnntg_model_set_encoder",
         "rnntg_encoder_forward",
         "rnntg_debug_decoder_projection",
@@ -466,6 +474,41 @@ class Decoder:
             )
         )
         return dict(num_nodes=nn.value, src=src[:n], dst=dst[:n], label=lab[:n], score=sc[:n])
+
+    # ---- the Algorithm-1 step API (fsa_search.hpp:95-297) ----
+    def fsa_stream_begin(self, graph: Graph, params: FsaParams, num_frames):
+        """init_streams over len(num_frames) streams sharing `graph`."""
+        nf = np.ascontiguousarray(num_frames, np.int32)
+        fp = _FsaParams(float(params.beam), int(params.max_states), int(params.max_contexts))
+        _check(self._lib.rnntg_fsa_stream_begin(self.h, graph.h, C.byref(fp), len(nf), _i32p(nf)))
+        self._step_graph = graph  # the device graph must outlive the decode (DecodeStream::graph)
+        self._step_B = len(nf)
+        self._last_fsa_splits = np.concatenate([[0], np.cumsum(nf)]).astype(np.int32)
+
+    def fsa_stream_contexts(self):
+        """get_contexts: (row_splits [B+1], packed contexts a*V+b per row)."""
+        rs = np.zeros(self._step_B + 1, np.int32)
+        _check(self._lib.rnntg_fsa_stream_contexts(self.h, _i32p(rs), 0, None))
+        ctx = np.zeros(max(1, int(rs[-1])), np.int32)
+        _check(self._lib.rnntg_fsa_stream_contexts(self.h, _i32p(rs), len(ctx), _i32p(ctx)))
+        return rs, ctx[: rs[-1]]
+
+    def fsa_stream_step(self, logprobs):
+        """expand_arcs + prune_streams with the caller's log-prob rows [rows][V]."""
+        if hasattr(logprobs, "is_cuda") and logprobs.is_cuda:
+            _check(self._lib.rnntg_fsa_stream_step(self.h, C.c_void_p(logprobs.data_ptr()), MEM_DEVICE))
+            return
+        lp = np.ascontiguousarray(logprobs, np.float64)
+        _check(self._lib.rnntg_fsa_stream_step(self.h, _ptr(lp) if lp.size else None, MEM_HOST))
+
+    def fsa_stream_end(self):
+        """finish_stream + lattice_to_best_seq(kMax): (token lists, best-path scores)."""
+        B = self._step_B
+        osp = np.zeros(B + 1, np.int32)
+        tok = np.zeros(max(1, int(self._last_fsa_splits[-1])), np.int32)
+        sc = np.zeros(max(1, B), np.float64)
+        _check(self._lib.rnntg_fsa_stream_end(self.h, _i32p(osp), _ptr(tok), _ptr(sc)))
+        return _ragged(osp, tok), sc[:B].copy()
 
     def fsa_lattice_best(self, nbest: int = 100, seed: int = 0, merge_op: int = MERGE_LOG_ADD):
         """lattice_to_best_seq(lattice, kLogAdd, nbest, seed) of every stream

@@ -60,6 +60,14 @@ struct rnntg_model_s {
   Scratch finfo, nodebest, lattice, flag, feat, hid, fenc;
   Scratch nodectx, ladd_u, ladd_tot, ladd_narc, ladd_paths, ladd_cells, ladd_pos;  // log-add best sequences
   int32_t last_fsa_K = 0;
+  // FSA step API (rnntg_fsa_stream_*): the open decode's graph, parameters,
+  // frame splits, per-stream device state, and the rows of the last
+  // rnntg_fsa_stream_contexts (host)
+  rnntg_graph_t step_graph = nullptr;
+  rnntg_fsa_params step_params{};
+  std::vector<int32_t> step_fs, step_rows, step_nact;
+  bool step_open = false, step_have_rows = false;
+  Scratch step_state, step_P, step_rsplits;
   uint64_t ladd_seed = 0;
   int64_t ladd_n = 0, ladd_cell_cap = 4096;
   int64_t lat_cap_hint = 0;
@@ -76,6 +84,7 @@ struct rnntg_model_s {
 struct rnntg_graph_s {
   rnntg_model_t model = nullptr;
   int32_t num_states = 0, num_arcs = 0;
+  int32_t max_out = 0;        // largest out-degree (step API lattice sizing)
   int32_t* splits = nullptr;  // device [S+1]
   void* arcs = nullptr;       // device 16-byte records {dst, label, weight}
   double* maxw = nullptr;     // device [S]: max outgoing arc weight per state
@@ -588,7 +597,8 @@ rnntg_status rnntg_model_destroy(rnntg_model_t h) {
                      &h->counters, &h->ctx, &h->out_tok, &h->out_splits, &h->logits,
                      &h->finfo, &h->nodebest, &h->lattice, &h->flag, &h->feat, &h->hid,
                      &h->hstate, &h->pool, &h->fenc, &h->nodectx, &h->ladd_u, &h->ladd_tot,
-                     &h->ladd_narc, &h->ladd_paths, &h->ladd_cells, &h->ladd_pos})
+                     &h->ladd_narc, &h->ladd_paths, &h->ladd_cells, &h->ladd_pos, &h->step_state, &h->step_P,
+                     &h->step_rsplits})
     s->release();
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
@@ -857,8 +867,11 @@ rnntg_status rnntg_graph_create(rnntg_model_t h, int32_t num_states,
   if (num_arcs < 0 || !arc_splits) return invalid("bad arc list");
   if (arc_splits[0] != 0 || arc_splits[num_states] != num_arcs)
     return invalid("arc_splits must start at 0 and end at num_arcs");
-  for (int32_t s = 0; s < num_states; ++s)
+  int32_t max_out = 0;
+  for (int32_t s = 0; s < num_states; ++s) {
     if (arc_splits[s + 1] < arc_splits[s]) return invalid("arc_splits must be non-decreasing");
+    max_out = std::max(max_out, arc_splits[s + 1] - arc_splits[s]);
+  }
   for (int32_t a = 0; a < num_arcs; ++a) {
     if (dst[a] < 0 || dst[a] >= num_states) return invalid("arc references state out of range");
     // init_streams, fsa_search.hpp:103-111.
@@ -873,6 +886,7 @@ rnntg_status rnntg_graph_create(rnntg_model_t h, int32_t num_states,
   g->model = h;
   g->num_states = num_states;
   g->num_arcs = num_arcs;
+  g->max_out = max_out;
   struct ArcRec {
     int32_t dst, label;
     double w;
@@ -904,6 +918,13 @@ rnntg_status rnntg_graph_create(rnntg_model_t h, int32_t num_states,
 
 rnntg_status rnntg_graph_destroy(rnntg_graph_t g) {
   if (!g) return RNNTG_OK;
+  if (g->model) {  // an open step decode over this graph ends with it
+    std::lock_guard<std::mutex> lk(g->model->mu);
+    if (g->model->step_graph == g) {
+      g->model->step_open = false;
+      g->model->step_graph = nullptr;
+    }
+  }
   if (g->arcs) cudaFree(g->arcs);
   if (g->splits) cudaFree(g->splits);
   if (g->maxw) cudaFree(g->maxw);
@@ -1034,6 +1055,230 @@ rnntg_status rnntg_fsa_beam_search(rnntg_model_t h, const float* enc,
     h->last_fsa_K = std::min(p->max_states, rnntg::kFsaMaxStates);
   }
   return st;
+}
+
+// ---- FSA step API (the reference's Algorithm-1 cycle, fsa_search.hpp:95-297) ----
+namespace {
+rnntg_status fsa_flag_status(int32_t flag) {
+  switch (flag) {
+    case 0:
+      return RNNTG_OK;
+    case 2:
+      set_error("more than 32 distinct contexts per CTA frame (max_contexts too large for this build)");
+      return RNNTG_UNSUPPORTED;
+    case 3:
+      set_error("candidate hash overflow (too many exact-score duplicates near the beam cut)");
+      return RNNTG_UNSUPPORTED;
+    case 4:
+      set_error("max_states binds above the device cap of 64 states per stream");
+      return RNNTG_UNSUPPORTED;
+    case 6:
+      set_error("more than 32768 expansion candidates in one stream-frame (graph out-degree too high)");
+      return RNNTG_UNSUPPORTED;
+    case 7:
+      set_error("expand_arcs: stale get_contexts data");
+      return RNNTG_INTERNAL;
+    default:
+      set_error("fsa kernel error flag " + std::to_string(flag));
+      return RNNTG_INTERNAL;
+  }
+}
+
+rnntg::FsaStepArgs step_args(rnntg_model_t h) {
+  rnntg::FsaStepArgs a{};
+  a.B = static_cast<int32_t>(h->step_fs.size()) - 1;
+  a.V = h->d.V;
+  a.frame_splits = h->splits.as<int32_t>();
+  a.row_splits = h->step_rsplits.as<int32_t>();
+  a.P = h->step_P.as<double>();
+  a.graph_arcs = h->step_graph->arcs;
+  a.graph_splits = h->step_graph->splits;
+  a.graph_maxw = h->step_graph->maxw;
+  a.beam = h->step_params.beam;
+  a.max_states = h->step_params.max_states;
+  a.max_contexts = h->step_params.max_contexts;
+  a.lattice = h->lattice.ptr;
+  a.lattice_cap = static_cast<int64_t>(h->lattice.bytes / 24);
+  a.lattice_count = reinterpret_cast<unsigned long long*>(h->flag.as<char>() + 8);
+  a.lat_frame_info = h->finfo.as<int32_t>();
+  a.node_best = h->nodebest.as<double>();
+  a.node_ctx = h->nodectx.as<int32_t>();
+  a.state = h->step_state.ptr;
+  a.tokens = h->tok.as<int32_t>();
+  a.lengths = h->len.as<int32_t>();
+  a.scores = h->score.as<double>();
+  a.counters = h->counters.as<unsigned long long>();
+  a.error_flag = h->flag.as<int32_t>();
+  return a;
+}
+}  // namespace
+
+rnntg_status rnntg_fsa_stream_begin(rnntg_model_t h, rnntg_graph_t graph, const rnntg_fsa_params* p, int32_t B,
+                                    const int32_t* num_frames) {
+  Nvtx nvtx_range("rnntg_fsa_stream_begin");
+  if (!h || !p || !graph) return invalid("null argument");
+  if (graph->model != h) return invalid("graph belongs to another model handle");
+  // check_fsa_search_params (fsa_search.hpp:83-90), init_streams (95-120).
+  if (!(p->beam >= 0.0)) return invalid("fsa search beam must be >= 0");
+  if (p->max_states < 1) return invalid("max_states must be >= 1");
+  if (p->max_contexts < 1) return invalid("max_contexts must be >= 1");
+  if (B < 0 || (B > 0 && !num_frames)) return invalid("bad stream count");
+  for (int32_t i = 0; i < B; ++i)
+    if (num_frames[i] < 0) return invalid("num_frames must be >= 0");
+  std::lock_guard<std::mutex> lk(h->mu);
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  h->last_fsa_fs.clear();
+  h->step_open = false;
+  h->step_have_rows = false;
+  h->step_fs.assign(B + 1, 0);
+  for (int32_t i = 0; i < B; ++i) h->step_fs[i + 1] = h->step_fs[i] + num_frames[i];
+  const int64_t total = h->step_fs[B];
+  const int K = std::min(p->max_states, rnntg::kFsaMaxStates);
+  RNNTG_CUDA_TRY(h->splits.ensure(sizeof(int32_t) * (B + 1)));
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(h->splits.ptr, h->step_fs.data(), sizeof(int32_t) * (B + 1),
+                                 cudaMemcpyHostToDevice, h->stream));
+  RNNTG_CUDA_TRY(h->finfo.ensure(sizeof(int32_t) * 4 * (total + B)));
+  RNNTG_CUDA_TRY(h->nodebest.ensure(sizeof(double) * (total * K + B)));
+  RNNTG_CUDA_TRY(h->nodectx.ensure(sizeof(int32_t) * (total * K + B)));
+  RNNTG_CUDA_TRY(h->lattice.ensure(sizeof(char) * 24 * std::max<int64_t>(int64_t{1} << 16, total * (2 * K + 8))));
+  RNNTG_CUDA_TRY(h->flag.ensure(16));
+  RNNTG_CUDA_TRY(cudaMemsetAsync(h->flag.ptr, 0, 16, h->stream));
+  RNNTG_CUDA_TRY(h->counters.ensure(sizeof(unsigned long long) * 16));
+  RNNTG_CUDA_TRY(cudaMemsetAsync(h->counters.ptr, 0, sizeof(unsigned long long) * 16, h->stream));
+  RNNTG_CUDA_TRY(h->tok.ensure(sizeof(int32_t) * std::max<int64_t>(1, total)));
+  RNNTG_CUDA_TRY(h->len.ensure(sizeof(int32_t) * std::max(1, B)));
+  RNNTG_CUDA_TRY(h->score.ensure(sizeof(double) * std::max(1, B)));
+  RNNTG_CUDA_TRY(h->step_state.ensure(sizeof(rnntg::FsaStepState) * std::max(1, B)));
+  std::vector<rnntg::FsaStepState> st(std::max(1, B));
+  for (int32_t i = 0; i < B; ++i) {
+    rnntg::FsaStepState& x = st[i];
+    std::memset(&x, 0, sizeof(x));
+    x.n_act = 1;  // ((0,0), state 0, score 0, node 0)
+    x.num_nodes = 1;
+    x.T = num_frames[i];
+  }
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(h->step_state.ptr, st.data(), sizeof(rnntg::FsaStepState) * std::max(1, B),
+                                 cudaMemcpyHostToDevice, h->stream));
+  RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  h->step_graph = graph;
+  h->step_params = *p;
+  h->step_open = true;
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_fsa_stream_contexts(rnntg_model_t h, int32_t* out_row_splits, int32_t capacity,
+                                       int32_t* out_contexts) {
+  Nvtx nvtx_range("rnntg_fsa_stream_contexts");
+  if (!h || !out_row_splits) return invalid("null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (!h->step_open) return invalid("no open FSA stream decode (rnntg_fsa_stream_begin)");
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  const int32_t B = static_cast<int32_t>(h->step_fs.size()) - 1;
+  std::vector<rnntg::FsaStepState> st(std::max(1, B));
+  if (B > 0)
+    RNNTG_CUDA_TRY(cudaMemcpy(st.data(), h->step_state.ptr, sizeof(rnntg::FsaStepState) * B,
+                              cudaMemcpyDeviceToHost));
+  // get_contexts (fsa_search.hpp:124-154): done streams contribute none.
+  std::vector<int32_t> ctx;
+  h->step_rows.assign(B + 1, 0);
+  h->step_nact.assign(B, 0);
+  for (int32_t i = 0; i < B; ++i) {
+    const rnntg::FsaStepState& x = st[i];
+    int32_t n = 0;
+    if (x.t < x.T) {
+      h->step_nact[i] = x.n_act;
+      for (int32_t j = 0; j < x.n_act; ++j)
+        if (j == 0 || x.act_ctx[j] != x.act_ctx[j - 1]) {
+          ctx.push_back(x.act_ctx[j]);
+          ++n;
+        }
+    }
+    h->step_rows[i + 1] = h->step_rows[i] + n;
+  }
+  std::memcpy(out_row_splits, h->step_rows.data(), sizeof(int32_t) * (B + 1));
+  h->step_have_rows = true;
+  if (capacity == 0) return RNNTG_OK;
+  if (capacity < static_cast<int32_t>(ctx.size()) || !out_contexts) return invalid("contexts capacity too small");
+  std::memcpy(out_contexts, ctx.data(), sizeof(int32_t) * ctx.size());
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_fsa_stream_step(rnntg_model_t h, const double* logprobs, int32_t mem) {
+  Nvtx nvtx_range("rnntg_fsa_stream_step");
+  if (!h) return invalid("null model");
+  if (mem != RNNTG_MEM_HOST && mem != RNNTG_MEM_DEVICE) return invalid("bad mem kind");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (!h->step_open) return invalid("no open FSA stream decode (rnntg_fsa_stream_begin)");
+  if (!h->step_have_rows) {  // expand_arcs without a fresh get_contexts
+    set_error("expand_arcs: stale get_contexts data");
+    return RNNTG_INTERNAL;
+  }
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  const int32_t B = static_cast<int32_t>(h->step_fs.size()) - 1;
+  const int64_t rows = h->step_rows[B];
+  if (rows > 0 && !logprobs) return invalid("logprobs is null");
+  // Lattice room for this frame's worst case (every candidate kept as an
+  // arc: n_act x (1 + out-degree) per stream); grown keeping the arcs so far.
+  unsigned long long used = 0;
+  RNNTG_CUDA_TRY(cudaMemcpy(&used, h->flag.as<char>() + 8, sizeof(used), cudaMemcpyDeviceToHost));
+  int64_t worst = 0;
+  for (int32_t i = 0; i < B; ++i) worst += static_cast<int64_t>(h->step_nact[i]) * (1 + h->step_graph->max_out);
+  const size_t need = static_cast<size_t>(used + worst) * 24;
+  if (need > h->lattice.bytes) RNNTG_CUDA_TRY(h->lattice.grow_keep(need * 2, used * 24, h->stream));
+  const double* P = logprobs;
+  if (mem == RNNTG_MEM_HOST && rows > 0) {
+    RNNTG_CUDA_TRY(h->step_P.ensure(sizeof(double) * rows * h->d.V));
+    RNNTG_CUDA_TRY(cudaMemcpyAsync(h->step_P.ptr, logprobs, sizeof(double) * rows * h->d.V, cudaMemcpyHostToDevice,
+                                   h->stream));
+    P = h->step_P.as<double>();
+  }
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(h->splits.ptr, h->step_fs.data(), sizeof(int32_t) * (B + 1),
+                                 cudaMemcpyHostToDevice, h->stream));  // the handle may have decoded meanwhile
+  RNNTG_CUDA_TRY(h->step_rsplits.ensure(sizeof(int32_t) * (B + 1)));
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(h->step_rsplits.ptr, h->step_rows.data(), sizeof(int32_t) * (B + 1),
+                                 cudaMemcpyHostToDevice, h->stream));
+  rnntg::FsaStepArgs a = step_args(h);
+  a.P = P;
+  RNNTG_CUDA_TRY(rnntg::launch_fsa_step(a, false, h->stream));
+  int32_t flag = 0;
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(&flag, h->flag.ptr, sizeof(flag), cudaMemcpyDeviceToHost, h->stream));
+  RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  h->step_have_rows = false;
+  if (flag) {
+    h->step_open = false;  // the decode state is no longer consistent
+    return fsa_flag_status(flag);
+  }
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_fsa_stream_end(rnntg_model_t h, int32_t* out_splits, int32_t* out_tokens, double* out_scores) {
+  Nvtx nvtx_range("rnntg_fsa_stream_end");
+  if (!h || !out_splits) return invalid("null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (!h->step_open) return invalid("no open FSA stream decode (rnntg_fsa_stream_begin)");
+  RNNTG_CUDA_TRY(cudaSetDevice(h->device));
+  const std::vector<int32_t> fs = h->step_fs;
+  const int32_t B = static_cast<int32_t>(fs.size()) - 1;
+  RNNTG_CUDA_TRY(h->splits.ensure(sizeof(int32_t) * (B + 1)));
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(h->splits.ptr, fs.data(), sizeof(int32_t) * (B + 1), cudaMemcpyHostToDevice,
+                                 h->stream));
+  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
+  RNNTG_CUDA_TRY(cudaEventRecord(h->ev[1], h->stream));
+  RNNTG_CUDA_TRY(rnntg::launch_fsa_step(step_args(h), true, h->stream));
+  int32_t flag = 0;
+  RNNTG_CUDA_TRY(cudaMemcpyAsync(&flag, h->flag.ptr, sizeof(flag), cudaMemcpyDeviceToHost, h->stream));
+  RNNTG_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (flag == 5) {
+    set_error("best_path trace failed (inconsistent scores)");
+    return RNNTG_INTERNAL;
+  }
+  h->pipelined = false;
+  rnntg_status st = finish(h, fs.data(), B, RNNTG_MEM_HOST, out_splits, out_tokens, out_scores, 1);
+  if (st) return st;
+  h->step_open = false;
+  h->last_fsa_fs = fs;
+  h->last_fsa_K = std::min(h->step_params.max_states, rnntg::kFsaMaxStates);
+  return RNNTG_OK;
 }
 
 rnntg_status rnntg_fsa_lattice(rnntg_model_t h, int32_t s, int32_t* num_nodes, int32_t* num_arcs,

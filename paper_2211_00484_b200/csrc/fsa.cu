@@ -26,6 +26,8 @@
 // (key -> max score, atomicMax on order-preserving integers), whose distinct
 // entries are bitonic-sorted.  This is exact, not approximate: every key with
 // max >= threshold is present with its true max.
+#include <algorithm>
+
 #include "decode_common.cuh"
 
 namespace rnntg {
@@ -589,6 +591,121 @@ __device__ __forceinline__ void fsa_frame(FsaStream& S, const Group& grp, const 
       grp.sync();
 }
 
+// lattice_to_best_seq(kMax) = best_path (fsa.hpp:311-376) on the stream's
+// HBM lattice, by the first warp of its thread group (lane < 32): backward
+// suffix maxima frame by frame (lanes over arcs, shared-memory atomicMax on
+// order-preserving bits; layer t+1 in S.act_score, layer t in S.hval, every
+// layer also in nb for the trace), then the forward trace taking the first
+// arc (lowest index) that attains the remainder (ballot over 32 arcs), next
+// frame prefetched.  S.flag / S.num_nodes are the stream's; its other fields
+// are scratch.
+__device__ __forceinline__ void fsa_best_path(FsaStream& S, int lane, const int4* __restrict__ finfo_s,
+                                              const LatArc* __restrict__ lat, double* __restrict__ nb, int32_t T,
+                                              int32_t* __restrict__ tokens_s, int32_t* __restrict__ length_s,
+                                              double* __restrict__ score_s, int32_t* __restrict__ error_flag) {
+    double* cur = S.act_score;                                      // layer t+1 suffix values
+    unsigned long long* nxt = reinterpret_cast<unsigned long long*>(S.hval);  // layer t (ordered bits)
+    int32_t len = 0;
+    double total = 0.0;
+    if (!(S.flag & 2)) {
+      const int32_t nn = S.num_nodes;
+      const int32_t lastb = T > 0 ? finfo_s[T - 1].z : 0;
+      for (int32_t n = lastb + lane; n < nn; n += 32) {
+        nb[n] = 0.0;  // layer T reaches the super-final node by a score-0 arc
+        cur[n - lastb] = 0.0;
+      }
+      __syncwarp();
+      // frame t-1's info and first 32 arcs are loaded while frame t is reduced
+      int4 fi_p = T > 0 ? finfo_s[T - 1] : make_int4(0, 0, 0, 0);
+      LatArc e_p{};
+      if (T > 0 && lane < fi_p.y) e_p = lat[static_cast<int64_t>(fi_p.x) + lane];
+      for (int32_t t = T - 1; t >= 0; --t) {
+        const int4 fi = fi_p;
+        const LatArc e0 = e_p;
+        if (t > 0) {
+          fi_p = finfo_s[t - 1];
+          if (lane < fi_p.y) e_p = lat[static_cast<int64_t>(fi_p.x) + lane];
+        }
+        const int32_t lb = t > 0 ? fi_p.z : 0;
+        const int32_t ln = t > 0 ? fi_p.w : 1;
+        for (int32_t i = lane; i < ln; i += 32) nxt[i] = 0ull;  // below ord_of(-inf)
+        __syncwarp();
+        for (int32_t a = lane; a < fi.y; a += 32) {
+          const LatArc e = a < 32 ? e0 : lat[static_cast<int64_t>(fi.x) + a];
+          atomicMax(&nxt[e.src - lb], ord_of(e.score + cur[e.dst - fi.z]));
+        }
+        __syncwarp();
+        for (int32_t i = lane; i < ln; i += 32) {
+          const double v = nxt[i] ? dbl_of(nxt[i]) : -INFINITY;
+          cur[i] = v;
+          nb[lb + i] = v;
+        }
+        __syncwarp();
+      }
+      double remaining = T > 0 ? nb[0] : 0.0;
+      if (remaining == -INFINITY || S.flag) {
+        total = -INFINITY;
+      } else {
+        int32_t n = 0;
+        LatArc e_n{};
+        double v_n = 0.0;
+        int4 fi_n = T > 0 ? finfo_s[0] : make_int4(0, 0, 0, 0);
+        if (T > 0 && lane < fi_n.y) {
+          e_n = lat[static_cast<int64_t>(fi_n.x) + lane];
+          v_n = nb[e_n.dst];
+        }
+        for (int32_t t = 0; t < T; ++t) {
+          const int4 fi = fi_n;
+          const LatArc e0 = e_n;
+          const double v0 = v_n;
+          if (t + 1 < T) {  // prefetch frame t+1's first 32 arcs and their suffix values
+            fi_n = finfo_s[t + 1];
+            if (lane < fi_n.y) {
+              e_n = lat[static_cast<int64_t>(fi_n.x) + lane];
+              v_n = nb[e_n.dst];
+            }
+          }
+          int32_t chosen = -1;
+          LatArc ce{};
+          for (int32_t a0 = 0; a0 < fi.y && chosen < 0; a0 += 32) {
+            LatArc e = e0;
+            double v = v0;
+            if (a0 > 0 && a0 + lane < fi.y) {
+              e = lat[static_cast<int64_t>(fi.x) + a0 + lane];
+              v = nb[e.dst];
+            }
+            const bool hit = a0 + lane < fi.y && e.src == n && e.score + v == remaining;
+            const unsigned ball = __ballot_sync(0xffffffffu, hit);
+            if (ball) {
+              const int src_lane = __ffs(ball) - 1;
+              chosen = a0 + src_lane;
+              ce.dst = __shfl_sync(0xffffffffu, e.dst, src_lane);
+              ce.label = __shfl_sync(0xffffffffu, e.label, src_lane);
+              ce.score = __shfl_sync(0xffffffffu, e.score, src_lane);
+              remaining = __shfl_sync(0xffffffffu, v, src_lane);
+            }
+          }
+          if (chosen < 0) {  // best_path "inconsistent scores"
+            if (lane == 0) atomicExch(error_flag, 5);
+            break;
+          }
+          if (ce.label != 0) {
+            if (lane == 0) tokens_s[len] = ce.label;
+            ++len;
+          }
+          total += ce.score;
+          n = ce.dst;
+        }
+        total += 0.0;  // the score-0 hop into the super-final node
+        total += 0.0;  // its final score
+      }
+    }
+    if (lane == 0) {
+      *length_s = len;
+      *score_s = (S.flag & 2) ? 0.0 : total;
+    }
+  }
+
 __global__ void __launch_bounds__(kDecodeThreads, 1)
     fsa_kernel(ModelView m, const float* __restrict__ pe, const int32_t* __restrict__ frame_splits,
                int32_t B, int32_t G, int32_t bk, const ArcRec* __restrict__ arcs,
@@ -746,111 +863,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   // frame's choice is made.
   const long long cb0 = clock64();
   __syncthreads();  // the frame loop's shared state is free from here on
-  if (have && grp.tid < 32) {
-    const int lane = grp.tid;
-    double* nb = nodebest + nbase;
-    double* cur = S.act_score;                                      // layer t+1 suffix values
-    unsigned long long* nxt = reinterpret_cast<unsigned long long*>(S.hval);  // layer t (ordered bits)
-    int32_t len = 0;
-    double total = 0.0;
-    if (!(S.flag & 2)) {
-      const int32_t nn = S.num_nodes;
-      const int32_t lastb = T > 0 ? finfo[fbase + T - 1].z : 0;
-      for (int32_t n = lastb + lane; n < nn; n += 32) {
-        nb[n] = 0.0;  // layer T reaches the super-final node by a score-0 arc
-        cur[n - lastb] = 0.0;
-      }
-      __syncwarp();
-      // frame t-1's info and first 32 arcs are loaded while frame t is reduced
-      int4 fi_p = T > 0 ? finfo[fbase + T - 1] : make_int4(0, 0, 0, 0);
-      LatArc e_p{};
-      if (T > 0 && lane < fi_p.y) e_p = lat[static_cast<int64_t>(fi_p.x) + lane];
-      for (int32_t t = T - 1; t >= 0; --t) {
-        const int4 fi = fi_p;
-        const LatArc e0 = e_p;
-        if (t > 0) {
-          fi_p = finfo[fbase + t - 1];
-          if (lane < fi_p.y) e_p = lat[static_cast<int64_t>(fi_p.x) + lane];
-        }
-        const int32_t lb = t > 0 ? fi_p.z : 0;
-        const int32_t ln = t > 0 ? fi_p.w : 1;
-        for (int32_t i = lane; i < ln; i += 32) nxt[i] = 0ull;  // below ord_of(-inf)
-        __syncwarp();
-        for (int32_t a = lane; a < fi.y; a += 32) {
-          const LatArc e = a < 32 ? e0 : lat[static_cast<int64_t>(fi.x) + a];
-          atomicMax(&nxt[e.src - lb], ord_of(e.score + cur[e.dst - fi.z]));
-        }
-        __syncwarp();
-        for (int32_t i = lane; i < ln; i += 32) {
-          const double v = nxt[i] ? dbl_of(nxt[i]) : -INFINITY;
-          cur[i] = v;
-          nb[lb + i] = v;
-        }
-        __syncwarp();
-      }
-      double remaining = T > 0 ? nb[0] : 0.0;
-      if (remaining == -INFINITY || S.flag) {
-        total = -INFINITY;
-      } else {
-        int32_t n = 0;
-        LatArc e_n{};
-        double v_n = 0.0;
-        int4 fi_n = T > 0 ? finfo[fbase] : make_int4(0, 0, 0, 0);
-        if (T > 0 && lane < fi_n.y) {
-          e_n = lat[static_cast<int64_t>(fi_n.x) + lane];
-          v_n = nb[e_n.dst];
-        }
-        for (int32_t t = 0; t < T; ++t) {
-          const int4 fi = fi_n;
-          const LatArc e0 = e_n;
-          const double v0 = v_n;
-          if (t + 1 < T) {  // prefetch frame t+1's first 32 arcs and their suffix values
-            fi_n = finfo[fbase + t + 1];
-            if (lane < fi_n.y) {
-              e_n = lat[static_cast<int64_t>(fi_n.x) + lane];
-              v_n = nb[e_n.dst];
-            }
-          }
-          int32_t chosen = -1;
-          LatArc ce{};
-          for (int32_t a0 = 0; a0 < fi.y && chosen < 0; a0 += 32) {
-            LatArc e = e0;
-            double v = v0;
-            if (a0 > 0 && a0 + lane < fi.y) {
-              e = lat[static_cast<int64_t>(fi.x) + a0 + lane];
-              v = nb[e.dst];
-            }
-            const bool hit = a0 + lane < fi.y && e.src == n && e.score + v == remaining;
-            const unsigned ball = __ballot_sync(0xffffffffu, hit);
-            if (ball) {
-              const int src_lane = __ffs(ball) - 1;
-              chosen = a0 + src_lane;
-              ce.dst = __shfl_sync(0xffffffffu, e.dst, src_lane);
-              ce.label = __shfl_sync(0xffffffffu, e.label, src_lane);
-              ce.score = __shfl_sync(0xffffffffu, e.score, src_lane);
-              remaining = __shfl_sync(0xffffffffu, v, src_lane);
-            }
-          }
-          if (chosen < 0) {  // best_path "inconsistent scores"
-            if (lane == 0) atomicExch(error_flag, 5);
-            break;
-          }
-          if (ce.label != 0) {
-            if (lane == 0) tokens[fs + len] = ce.label;
-            ++len;
-          }
-          total += ce.score;
-          n = ce.dst;
-        }
-        total += 0.0;  // the score-0 hop into the super-final node
-        total += 0.0;  // its final score
-      }
-    }
-    if (lane == 0) {
-      lengths[sidx] = len;
-      scores[sidx] = (S.flag & 2) ? 0.0 : total;
-    }
-  }
+  if (have && grp.tid < 32)
+    fsa_best_path(S, grp.tid, finfo + fbase, lat, nodebest + nbase, T, tokens + fs, lengths + sidx, scores + sidx,
+                  error_flag);
   if (grp.tid == 0 && have) atomicAdd(&counters[11], static_cast<unsigned long long>(clock64() - cb0));
   if (threadIdx.x == 0) {
     atomicAdd(&counters[8], static_cast<unsigned long long>(C.ph[0]));
@@ -869,9 +884,142 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// The Algorithm-1 step API (fsa_search.hpp:95-297, Algorithm 1):
+// the caller runs its own model between get_contexts and expand_arcs and
+// hands the log-prob rows in; the decoder's expand / prune (fsa_frame with
+// LpRows) and best path run on the GPU.  Stream state lives in HBM between
+// steps (StepState, the reference's DecodeStream minus the host vectors).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kDecodeThreads, 1) fsa_step_kernel(FsaStepArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int G = a.G;
+  FsaStream* SS = reinterpret_cast<FsaStream*>(smem_raw);
+  double* lpmax_all = reinterpret_cast<double*>(SS + G);  // [G][kMaxStates]
+  const int s0 = blockIdx.x * G;
+  const int ns = min(G, a.B - s0);
+  const int nt = kDecodeThreads / G;
+  const Group grp{static_cast<int>(threadIdx.x) / nt, static_cast<int>(threadIdx.x) % nt, nt};
+  const bool have = grp.id < ns;
+  if (!have) return;  // whole groups only: named barriers are per group
+  FsaStream& S = SS[grp.id];
+  double* lpmax = lpmax_all + grp.id * kMaxStates;
+  const int sidx = s0 + grp.id;
+  FsaStepState& X = static_cast<FsaStepState*>(a.state)[sidx];
+  const int32_t fs = a.frame_splits[sidx];
+  const int K = min(a.max_states, kMaxStates);
+  const int64_t fbase = static_cast<int64_t>(fs) + sidx;
+  const int64_t nbase = static_cast<int64_t>(fs) * K + sidx;
+  const int32_t t = X.t, T = X.T;
+  if (t >= T) return;  // done (finish_stream at its last frame)
+  if (grp.tid == 0) {
+    S.n_act = X.n_act;
+    S.num_nodes = X.num_nodes;
+    S.flag = X.flag;
+    S.raw_total = S.lat_total = 0;
+    if (t == 0) a.node_ctx[nbase] = 0;
+  }
+  grp.sync();
+  for (int i = grp.tid; i < S.n_act; i += nt) {
+    S.act_ctx[i] = X.act_ctx[i];
+    S.act_state[i] = X.act_state[i];
+    S.act_score[i] = X.act_score[i];
+    S.act_node[i] = X.act_node[i];
+  }
+  grp.sync();
+  // get_contexts (124-154): the caller's rows for this stream must be its
+  // distinct active contexts in order (else "stale get_contexts data")
+  if (grp.tid == 0) {
+    int nr = 0;
+    for (int i = 0; i < S.n_act; ++i) {
+      if (nr == 0 || S.row_ctx[nr - 1] != S.act_ctx[i]) S.row_ctx[nr++] = S.act_ctx[i];
+      S.act_row[i] = nr - 1;
+    }
+    S.nrows = nr;
+    S.row_base = a.row_splits[sidx];
+    if (a.row_splits[sidx + 1] - S.row_base != nr) atomicExch(a.error_flag, 7);
+  }
+  grp.sync();
+  if (a.row_splits[sidx + 1] - S.row_base != S.nrows) return;
+  // row maxima of the caller's rows (the frame's upper bound, fsa_frame)
+  for (int r = 0; r < S.nrows; ++r) {
+    const double* P = a.P + static_cast<int64_t>(S.row_base + r) * a.V;
+    double mx = -INFINITY;
+    for (int k = grp.tid; k < a.V; k += nt) mx = fmax(mx, P[k]);
+    mx = group_max(grp, S, mx);
+    if (grp.tid == 0) lpmax[r] = mx;
+  }
+  grp.sync();
+  const double scale = kBins / ((a.beam < 8.0 ? a.beam : 8.0) + 2.0);
+  fsa_frame(S, grp, LpRows{a.P, a.V}, lpmax - S.row_base, a.V, static_cast<const ArcRec*>(a.graph_arcs),
+            a.graph_splits, a.graph_maxw, a.beam, K, a.max_states, a.max_contexts, K + 32, scale,
+            static_cast<LatArc*>(a.lattice), a.lattice_cap, a.lattice_count,
+            reinterpret_cast<int4*>(a.lat_frame_info) + fbase + t, a.node_ctx + nbase, a.error_flag);
+  // back to HBM
+  for (int i = grp.tid; i < S.n_act; i += nt) {
+    X.act_ctx[i] = S.act_ctx[i];
+    X.act_state[i] = S.act_state[i];
+    X.act_score[i] = S.act_score[i];
+    X.act_node[i] = S.act_node[i];
+  }
+  if (grp.tid == 0) {
+    X.n_act = S.n_act;
+    X.num_nodes = S.num_nodes;
+    X.flag = S.flag;
+    X.t = t + 1;
+    atomicAdd(&a.counters[2], S.raw_total);
+    atomicAdd(&a.counters[3], S.lat_total);
+    atomicAdd(&a.counters[0], 1ull);
+  }
+}
+
+// finish_stream + lattice_to_best_seq(kMax) of every stream (the driver's
+// tail, fsa_search.hpp:375-387).
+__global__ void __launch_bounds__(kDecodeThreads, 1) fsa_step_finish_kernel(FsaStepArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int G = a.G;
+  FsaStream* SS = reinterpret_cast<FsaStream*>(smem_raw);
+  const int s0 = blockIdx.x * G;
+  const int ns = min(G, a.B - s0);
+  const int nt = kDecodeThreads / G;
+  const Group grp{static_cast<int>(threadIdx.x) / nt, static_cast<int>(threadIdx.x) % nt, nt};
+  if (grp.id >= ns) return;
+  FsaStream& S = SS[grp.id];
+  const int sidx = s0 + grp.id;
+  const FsaStepState& X = static_cast<const FsaStepState*>(a.state)[sidx];
+  const int32_t fs = a.frame_splits[sidx];
+  const int32_t T = a.frame_splits[sidx + 1] - fs;
+  const int K = min(a.max_states, kMaxStates);
+  const int64_t nbase = static_cast<int64_t>(fs) * K + sidx;
+  if (grp.tid == 0) {
+    S.flag = X.flag | (X.t < T ? 4 : 0);  // a stream stopped before its last frame has no complete path
+    S.num_nodes = X.num_nodes;
+    if (T == 0) a.node_ctx[nbase] = 0;
+  }
+  grp.sync();
+  if (grp.tid < 32)
+    fsa_best_path(S, grp.tid, reinterpret_cast<const int4*>(a.lat_frame_info) + fs + sidx,
+                  static_cast<const LatArc*>(a.lattice), a.node_best + nbase, T, a.tokens + fs, a.lengths + sidx,
+                  a.scores + sidx, a.error_flag);
+}
+
 }  // namespace
 
 size_t fsa_stream_smem() { return sizeof(FsaStream); }
+
+static int step_streams_per_cta(int K) { return K > 16 ? 2 : 4; }
+
+cudaError_t launch_fsa_step(FsaStepArgs a, bool finish, cudaStream_t s) {
+  if (a.B <= 0) return cudaSuccess;
+  const int K = std::min(a.max_states, kMaxStates);
+  a.G = step_streams_per_cta(K);
+  const size_t smem = sizeof(FsaStream) * a.G + (finish ? 0 : sizeof(double) * kMaxStates * a.G);
+  auto kern = finish ? fsa_step_finish_kernel : fsa_step_kernel;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  kern<<<(a.B + a.G - 1) / a.G, kDecodeThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s) {
   const ModelView m = view_of(*a.m);

@@ -66,6 +66,19 @@ struct Scratch {
     if (e == cudaSuccess) bytes = need;
     return e;
   }
+  // grow to `need` bytes keeping the first `keep` bytes (stream-ordered copy)
+  cudaError_t grow_keep(size_t need, size_t keep, cudaStream_t s) {
+    if (need <= bytes) return cudaSuccess;
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, need);
+    if (e != cudaSuccess) return e;
+    if (ptr && keep) e = cudaMemcpyAsync(p, ptr, keep, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (ptr) cudaFree(ptr);
+    ptr = p;
+    bytes = need;
+    return e;
+  }
   void release() {
     if (ptr) cudaFree(ptr);
     ptr = nullptr;
@@ -152,6 +165,39 @@ cudaError_t launch_decode_beam(const DecodeArgs& a, cudaStream_t s);
 int beam_cluster_streams(const DeviceModel& d, int32_t B, int32_t beam_size, int num_sms);
 cudaError_t launch_decode_beam_cluster(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_decode_fsa(const DecodeArgs& a, cudaStream_t s);
+
+// The FSA step API (fsa_search.hpp:95-297): per-stream state between steps
+// (the reference's DecodeStream without its host vectors) and one launch
+// per expand_arcs + prune_streams, or for the final best paths.
+struct FsaStepState {
+  int32_t n_act, num_nodes, t, T, flag, pad;
+  int32_t act_ctx[kFsaMaxStates], act_state[kFsaMaxStates], act_node[kFsaMaxStates];
+  double act_score[kFsaMaxStates];
+};
+struct FsaStepArgs {
+  int32_t B, G, V;
+  const int32_t* frame_splits;  // device [B+1]: each stream's num_frames, as splits
+  const int32_t* row_splits;    // device [B+1]: the caller's log-prob rows of this step per stream
+  const double* P;              // device [rows][V] log-prob rows (expand_arcs' logprobs)
+  const void* graph_arcs;
+  const int32_t* graph_splits;
+  const double* graph_maxw;
+  double beam;
+  int32_t max_states, max_contexts;
+  void* lattice;
+  int64_t lattice_cap;
+  unsigned long long* lattice_count;
+  int32_t* lat_frame_info;
+  double* node_best;
+  int32_t* node_ctx;
+  void* state;                  // device FsaStepState [B]
+  int32_t* tokens;              // device [sum T] (finish)
+  int32_t* lengths;             // device [B] (finish)
+  double* scores;               // device [B] (finish)
+  unsigned long long* counters; // device [16]
+  int32_t* error_flag;
+};
+cudaError_t launch_fsa_step(FsaStepArgs a, bool finish, cudaStream_t s);
 
 // lattice_to_best_seq(kLogAdd) (fsa_search.hpp:410-425) on the device
 // lattices of the last FSA decode (logadd.cu).

@@ -62,6 +62,14 @@ def main():
               -0.1 * np.arange(len(src), dtype=np.float64) / len(src))
     dec.fsa_beam_search(enc_r, rag, g, FsaParams(6.0, 16, 6))
     dec.fsa_lattice_text(0, header=True)
+    dec.fsa_lattice_best(nbest=20, seed=3)
+    # the step API, caller rows
+    dec.fsa_stream_begin(g, FsaParams(6.0, 16, 6), lens)
+    for t in range(max(lens)):
+        rs, ctx = dec.fsa_stream_contexts()
+        z = np.random.default_rng(t).normal(size=(len(ctx), V))
+        dec.fsa_stream_step(z - np.log(np.exp(z).sum(1, keepdims=True)))
+    dec.fsa_stream_end()
     log_softmax_lse(np.random.default_rng(0).normal(0, 3, (5, V)).astype(np.float32))
     f64_math("log1p", np.linspace(-0.5, 2.0, 100))
     dec.close()
