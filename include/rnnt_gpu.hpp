@@ -68,6 +68,7 @@ class Context {
     d.out_w = m.out_w.data.data();
     d.out_b = m.out_b.data.data();
     check(rnntg_model_create(&d, device, &h_));
+    vocab_ = m.cfg.vocab_size;
     rnntg_encoder_desc e{};
     e.feat_dim = m.cfg.feat_dim;
     e.enc_w1 = m.enc_w1.data.data();
@@ -87,6 +88,7 @@ class Context {
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
   rnntg_model_t handle() const { return h_; }
+  int32_t vocab_size() const { return vocab_; }
 
   // The device copy of `graph` (fsa.hpp:54-80), uploaded on first use and
   // reused by content (a 64-bit hash of the CSR, confirmed by Fsa equality).
@@ -130,6 +132,7 @@ class Context {
     return x;
   }
   rnntg_model_t h_ = nullptr;
+  int32_t vocab_ = 0;
   std::vector<Cached> graphs_;
 };
 
@@ -305,6 +308,72 @@ inline std::vector<Fsa> fsa_beam_search(Context& ctx, const ToyTransducer& m,
   }
   return out;
 }
+
+// The Algorithm-1 step API (fsa_search.hpp:95-297) on the GPU, with the
+// reference's types: construct = init_streams over one graph shared by all
+// streams; get_contexts() as rnnt::get_contexts; expand_and_prune(logprobs)
+// as expand_arcs + prune_streams (the caller's model output enters here,
+// 59-61); finish() = finish_stream + build_lattice for every stream (equal
+// to the reference's lattices), optionally with lattice_to_best_seq(kMax)
+// and best_path scores.  num_frames[i] is the frames stream i consumes (the
+// driver's DecodeStream::num_frames).  `graph` must outlive the object.
+class FsaStreams {
+ public:
+  FsaStreams(Context& ctx, const Fsa& graph, const FsaSearchParams& p, const std::vector<int32_t>& num_frames)
+      : ctx_(ctx), B_(static_cast<int32_t>(num_frames.size())), frames_(num_frames) {
+    rnntg_fsa_params fp{p.beam, p.max_states, p.max_contexts};
+    check(rnntg_fsa_stream_begin(ctx.handle(), ctx.graph(graph), &fp, B_, num_frames.data()));
+  }
+  std::pair<RaggedShape, Mat<int32_t>> get_contexts() {
+    std::vector<int32_t> splits(B_ + 1);
+    check(rnntg_fsa_stream_contexts(ctx_.handle(), splits.data(), 0, nullptr));
+    std::vector<int32_t> packed(std::max(1, splits[B_]));
+    check(rnntg_fsa_stream_contexts(ctx_.handle(), splits.data(), splits[B_], packed.data()));
+    std::vector<int32_t> counts(B_);
+    for (int32_t i = 0; i < B_; ++i) counts[i] = splits[i + 1] - splits[i];
+    Mat<int32_t> ctx(splits[B_], 2);
+    for (int32_t r = 0; r < splits[B_]; ++r) {
+      auto [a, b] = unpack_context(packed[r], vocab());
+      ctx.at(r, 0) = a;
+      ctx.at(r, 1) = b;
+    }
+    rows_ = splits[B_];
+    return {build_ragged(counts), std::move(ctx)};
+  }
+  void expand_and_prune(const Mat<double>& logprobs) {
+    if (logprobs.rows != rows_) throw std::logic_error("expand_arcs: log-prob rows != context count");
+    if (rows_ > 0 && logprobs.cols != vocab()) throw std::logic_error("expand_arcs: log-prob columns != vocab size");
+    check(rnntg_fsa_stream_step(ctx_.handle(), logprobs.data.data(), RNNTG_MEM_HOST));
+  }
+  std::vector<Fsa> finish(std::vector<std::vector<int32_t>>* best = nullptr, std::vector<double>* scores = nullptr) {
+    int64_t total = 0;
+    for (int32_t n : frames_) total += n;
+    std::vector<int32_t> splits(B_ + 1), toks(std::max<int64_t>(1, total));
+    std::vector<double> sc(std::max(1, B_));
+    check(rnntg_fsa_stream_end(ctx_.handle(), splits.data(), toks.data(), sc.data()));
+    if (best) *best = detail::unpack(splits, toks);
+    if (scores) scores->assign(sc.begin(), sc.begin() + B_);
+    std::vector<Fsa> out(B_);
+    for (int32_t k = 0; k < B_; ++k) {
+      int32_t nn = 0, na = 0;
+      check(rnntg_fsa_lattice(ctx_.handle(), k, &nn, &na, 0, nullptr, nullptr, nullptr, nullptr));
+      std::vector<int32_t> src(na), dst(na), lab(na);
+      std::vector<double> w(na);
+      check(rnntg_fsa_lattice(ctx_.handle(), k, &nn, &na, na, src.data(), dst.data(), lab.data(), w.data()));
+      std::vector<Arc> arcs(na);
+      for (int32_t a = 0; a < na; ++a) arcs[a] = {src[a], dst[a], lab[a], w[a]};
+      out[k] = make_fsa(nn, std::move(arcs), {{nn - 1, 0.0}});
+    }
+    return out;
+  }
+
+ private:
+  int32_t vocab() const { return ctx_.vocab_size(); }
+  Context& ctx_;
+  int32_t B_;
+  std::vector<int32_t> frames_;
+  int32_t rows_ = 0;
+};
 
 }  // namespace gpu
 }  // namespace rnnt

@@ -3,7 +3,9 @@
 // lattice_to_best_seq) and through rnnt::gpu (include/rnnt_gpu.hpp over
 // librnntg.so); outputs must be identical.  Built against the reference
 // headers by tests/cpp/Makefile; run on the GPU by tests/test_cpp_shim.py.
+#include <cmath>
 #include <cstdio>
+#include <random>
 #include <vector>
 
 #include "rnnt/fsa_search.hpp"
@@ -118,6 +120,52 @@ int main() {
     for (size_t i = 0; i < batch.size(); ++i)
       if (gb[i] != beam_search(m, batch[i], bp)) {
         std::printf("beam S=%d mismatch %zu\n", S, i);
+        ++bad;
+      }
+  }
+  // The step API with the reference's types, against the reference's own
+  // init_streams / get_contexts / expand_arcs / prune_streams on identical
+  // caller rows (random_logprob_rows style): equal contexts, equal lattices.
+  {
+    std::vector<int32_t> nf = {5, 0, 3};
+    FsaSearchParams sp2;
+    sp2.beam = 3.0;
+    sp2.max_states = 6;
+    sp2.max_contexts = 3;
+    gpu::FsaStreams gs(ctx, g, sp2, nf);
+    std::vector<Fsa> rgraphs(nf.size(), g);
+    std::vector<DecodeStream> rs = init_streams(rgraphs, sp2, cfg.vocab_size);
+    for (size_t i = 0; i < nf.size(); ++i) {
+      rs[i].num_frames = nf[i];
+      if (nf[i] == 0) detail::finish_stream(rs[i]);
+    }
+    std::mt19937_64 rng(17);
+    std::normal_distribution<double> nd(0.0, 1.0);
+    for (int32_t t = 0; t < 5; ++t) {
+      auto [gshape, gctx] = gs.get_contexts();
+      auto [rshape, rctx] = get_contexts(rs);
+      if (gshape.row_splits != rshape.row_splits || !(gctx == rctx)) {
+        std::printf("step contexts mismatch t=%d\n", t);
+        ++bad;
+        break;
+      }
+      Mat<double> lp(rctx.rows, cfg.vocab_size);
+      for (int32_t r = 0; r < lp.rows; ++r) {
+        double mx = -1e300, sum = 0.0;
+        for (int32_t k = 0; k < lp.cols; ++k) mx = std::max(mx, lp.at(r, k) = nd(rng));
+        for (int32_t k = 0; k < lp.cols; ++k) sum += std::exp(lp.at(r, k) - mx);
+        for (int32_t k = 0; k < lp.cols; ++k) lp.at(r, k) -= mx + std::log(sum);
+      }
+      gs.expand_and_prune(lp);
+      expand_arcs(rs, rshape, lp);
+      prune_streams(rs);
+      for (DecodeStream& s : rs)
+        if (!s.done && s.t == s.num_frames) detail::finish_stream(s);
+    }
+    std::vector<Fsa> glat = gs.finish();
+    for (size_t i = 0; i < nf.size(); ++i)
+      if (!(glat[i] == detail::build_lattice(rs[i]))) {
+        std::printf("step lattice mismatch %zu\n", i);
         ++bad;
       }
   }
