@@ -63,6 +63,7 @@ struct FsaStream {
   double act_score[kMaxStates];
   int32_t act_off[kMaxStates + 1];
   int32_t act_abase[kMaxStates];  // first CSR arc of the tuple's graph state
+  int32_t act_shift[kMaxStates];  // (ctx % V) * V: the tuple's context shifted for a token (a1)
   double ub;                      // upper bound on the frame's best candidate
   uint32_t mbits[kMaxRaw / 32];   // raw candidates that enter the lattice
   int32_t row_ctx[kMaxStates];
@@ -76,6 +77,9 @@ struct FsaStream {
   int32_t shnode[kSurvHash];
   double red_d[16];
   int32_t red_i[16];
+#if RNNTG_FSA_PASS_CLOCKS
+  long long pclk[8], pclk_last;
+#endif
 };
 
 struct FsaSmem {
@@ -201,7 +205,7 @@ __device__ __forceinline__ Raw raw_cand(const FsaStream& S, int q, const ArcRec*
     r.arc_score = src.lp(row, 0);
   } else {
     const ArcRec a = arcs[S.act_abase[lo] + j - 1];
-    r.ctx = (S.act_ctx[lo] % V) * V + a.label;
+    r.ctx = S.act_shift[lo] + a.label;
     r.state = a.dst;
     r.label = a.label;
     r.arc_score = a.w + src.lp(row, a.label);
@@ -247,7 +251,7 @@ __device__ __forceinline__ void raw_batch(const FsaStream& S, int q0, int stride
       r[u].label = 0;
       r[u].arc_score = src.lp(row, 0);
     } else {
-      r[u].ctx = (S.act_ctx[lo] % V) * V + a[u].label;
+      r[u].ctx = S.act_shift[lo] + a[u].label;
       r[u].state = a[u].dst;
       r[u].label = a[u].label;
       r[u].arc_score = a[u].w + src.lp(row, a[u].label);
@@ -269,6 +273,27 @@ __device__ __forceinline__ int ub_bin(double ub, double score, double scale) {
 // the new active set in S, the frame's lattice arcs in the pool, its frame
 // info in *finfo_t, the new nodes' contexts in nctx.  Shared by the decoder
 // (fsa_kernel, LpJoiner) and the step API (fsa_step_kernel, LpRows).
+// Development: RNNTG_FSA_PASS_CLOCKS=1 accumulates group 0's per-pass cycles
+// into fsa_pass_clk (read by tools/prof_fsa.py through rnntg_get_stats? no:
+// through the counters slots 12..15 and 5-7 at kernel end).
+#ifndef RNNTG_FSA_PASS_CLOCKS
+#define RNNTG_FSA_PASS_CLOCKS 0
+#endif
+#if RNNTG_FSA_PASS_CLOCKS
+#define FSA_MARK(i)                                   \
+  do {                                                \
+    if (grp.tid == 0 && grp.id == 0) {                \
+      const long long now_ = clock64();               \
+      S.pclk[i] += now_ - S.pclk_last;                \
+      S.pclk_last = now_;                             \
+    }                                                 \
+  } while (0)
+#else
+#define FSA_MARK(i) \
+  do {              \
+  } while (0)
+#endif
+
 template <class Src>
 __device__ __forceinline__ void fsa_frame(FsaStream& S, const Group& grp, const Src& src,
                                           const double* __restrict__ row_lpmax, int V,
@@ -293,6 +318,7 @@ __device__ __forceinline__ void fsa_frame(FsaStream& S, const Group& grp, const 
           const int st = S.act_state[i];
           const int a0 = gsplits[st], a1 = gsplits[st + 1];
           S.act_abase[i] = a0;
+          S.act_shift[i] = (S.act_ctx[i] % V) * V;
           cnt = 1 + a1 - a0;
           bound = S.act_score[i] + fmax(0.0, gmaxw[st]) + row_lpmax[S.row_base + S.act_row[i]];
         }
@@ -319,6 +345,7 @@ __device__ __forceinline__ void fsa_frame(FsaStream& S, const Group& grp, const 
       const int nraw = min(S.n_raw, kMaxRaw);
       const double ub = S.ub;
       if (grp.tid == 0) S.raw_total += nraw;
+      FSA_MARK(0);  // segment offsets, bound, clears
       // Pass A: the stream's best candidate and a histogram below `ub`.
       double mx = -INFINITY;
       for (int q0 = grp.tid; q0 < nraw; q0 += kU * nt) {
@@ -369,6 +396,7 @@ __device__ __forceinline__ void fsa_frame(FsaStream& S, const Group& grp, const 
         }
       }
       grp.sync();
+      FSA_MARK(1);  // pass A + threshold
       // Pass B: hot candidates into the hash; widen the threshold if
       // duplicates left fewer than K distinct keys.
       while (true) {
@@ -415,6 +443,7 @@ __device__ __forceinline__ void fsa_frame(FsaStream& S, const Group& grp, const 
         grp.sync();
       }
       if (grp.tid == 0 && S.n_hot > kHashCap * 3 / 4) atomicExch(error_flag, 3);
+      FSA_MARK(2);  // pass B
       // Compact the distinct keys; the first min(K, D) of them in (score
       // desc, key asc) order are found by rank (each entry counts the
       // entries before it: keys are distinct, so ranks are too) and land in
@@ -509,6 +538,7 @@ __device__ __forceinline__ void fsa_frame(FsaStream& S, const Group& grp, const 
       }
       grp.sync();
       // ---- lattice arcs: raw candidates into survivors, generation order ----
+      FSA_MARK(3);  // rank selection, prune, node ids
       // Pass C: one bit per raw candidate whose key survived.
       for (int q0 = grp.tid; q0 < nraw; q0 += kU * nt) {
         Raw rc[kU];
@@ -550,6 +580,7 @@ __device__ __forceinline__ void fsa_frame(FsaStream& S, const Group& grp, const 
       grp.sync();
       const int arc_off = S.arc_off;
       if (grp.tid == 0) S.lat_total += total;
+      FSA_MARK(4);  // pass C + scan
       // Pass D: only the (few) hits are recomputed and written.
       if (arc_off >= 0) {
         int pos = my_pos;
@@ -573,6 +604,7 @@ __device__ __forceinline__ void fsa_frame(FsaStream& S, const Group& grp, const 
         }
       }
       grp.sync();
+      FSA_MARK(5);  // pass D
       // New active set, sorted by (ctx, state).
       if (my_rank >= 0) {
         nctx[S.num_nodes + my_rank] = my_ctx;
@@ -764,6 +796,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     fence_mbar_init();
   }
   if (have && grp.tid == 0) S.raw_total = S.lat_total = 0;
+#if RNNTG_FSA_PASS_CLOCKS
+  if (have && grp.tid == 0)
+    for (int i = 0; i < 8; ++i) S.pclk[i] = 0;
+#endif
   load_exp_table(C.etab);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -840,6 +876,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     }
     __syncthreads();
 
+#if RNNTG_FSA_PASS_CLOCKS
+    if (live && grp.tid == 0) S.pclk_last = clock64();
+#endif
     if (live)
       fsa_frame(S, grp, LpJoiner{HL, C.row_lse, m.Vp}, C.row_lpmax, m.V, arcs, gsplits, gmaxw, beam, K, max_states,
                 max_contexts, M, scale, lat, lat_cap, lat_count, finfo + fbase + t, node_ctx + nbase, error_flag);
@@ -880,6 +919,13 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   }
   if (have && grp.tid == 0) {
     atomicAdd(&counters[2], S.raw_total);
+#if RNNTG_FSA_PASS_CLOCKS
+    if (grp.id == 0) {  // development: setup + pass A | pass B + prune | pass C + D
+      atomicAdd(&counters[5], static_cast<unsigned long long>(S.pclk[0] + S.pclk[1]));
+      atomicAdd(&counters[6], static_cast<unsigned long long>(S.pclk[2] + S.pclk[3]));
+      atomicAdd(&counters[7], static_cast<unsigned long long>(S.pclk[4] + S.pclk[5]));
+    }
+#endif
     atomicAdd(&counters[3], S.lat_total);
   }
 }
