@@ -1,6 +1,7 @@
 """Beam-search timing on the bench workload (reference-encoder frames in HBM),
 for A/B comparisons of builds / knobs and for ncu captures.  Usage: python tools/prof_beam.py [B] [T] [reps]"""
 import json
+import os
 import sys
 
 import torch
@@ -15,6 +16,8 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 w = bench.reference_weights()
 dec = Decoder(ModelWeights.from_dict(w))
 dec.set_encoder(w)
+if os.environ.get("RNNTG_PROF_BF16") == "1":  # the tcgen05 bf16 joiner variant
+    dec.set_joiner_mode("bf16")
 d_enc, splits = bench.synthetic_frames(dec, 0, B, T, "cuda:0")
 tok = torch.zeros(B * T, dtype=torch.int32, device="cuda")
 sc = torch.zeros(B, dtype=torch.float64, device="cuda")
