@@ -79,6 +79,7 @@ struct rnntg_model_s {
   rnntg_stats stats{};
   std::mutex mu;
   std::vector<void*> owned;  // device weight buffers
+  std::vector<rnntg_graph_t> graphs;  // live graphs bound to this model (detached on destroy)
 };
 
 struct rnntg_graph_s {
@@ -590,6 +591,13 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
 
 rnntg_status rnntg_model_destroy(rnntg_model_t h) {
   if (!h) return RNNTG_OK;
+  {
+    // graphs may outlive their model (destroyed later, in any order): they
+    // are detached and refuse further searches
+    std::lock_guard<std::mutex> lk(h->mu);
+    for (rnntg_graph_t g : h->graphs) g->model = nullptr;
+    h->graphs.clear();
+  }
   cudaSetDevice(h->device);
   if (h->own_stream) cudaStreamSynchronize(h->own_stream);
   for (void* p : h->owned) cudaFree(p);
@@ -882,8 +890,7 @@ rnntg_status rnntg_graph_create(rnntg_model_t h, int32_t num_states,
   }
   std::lock_guard<std::mutex> lk(h->mu);
   RNNTG_CUDA_TRY(cudaSetDevice(h->device));
-  auto* g = new rnntg_graph_s();
-  g->model = h;
+  auto* g = new rnntg_graph_s();  // bound to h once complete (error paths destroy it unbound)
   g->num_states = num_states;
   g->num_arcs = num_arcs;
   g->max_out = max_out;
@@ -912,6 +919,8 @@ rnntg_status rnntg_graph_create(rnntg_model_t h, int32_t num_states,
     }
     cudaMemcpy(g->maxw, mw.data(), sizeof(double) * num_states, cudaMemcpyHostToDevice);
   }
+  g->model = h;
+  h->graphs.push_back(g);
   *out = g;
   return RNNTG_OK;
 }
@@ -924,6 +933,8 @@ rnntg_status rnntg_graph_destroy(rnntg_graph_t g) {
       g->model->step_open = false;
       g->model->step_graph = nullptr;
     }
+    auto& gs = g->model->graphs;
+    gs.erase(std::remove(gs.begin(), gs.end(), g), gs.end());
   }
   if (g->arcs) cudaFree(g->arcs);
   if (g->splits) cudaFree(g->splits);

@@ -48,7 +48,7 @@ struct ClSmem {
   int32_t rb[kClRows];      // this frame: compact rows rebuilt (into Hr)
   int32_t rbflag[kClRows];  // this frame: row r reads Hr (else Hs[parity])
   int32_t nrow_s[kClRows];  // next frame: compact row -> stream slot
-  int32_t nrb, nR;
+  int32_t nrb, nR, nsp;
   long long chain_clk;      // thread 0: the logit chain part of the GEMM phase
 };
 
@@ -96,7 +96,7 @@ __host__ __device__ constexpr size_t cluster_smem_bytes(int J, int Vp) {
 // row r of `dst` in every CTA of the cluster, completing J*4 bytes per row on
 // each receiver's `bar`.  List entry q names compact row r = rows ? rows[q]
 // : q of stream slot row_s[r]; tid/nt enumerate whole warps.
-__device__ __forceinline__ void build_send_h(float* dst, uint64_t* bar, int JS, const float* PeS,
+__device__ __noinline__ void build_send_h(float* dst, uint64_t* bar, int JS, const float* PeS,
                                              const float* PdS, const float* JbS, int Sl, int rank,
                                              const int32_t* rows, const int32_t* row_s, int nq, int tid,
                                              int nt) {
@@ -221,8 +221,12 @@ __global__ void __launch_bounds__(kClThreads, 1)
     S.nfr[i] = i < ns ? frame_splits[s0 + i + 1] - frame_splits[s0 + i] : 0;
   }
   __syncthreads();
-  int32_t tmax = 0;
-  for (int i = 0; i < ns; ++i) tmax = max(tmax, S.nfr[i]);
+  int32_t tmax = 0, nfr_r[kClRows];
+#pragma unroll
+  for (int i = 0; i < kClRows; ++i) {
+    nfr_r[i] = S.nfr[i];  // 0 past ns
+    tmax = max(tmax, nfr_r[i]);
+  }
   // Asynchronous fetches of this CTA's slices: pe rows of frame t for the
   // slots live at t (into PeS[t & 1]), pd[ctx] for the slots whose context
   // moved.  Waited for at the top of the frame that reads them.
@@ -257,33 +261,44 @@ __global__ void __launch_bounds__(kClThreads, 1)
     const long long ca = clock64();
     const int par = t & 1;
     // rows of the live streams (compact, stream order); the ones not built
-    // ahead with the current context (rebuilt now); next frame's rows
+    // ahead with the current context (rebuilt now); next frame's rows.
+    // Warp 0, lane i = slot i, compacts them with ballots.
     int R = 0;
-    for (int i = 0; i < ns; ++i) R += t < S.nfr[i];
-    if (threadIdx.x == 0) {
-      int r = 0, nrb = 0, nsp = 0, rn = 0;
-      for (int i = 0; i < ns; ++i) {
-        if (t < S.nfr[i]) {
-          S.row_s[r] = i;
-          nsp += S.spec_t[i] == t;
-          const bool rebuild = S.spec_t[i] != t || S.spec_ctx[i] != S.ctx[i];
-          S.rbflag[r] = rebuild;
-          if (rebuild) S.rb[nrb++] = r;
-          ++r;
-        }
-        if (t + 1 < S.nfr[i]) S.nrow_s[rn++] = i;
+#pragma unroll
+    for (int i = 0; i < kClRows; ++i) R += t < nfr_r[i];
+    if (warp == 0) {
+      const int i = lane;
+      const bool live = i < ns && t < S.nfr[i];
+      const bool ahead = live && S.spec_t[i] == t;
+      const bool rebuild = live && !(ahead && S.spec_ctx[i] == S.ctx[i]);
+      const bool nlive = i < ns && t + 1 < S.nfr[i];
+      const unsigned lt = (1u << lane) - 1u;
+      const unsigned mlive = __ballot_sync(0xffffffffu, live), mrb = __ballot_sync(0xffffffffu, rebuild);
+      const unsigned mnext = __ballot_sync(0xffffffffu, nlive), mahead = __ballot_sync(0xffffffffu, ahead);
+      if (live) {
+        const int r = __popc(mlive & lt);
+        S.row_s[r] = i;
+        S.rbflag[r] = rebuild;
+        if (rebuild) S.rb[__popc(mrb & lt)] = r;
       }
-      S.nrb = nrb;
-      S.nR = rn;
-      // this frame's deliveries: rows built ahead (sent last frame) and rows
-      // rebuilt now, J*4 bytes each; R slice maxima from each CTA
-      mbar_expect_tx(&S.hbar[par], static_cast<uint32_t>((nsp + nrb) * J * 4));
-      mbar_expect_tx(&S.xbar[par], static_cast<uint32_t>(r * kCl * sizeof(uint2)));
+      if (nlive) S.nrow_s[__popc(mnext & lt)] = i;
+      if (lane == 0) {
+        S.nrb = __popc(mrb);
+        S.nR = __popc(mnext);
+        S.nsp = __popc(mahead);
+      }
     }
     rows_total += R;
     cp_async_wait_all();
     __syncthreads();
     if (threadIdx.x < ns) S.pd_ctx[threadIdx.x] = S.ctx[threadIdx.x];
+    if (threadIdx.x == (R == 1 ? 128 : kClThreads - 32)) {
+      // this frame's deliveries (armed off thread 0's path, by a warp with no
+      // logit rows when R = 1): rows built ahead (sent last frame) and rows
+      // rebuilt now, J*4 bytes each; R slice maxima from each CTA
+      mbar_expect_tx(&S.hbar[par], static_cast<uint32_t>((S.nsp + S.nrb) * J * 4));
+      mbar_expect_tx(&S.xbar[par], static_cast<uint32_t>(R * kCl * sizeof(uint2)));
+    }
     const int nrb = S.nrb;
     if (nrb > 0) {
       build_send_h(Hr, &S.hbar[par], JS, PeS + par * kClRows * Sl, PdS, JbS, Sl, rank, S.rb, S.row_s, nrb,

@@ -133,6 +133,26 @@ def test_fsa_invalid_params(big):
         Graph(dec, 1, np.array([0, 1], np.int32), np.zeros(1, np.int32), np.array([500], np.int32), np.zeros(1))
 
 
+def test_graph_outlives_its_model():
+    """A graph destroyed after its model (any order, as garbage collection
+    goes) is detached, not a use-after-free; a second model refuses it."""
+    from paper_2211_00484_b200.api import Decoder, FsaParams, Graph, ValidationError
+
+    m = H.ref().model(6, 4, 8, 8, 8, 3, -0.5)
+    dec, dec2 = Decoder(H.api_weights(m.w)), Decoder(H.api_weights(m.w))
+    g = Graph.trivial(dec)
+    g2 = Graph.trivial(dec)
+    _, enc, splits = H.frames(m, [5, 3], seed0=11)
+    with pytest.raises(ValidationError):
+        dec2.fsa_beam_search(enc, splits, g, FsaParams(4.0, 8, 4))
+    dec.close()
+    del g  # after its model
+    with pytest.raises(ValidationError):
+        dec2.fsa_beam_search(enc, splits, g2, FsaParams(4.0, 8, 4))
+    g2.__del__()
+    dec2.close()
+
+
 def test_lattice_pool_overflow_regrows_and_device_frames(big, monkeypatch):
     """A lattice pool far too small for the call: every stream's lattice
     overflows, best path is skipped for the incomplete lattices, the host
