@@ -1358,17 +1358,21 @@ cudaError_t launch_beam_multi(const DecodeArgs& a, cudaStream_t s) {
 // streams:
 //  - CTA c keeps out_w columns [64c, 64c+64) resident in shared memory for
 //    the whole utterance (no weight traffic after the first frame);
-//  - every CTA builds the h rows of the cluster's joiner rows (<= 64, in
-//    passes of 32) and computes its column slice of their logits (thread =
-//    column x 4 rows, sequential FMUL/FADD in k, the reference's order);
-//  - row r's slices are pushed into CTA (r mod 8)'s shared memory (DSMEM),
-//    which reduces it: exact normaliser (lse_cta_exps / lse_cta_chain) with
-//    the top-`beam` tokens picked meanwhile, results pushed to CTA 0;
+//  - the cluster builds the h rows of its joiner rows (<= 64, in passes of
+//    32) together: CTA c evaluates k in [cJ/8, (c+1)J/8) of every row and
+//    stores the slice into every CTA (16-byte st.async completing an
+//    mbarrier transaction, no cluster barrier);
+//  - every CTA computes its column slice of the logits (thread = column x
+//    up to 4 rows, k-contiguous LDS.128 operands, sequential FMUL/FADD in
+//    k, the reference's order); row r's slices go to CTA (r mod 8) by
+//    st.async, which reduces it: exact normaliser (lse_cta_exps /
+//    lse_cta_chain) with the top-`beam` tokens picked meanwhile, results
+//    pushed to CTA 0;
 //  - CTA 0 runs the beam steps (warp per stream: the persistent kernel's
 //    beam_stream_step) and the next frame's rows; the others read the row
 //    table back through DSMEM.
-// Three cluster barriers per frame.  Same arithmetic as the persistent
-// kernel (identical tokens, bit-equal scores).
+// Two cluster barriers per frame (three with a second pass).  Same
+// arithmetic as the persistent kernel (identical tokens, bit-equal scores).
 // ---------------------------------------------------------------------------
 constexpr int kBc = 8;            // CTAs per cluster (portable maximum)
 constexpr int kBcCols = 64;       // out_w columns per CTA (Vp = 512)
@@ -1377,6 +1381,8 @@ constexpr int kBcPass = 32;       // rows per h / GEMM pass
 constexpr int kBcLocal = kBcRows / kBc;  // rows reduced per CTA
 
 struct BcSmem {
+  uint64_t hbar;  // this pass's h slices from every CTA have landed
+  uint64_t lbar;  // this frame's logit slices of the rows reduced here have landed
   uint64_t etab[256];
   unsigned long long stat[8];
   int32_t R;
@@ -1407,9 +1413,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int rank = static_cast<int>(cluster.block_rank());
   const int cl = blockIdx.x / kBc;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* Ws = reinterpret_cast<float*>(smem_raw);      // [J][64] k-major out_w slice
-  float* Hs = Ws + m.J * kBcCols;                      // [J][32] k-major h rows (scratch after the GEMM)
-  float* recv = Hs + m.J * kBcPass;                    // [kBcLocal][Vp] logits of the rows reduced here
+  const int JS = m.J + 4;     // k-contiguous rows, +4 floats: 16-byte column reads spread over the banks
+  const int Sl = m.J / kBc;   // this CTA's k-slice of every h row
+  float* Ws = reinterpret_cast<float*>(smem_raw);      // [64][J+4] out_w column slice, column-major
+  float* Hs = Ws + kBcCols * JS;                       // [32][J+4] h rows of a pass (scratch after the GEMM)
+  float* recv = Hs + kBcPass * JS;                     // [kBcLocal][Vp] logits of the rows reduced here
   BcSmem& S = *reinterpret_cast<BcSmem*>(recv + kBcLocal * m.Vp);
   Hyps* H = reinterpret_cast<Hyps*>(&S + 1);            // CTA 0: [G]
   BcSmem& S0 = *cluster.map_shared_rank(&S, 0);
@@ -1422,7 +1430,12 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const int c0 = rank * kBcCols;
   for (int x = threadIdx.x; x < m.J * kBcCols; x += kDecodeThreads) {
     const int k = x / kBcCols, c = x - k * kBcCols;
-    Ws[x] = m.out_wt[static_cast<int64_t>(k) * m.Vp + c0 + c];
+    Ws[c * JS + k] = m.out_wt[static_cast<int64_t>(k) * m.Vp + c0 + c];
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&S.hbar, 1);
+    mbar_init(&S.lbar, 1);
+    fence_mbar_init();
   }
   load_exp_table(S.etab);
   if (threadIdx.x < 8) S.stat[threadIdx.x] = 0;
@@ -1450,6 +1463,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
   const RowRes rr0{S.row_lse, S.row_l0, S.row_tl, S.row_tk};
   const RowRes rloc{S.loc_lse, S.loc_l0, S.loc_tl, S.loc_tk};
   long long ph[4] = {0, 0, 0, 0};  // thread 0: h + GEMM + push, reduce, beam step, cluster-barrier waits
+  const float bias = m.out_b[c0 + (threadIdx.x & (kBcCols - 1))];  // this thread's column
+  uint32_t hph = 0;  // h passes so far (the hbar phase)
   for (int32_t t = 0; t < tmax; ++t) {
     const long long ca = clock64();
     // row table from CTA 0
@@ -1469,105 +1484,86 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(pe + static_cast<int64_t>(f + t + 1) * m.J + c0));
     }
     // h rows and this CTA's column slice of their logits, 32 rows a pass.
-    // h: CTA c builds k in [64c, 64c+64) of every row of the pass (unit = 4
-    // rows at one k: scalar gathers, four tanhf, one 16-byte store into each
-    // CTA's Hs) -- the gathers and tanhf are split 8 ways, not replicated.
-    // Hs slot of pass row lr: (lr % 8) * 4 + lr / 8, so thread group q's
-    // rows q, q+8, q+16, q+24 are one 16-byte load.  GEMM: thread = column
-    // c x group q (all 16 warps busy for R >= 8); row r's logit slice goes
-    // to CTA r % 8 (local row r / 8).
+    // h: unit = 2 consecutive k of one row (float2 gathers, two tanhf in
+    // flight); lane pairs form 4-k quads, each lane stores the quad into four
+    // of the eight CTAs.  GEMM: thread = column c x group q, rows q, q+8,
+    // q+16, q+24 of the pass (all 16 warps busy for R >= 8); row r's logit
+    // slice goes to CTA r % 8 (local row r / 8).
+    const int nloc = R > rank ? (R - rank + kBc - 1) / kBc : 0;
+    if (threadIdx.x == 0) mbar_expect_tx(&S.lbar, static_cast<uint32_t>(nloc * m.Vp * 4));
     const int c = threadIdx.x & (kBcCols - 1), q = threadIdx.x / kBcCols;
     for (int p0 = 0; p0 < R; p0 += kBcPass) {
       const int Rp = min(kBcPass, R - p0);
       if (p0 > 0) cluster.sync();  // every CTA is done reading the previous pass's Hs
+      if (threadIdx.x == 0) mbar_expect_tx(&S.hbar, static_cast<uint32_t>(Rp * m.J * 4));
       {
-        const int units = kBcCols * min(8, Rp);  // (k, slot group g: rows g, g+8, g+16, g+24)
-        for (int x = threadIdx.x; x < units; x += kDecodeThreads) {
-          const int g = x / kBcCols, kk = c0 + (x - g * kBcCols);  // slots 4g .. 4g+3
-          float v[4];
+        const int half = Sl / 2, n2 = Rp * half;
+        for (int base = 0; base < n2; base += kDecodeThreads) {  // uniform trip count: shuffles below
+          const int x = base + threadIdx.x;
+          const bool ok = x < n2;  // pairs (x, x ^ 1) are both in or both out (n2 even)
+          const int lr = ok ? x / half : 0, k = rank * Sl + (x - lr * half) * 2;
+          float v[2] = {0.5f, 0.5f};
+          if (ok) {
+            const int r = p0 + lr;
+            const float2 a = *reinterpret_cast<const float2*>(pe + S.row_pe[r] * m.J + k);
+            const float2 b = *reinterpret_cast<const float2*>(m.pd + static_cast<int64_t>(S.row_ctx[r]) * m.J + k);
+            const float2 jb = *reinterpret_cast<const float2*>(m.j_b + k);
+            v[0] = fadd(fadd(a.x, b.x), jb.x);
+            v[1] = fadd(fadd(a.y, b.y), jb.y);
+          }
+          float z[2];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int lr = (4 * g + j) % 4 * 8 + (4 * g + j) / 4;  // slot -> pass row
-            if (lr < Rp) {
-              const int r = p0 + lr;
-              v[j] = fadd(fadd(pe[S.row_pe[r] * m.J + kk], m.pd[static_cast<int64_t>(S.row_ctx[r]) * m.J + kk]),
-                          m.j_b[kk]);
-            } else {
-              v[j] = 0.0f;
+          for (int j = 0; j < 2; ++j) z[j] = rnntg_exact::tanhf_main(v[j]);
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            if (!rnntg_exact::tanhf_main_path(v[j])) z[j] = rnntg_exact::tanhf_glibc(v[j]);
+          const float o0 = __shfl_xor_sync(0xffffffffu, z[0], 1), o1 = __shfl_xor_sync(0xffffffffu, z[1], 1);
+          if (ok) {
+            const bool odd = x & 1;
+            const uint32_t dst = smem_u32(Hs + lr * JS + (k & ~3)), bar = smem_u32(&S.hbar);
+            const float q0 = odd ? o0 : z[0], q1 = odd ? o1 : z[1], q2 = odd ? z[0] : o0, q3 = odd ? z[1] : o1;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t d = (odd ? 4 : 0) + e;
+              st_async_v4(mapa(dst, d), q0, q1, q2, q3, mapa(bar, d));
             }
           }
-          float z[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) z[j] = rnntg_exact::tanhf_main(v[j]);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (!rnntg_exact::tanhf_main_path(v[j])) z[j] = rnntg_exact::tanhf_glibc(v[j]);
-          const float4 z4 = make_float4(z[0], z[1], z[2], z[3]);
-#pragma unroll
-          for (int d = 0; d < kBc; ++d)
-            *reinterpret_cast<float4*>(cluster.map_shared_rank(Hs, d) + kk * kBcPass + 4 * g) = z4;
         }
       }
-      cluster.sync();  // every h piece in place
+      mbar_wait(&S.hbar, hph & 1u);  // every CTA's h slices of this pass have landed
+      ++hph;
       if (threadIdx.x == 0) S.stat[5] += clock64() - ca;
       const int nr = q < Rp ? (Rp - q + 7) / 8 : 0;  // rows q, q+8, ... of this pass
       if (nr > 0) {
         float acc[4];
-        const float bias = m.out_b[c0 + c];
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[j] = bias;
-        const float* hq = Hs + 4 * q;
-        if (nr == 4) {
-#pragma unroll 4
-          for (int k = 0; k < m.J; ++k) {
-            const float w = Ws[k * kBcCols + c];
-            const float4 h4 = *reinterpret_cast<const float4*>(hq + k * kBcPass);
-            acc[0] = fadd(acc[0], fmul(w, h4.x));
-            acc[1] = fadd(acc[1], fmul(w, h4.y));
-            acc[2] = fadd(acc[2], fmul(w, h4.z));
-            acc[3] = fadd(acc[3], fmul(w, h4.w));
-          }
-        } else if (nr == 3) {
-#pragma unroll 4
-          for (int k = 0; k < m.J; ++k) {
-            const float w = Ws[k * kBcCols + c];
-            const float4 h4 = *reinterpret_cast<const float4*>(hq + k * kBcPass);
-            acc[0] = fadd(acc[0], fmul(w, h4.x));
-            acc[1] = fadd(acc[1], fmul(w, h4.y));
-            acc[2] = fadd(acc[2], fmul(w, h4.z));
-          }
-        } else if (nr == 2) {
-#pragma unroll 4
-          for (int k = 0; k < m.J; ++k) {
-            const float w = Ws[k * kBcCols + c];
-            const float2 h2 = *reinterpret_cast<const float2*>(hq + k * kBcPass);
-            acc[0] = fadd(acc[0], fmul(w, h2.x));
-            acc[1] = fadd(acc[1], fmul(w, h2.y));
-          }
-        } else {
-#pragma unroll 4
-          for (int k = 0; k < m.J; ++k) acc[0] = fadd(acc[0], fmul(Ws[k * kBcCols + c], hq[k * kBcPass]));
-        }
+        const float* wc = Ws + c * JS;
+        const float* hq = Hs + q * JS;
+        if (nr == 4) logit_chain_rows<4, 2>(wc, hq, 8 * JS, m.J, acc);
+        else if (nr == 3) logit_chain_rows<3, 2>(wc, hq, 8 * JS, m.J, acc);
+        else if (nr == 2) logit_chain_rows<2, 4>(wc, hq, 8 * JS, m.J, acc);
+        else logit_chain_rows<1, 4>(wc, hq, 8 * JS, m.J, acc);
+        const int d = (p0 + q) % kBc;  // rows q + 8j all go to one CTA
+        const uint32_t lb = mapa(smem_u32(&S.lbar), d);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (j < nr) {
             const int r = p0 + q + 8 * j;
-            float* dst = cluster.map_shared_rank(recv, r % kBc);
-            dst[(r / kBc) * m.Vp + c0 + c] = acc[j];
+            st_async_b32(mapa(smem_u32(recv + (r / kBc) * m.Vp + c0 + c), d), acc[j], lb);
           }
         }
       }
     }
     const long long cb = clock64();
     if (threadIdx.x == 0) S.stat[6] += cb - ca;
-    cluster.sync();  // every slice delivered
+    mbar_wait(&S.lbar, static_cast<uint32_t>(t & 1));  // every slice of the rows reduced here delivered
     const long long cc = clock64();
     // reduce the rows r = rank + 8 i
-    const int nloc = R > rank ? (R - rank + kBc - 1) / kBc : 0;
     double* E = reinterpret_cast<double*>(Hs);
-    lse_cta_exps(recv, E, kBcPass * m.J / 2, m.Vp, m.V, nloc, S.etab, S.loc_m);
+    lse_cta_exps(recv, E, kBcPass * JS / 2, m.Vp, m.V, nloc, S.etab, S.loc_m);
     if (warp == 0) {
-      lse_cta_chain(recv, E, kBcPass * m.J / 2, m.Vp, m.V, nloc, S.loc_m, S.loc_lse, S.loc_l0);
+      lse_cta_chain(recv, E, kBcPass * JS / 2, m.Vp, m.V, nloc, S.loc_m, S.loc_lse, S.loc_l0);
     } else if (warp - 1 < nloc) {
       beam_row_reduce_n<BCAP, 1, false>(recv, m.Vp, m.V, beam, warp - 1, nloc, rloc, S.etab);
     }
@@ -1593,18 +1589,21 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
                                length_norm, max_total, rr0, tokens, lengths + s0 + i, scores + s0 + i, &S.stat[4]);
       }
       __syncthreads();
+      if (threadIdx.x == 0) S.stat[7] += clock64() - ce;  // the beam steps alone
       if (warp == 0) {
         const int Rn = beam_rows(H, ns, frame_splits + s0, t + 1, S.row_pe, S.row_ctx);
         if (lane == 0) {
           S.R = Rn;
           S.stat[1] += R;
         }
+#ifdef RNNTG_BC_PD_PREFETCH
         // the next frame's decoder-table rows into L2 (each CTA gathers a
         // 256-byte segment of every row): a head start on the h build
         for (int x = lane; x < Rn * (m.J / 32); x += 32) {
           const int r = x / (m.J / 32), l = x - r * (m.J / 32);
           asm volatile("prefetch.global.L2 [%0];" ::"l"(m.pd + static_cast<int64_t>(S.row_ctx[r]) * m.J + l * 32));
         }
+#endif
       }
     }
     const long long cf = clock64();
@@ -1631,13 +1630,14 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
     atomicAdd(&counters[4], S.stat[4]);
     for (int i = 0; i < 4; ++i) atomicAdd(&counters[8 + i], static_cast<unsigned long long>(ph[i]));
     atomicAdd(&counters[6], S.stat[5]);  // h build (diagnostic, gather_cycles slot)
+    atomicAdd(&counters[7], S.stat[7]);  // beam steps (diagnostic, gemm_wait_cycles slot)
   }
   cluster.sync();  // no CTA leaves while others may still read its shared memory
 }
 
 template <int BCAP>
 size_t beam_cluster_smem(const ModelView& m, int G) {
-  return static_cast<size_t>(m.J) * (kBcCols + kBcPass) * 4 + static_cast<size_t>(kBcLocal) * m.Vp * 4 +
+  return static_cast<size_t>(m.J + 4) * (kBcCols + kBcPass) * 4 + static_cast<size_t>(kBcLocal) * m.Vp * 4 +
          sizeof(BcSmem) + sizeof(Hyps) * G;
 }
 
@@ -1744,7 +1744,8 @@ size_t beam_state_bytes() { return sizeof(Hyps); }
 
 int beam_cluster_streams(const DeviceModel& d, int32_t B, int32_t beam_size, int num_sms) {
   // streams per cluster when the cluster kernel serves this batch, else 0
-  if (d.Vp != kBc * kBcCols || d.V > kDecodeThreads || B <= 0 || beam_size > kMaxBeam) return 0;
+  if (d.Vp != kBc * kBcCols || d.V > kDecodeThreads || d.J % (4 * kBc) != 0 || B <= 0 || beam_size > kMaxBeam)
+    return 0;
   // clusters that can be resident at once (8 co-scheduled SMs of one GPC each)
   static int resident = -1;
   if (resident < 0) {
@@ -1767,11 +1768,12 @@ int beam_cluster_streams(const DeviceModel& d, int32_t B, int32_t beam_size, int
     resident = n > 0 ? n : num_sms / kBc;
   }
   const int nmax = std::min(resident, num_sms / kBc);
-  // up to 12 streams a cluster: beyond, the one-CTA beam steps of CTA 0 and
-  // the second h / GEMM pass make the persistent kernel faster (measured:
-  // B = 64 / 128 / 192 / 240 at T = 1000: 27.3 / 31.6 / 38.9 / 49.3 ms
-  // against 33.4 / 33.5 / 40.4 / 40.2 ms)
-  const int gmax = std::min(12, kBcRows / std::max(1, beam_size));
+  // up to 14 streams a cluster (~31 joiner rows: one h / GEMM pass); beyond,
+  // the second pass and the one-CTA beam steps of CTA 0 make the persistent
+  // kernel as fast (measured at T = 1000, cluster vs persistent: B = 64 /
+  // 128 / 160 / 192: 21.7 / 27.4 / 29.7 / 32.5 ms against 33.4 / 33.5 / - /
+  // 40.5 ms; B = 240 at 16 a cluster: 40.5 against 40.2 ms)
+  const int gmax = std::min(14, kBcRows / std::max(1, beam_size));
   if (B > nmax * gmax) return 0;
   const int G = (B + nmax - 1) / nmax;
   const ModelView m = view_of(d);

@@ -90,6 +90,86 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------------------
+// Asynchronous copies and cluster (DSMEM) stores.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+// DSMEM address of the same shared variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// Stores into another CTA's shared memory that complete their byte count on
+// that CTA's mbarrier (no cluster barrier needed).
+__device__ __forceinline__ void st_async_v2(uint32_t dst, uint32_t a, uint32_t b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(dst),
+               "r"(a), "r"(b), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t dst, float a, float b, float c, float d, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   dst),
+               "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(c)), "r"(__float_as_uint(d)),
+               "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void st_async_b32(uint32_t dst, float a, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst),
+               "r"(__float_as_uint(a)), "r"(bar)
+               : "memory");
+}
+
+// acc[j] += w[k] * h_j[k] for k = 0..J-1 in order (FMUL, then FADD: the
+// reference's sequential sum) for NR rows h_j = h0 + j * hstep sharing the
+// column wc (both k-contiguous, 16-byte aligned).  Operands come 4 k per
+// LDS.128; the next U*4 k are loaded while the current ones run, so the
+// shared-memory latency hides under the FADD chains.  J % (4U) == 0.
+template <int NR, int U>
+__device__ __forceinline__ void logit_chain_rows(const float* wc, const float* h0, int hstep, int J, float* acc) {
+  float4 w[U], h[NR][U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    w[u] = *reinterpret_cast<const float4*>(wc + 4 * u);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) h[j][u] = *reinterpret_cast<const float4*>(h0 + j * hstep + 4 * u);
+  }
+  for (int k = 0; k < J; k += 4 * U) {
+    const int kn = min(k + 4 * U, J - 4 * U);  // the last block reloads itself
+    float4 wn[U], hn[NR][U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      wn[u] = *reinterpret_cast<const float4*>(wc + kn + 4 * u);
+#pragma unroll
+      for (int j = 0; j < NR; ++j) hn[j][u] = *reinterpret_cast<const float4*>(h0 + j * hstep + kn + 4 * u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int j = 0; j < NR; ++j) acc[j] = fadd(acc[j], fmul(w[u].x, h[j][u].x));
+#pragma unroll
+      for (int j = 0; j < NR; ++j) acc[j] = fadd(acc[j], fmul(w[u].y, h[j][u].y));
+#pragma unroll
+      for (int j = 0; j < NR; ++j) acc[j] = fadd(acc[j], fmul(w[u].z, h[j][u].z));
+#pragma unroll
+      for (int j = 0; j < NR; ++j) acc[j] = fadd(acc[j], fmul(w[u].w, h[j][u].w));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      w[u] = wn[u];
+#pragma unroll
+      for (int j = 0; j < NR; ++j) h[j][u] = hn[j][u];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Weight chunk pipeline.  Chunk g (a running sequence number across frames)
 // lives in stage g & 1.  The sequence is data independent and periodic:
 // optionally a_nc chunks of matrix A (the fused encoder projection j_we^T,
