@@ -9,6 +9,11 @@
   lattice export, and the exact log-softmax / glibc fp64 entry points.
 
     python tools/sanitize_smoke.py [V=64] [B=3] [T=12]
+    python tools/sanitize_smoke.py cluster [T=4]
+
+`cluster`: the V = 500 (Vp = 512) cluster kernels only -- the small-batch
+modified beam search (st.async h / logit slices, mbarrier phases) and the
+greedy cluster kernel -- on two streams.
 
 No torch: host buffers through the C ABI only."""
 import os
@@ -24,7 +29,22 @@ from paper_2211_00484_b200.api import (  # noqa: E402
     log_softmax_lse)
 
 
+def cluster_kernels(T):
+    w = init_model_weights(500, 80, 512, 512, 512, seed=0, blank_bias=0.4)
+    dec = Decoder(ModelWeights.from_dict(w))
+    dec.set_encoder(w)
+    enc = dec.encoder_forward(gaussian_features(7100, 2, T, 80), np.array([0, T, 2 * T], np.int32))
+    rag = np.array([0, T, T + max(1, T // 2)], np.int32)
+    enc_r = np.ascontiguousarray(enc[: rag[-1]])
+    dec.beam_search_batch(enc_r, rag, BeamParams(beam_size=4))  # beam_cluster_kernel
+    dec.greedy_search_batch(enc_r, rag)                          # greedy_cluster_kernel
+    dec.close()
+    print("sanitize smoke ok", flush=True)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "cluster":
+        return cluster_kernels(int(sys.argv[2]) if len(sys.argv) > 2 else 4)
     V = int(sys.argv[1]) if len(sys.argv) > 1 else 64
     B = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     T = int(sys.argv[3]) if len(sys.argv) > 3 else 12
