@@ -27,11 +27,13 @@
 #ifndef RNNT_GPU_HPP_
 #define RNNT_GPU_HPP_
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "rnntg.h"
@@ -83,12 +85,29 @@ class Context {
   }
   ~Context() {
     for (Cached& c : graphs_) rnntg_graph_destroy(c.handle);
+    rnntg_host_free(stage_);
     rnntg_model_destroy(h_);
   }
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
   rnntg_model_t handle() const { return h_; }
   int32_t vocab_size() const { return vocab_; }
+
+  // Pinned staging for a call's features, kept across calls (grown, never
+  // shrunk): no page faults on a fresh buffer, one fast asynchronous DMA.
+  float* staging(size_t floats) {
+    if (floats > stage_cap_) {
+      check(rnntg_host_free(stage_));
+      stage_ = nullptr;
+      stage_cap_ = 0;
+      const size_t cap = std::max(floats, stage_cap_ + stage_cap_ / 2);
+      void* p = nullptr;
+      check(rnntg_host_alloc(cap * sizeof(float), &p));
+      stage_ = static_cast<float*>(p);
+      stage_cap_ = cap;
+    }
+    return stage_;
+  }
 
   // The device copy of `graph` (fsa.hpp:54-80), uploaded on first use and
   // reused by content (a 64-bit hash of the CSR, confirmed by Fsa equality).
@@ -134,30 +153,52 @@ class Context {
   rnntg_model_t h_ = nullptr;
   int32_t vocab_ = 0;
   std::vector<Cached> graphs_;
+  float* stage_ = nullptr;
+  size_t stage_cap_ = 0;
 };
 
 namespace detail {
 
-// The batch's features, concatenated, with the reference encoder's
-// validation (model.hpp:226-228); the GPU runs the encoder itself.
+// The batch's features, concatenated into the Context's pinned staging
+// buffer (streams copied by up to 16 threads for large batches), with the
+// reference encoder's validation (model.hpp:226-228); the GPU runs the
+// encoder itself.
 struct Frames {
-  std::vector<float> enc;  // features [sum T][F] (RNNTG_MEM_HOST_FEATURES)
+  const float* enc = nullptr;  // features [sum T][F] (RNNTG_MEM_HOST_FEATURES), pinned
   std::vector<int32_t> splits;
 };
 
-inline Frames encode(const ToyTransducer& m, const std::vector<Mat<float>>& batch) {
+inline Frames encode(Context& ctx, const ToyTransducer& m, const std::vector<Mat<float>>& batch) {
   check_model_shapes(m);
   Frames f;
+  f.splits.reserve(batch.size() + 1);
   f.splits.push_back(0);
-  size_t n = 0;
-  for (const Mat<float>& x : batch) n += x.data.size();
-  f.enc.reserve(std::max<size_t>(1, n));
-  for (const Mat<float>& x : batch) {
+  std::vector<size_t> off(batch.size() + 1, 0);
+  for (size_t i = 0; i < batch.size(); ++i) {
+    const Mat<float>& x = batch[i];
     if (x.cols != m.cfg.feat_dim) throw ValidationError("features must have feat_dim columns");
-    f.enc.insert(f.enc.end(), x.data.begin(), x.data.end());
     f.splits.push_back(f.splits.back() + x.rows);
+    off[i + 1] = off[i] + x.data.size();
   }
-  if (f.enc.empty()) f.enc.push_back(0.0f);
+  float* dst = ctx.staging(std::max<size_t>(1, off.back()));
+  if (off.back() == 0) dst[0] = 0.0f;
+  const size_t nb = batch.size();
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nth = off.back() * sizeof(float) < (8u << 20) ? 1 : std::min<size_t>({16, hw, nb});
+  auto copy = [&](size_t w) {
+    for (size_t i = w; i < nb; i += nth)
+      if (!batch[i].data.empty()) std::memcpy(dst + off[i], batch[i].data.data(), batch[i].data.size() * sizeof(float));
+  };
+  if (nth <= 1) {
+    copy(0);
+  } else {
+    std::vector<std::thread> th;
+    th.reserve(nth - 1);
+    for (size_t w = 1; w < nth; ++w) th.emplace_back(copy, w);
+    copy(0);
+    for (std::thread& t : th) t.join();
+  }
+  f.enc = dst;
   return f;
 }
 
@@ -176,10 +217,10 @@ inline std::vector<std::vector<int32_t>> greedy_search_batch(
     int32_t max_symbols = 1) {
   if (max_symbols != 1)
     throw ValidationError("greedy_search_batch supports max_symbols = 1 only");
-  detail::Frames f = detail::encode(m, batch);
+  detail::Frames f = detail::encode(ctx, m, batch);
   const int32_t B = static_cast<int32_t>(batch.size());
   std::vector<int32_t> splits(B + 1), toks(std::max<int32_t>(1, f.splits.back()));
-  check(rnntg_greedy_search_batch(ctx.handle(), f.enc.data(), f.splits.data(), B, max_symbols,
+  check(rnntg_greedy_search_batch(ctx.handle(), f.enc, f.splits.data(), B, max_symbols,
                                   RNNTG_MEM_HOST_FEATURES, splits.data(), toks.data()));
   return detail::unpack(splits, toks);
 }
@@ -190,12 +231,12 @@ inline std::vector<std::vector<int32_t>> greedy_search_batched(
     Context& ctx, const ToyTransducer& m, const std::vector<Mat<float>>& batch,
     int32_t max_symbols, int64_t* capped_frames = nullptr) {
   if (max_symbols < 1) throw ValidationError("max_symbols must be >= 1");
-  detail::Frames f = detail::encode(m, batch);
+  detail::Frames f = detail::encode(ctx, m, batch);
   const int32_t B = static_cast<int32_t>(batch.size());
   const int64_t cap = max_symbols == kNoSymbolLimit ? kMaxSymbolsPerFrameSafety : max_symbols;
   std::vector<int32_t> splits(B + 1), toks(std::max<int64_t>(1, f.splits.back() * cap));
   int64_t capped = 0;
-  check(rnntg_greedy_search(ctx.handle(), f.enc.data(), f.splits.data(), B, max_symbols,
+  check(rnntg_greedy_search(ctx.handle(), f.enc, f.splits.data(), B, max_symbols,
                             RNNTG_MEM_HOST_FEATURES, splits.data(), toks.data(), &capped));
   if (capped_frames) *capped_frames = capped;
   return detail::unpack(splits, toks);
@@ -212,7 +253,7 @@ inline std::vector<std::vector<int32_t>> beam_search_batch(
     const SearchParams& params, std::vector<double>* scores = nullptr) {
   if (params.max_symbols < 1) throw ValidationError("max_symbols must be >= 1");
   if (params.beam_size < 1) throw ValidationError("beam_size must be >= 1");
-  detail::Frames f = detail::encode(m, batch);
+  detail::Frames f = detail::encode(ctx, m, batch);
   const int32_t B = static_cast<int32_t>(batch.size());
   rnntg_beam_params p{params.beam_size, params.max_symbols,
                       params.merge_op == MergeOp::kLogAdd ? RNNTG_MERGE_LOG_ADD : RNNTG_MERGE_MAX,
@@ -220,7 +261,7 @@ inline std::vector<std::vector<int32_t>> beam_search_batch(
   const int64_t cap = params.max_symbols == kNoSymbolLimit ? kMaxSymbolsPerFrameSafety : params.max_symbols;
   std::vector<int32_t> splits(B + 1), toks(std::max<int64_t>(1, f.splits.back() * cap));
   std::vector<double> sc(std::max<int32_t>(1, B));
-  check(rnntg_beam_search_batch(ctx.handle(), f.enc.data(), f.splits.data(), B, &p,
+  check(rnntg_beam_search_batch(ctx.handle(), f.enc, f.splits.data(), B, &p,
                                 RNNTG_MEM_HOST_FEATURES, splits.data(), toks.data(), sc.data()));
   if (scores) scores->assign(sc.begin(), sc.begin() + B);
   return detail::unpack(splits, toks);
@@ -239,12 +280,12 @@ inline std::vector<std::vector<int32_t>> fsa_best_sequences(
     const Fsa& graph, const FsaSearchParams& params,
     std::vector<double>* scores = nullptr) {
   rnntg_graph_t g = ctx.graph(graph);
-  detail::Frames f = detail::encode(m, batch);
+  detail::Frames f = detail::encode(ctx, m, batch);
   const int32_t B = static_cast<int32_t>(batch.size());
   rnntg_fsa_params p{params.beam, params.max_states, params.max_contexts};
   std::vector<int32_t> splits(B + 1), toks(std::max<int32_t>(1, f.splits.back()));
   std::vector<double> sc(std::max<int32_t>(1, B));
-  check(rnntg_fsa_beam_search(ctx.handle(), f.enc.data(), f.splits.data(), B, g, &p,
+  check(rnntg_fsa_beam_search(ctx.handle(), f.enc, f.splits.data(), B, g, &p,
                               RNNTG_MEM_HOST_FEATURES, splits.data(), toks.data(), sc.data()));
   if (scores) scores->assign(sc.begin(), sc.begin() + B);
   return detail::unpack(splits, toks);

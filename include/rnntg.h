@@ -296,6 +296,14 @@ typedef struct {
   const float* enc_b2;   /* [D]    */
 } rnntg_encoder_desc;
 
+/* Page-locked (pinned) host memory for staging inputs and outputs: a copy
+ * from it is one DMA at full PCIe / C2C speed and stays asynchronous
+ * (cudaHostAlloc, portable).  No reference counterpart: the C++ drop-in
+ * (rnnt_gpu.hpp) gathers a batch's features into one such buffer per
+ * Context instead of a fresh pageable vector per call. */
+rnntg_status rnntg_host_alloc(size_t bytes, void** out);
+rnntg_status rnntg_host_free(void* ptr);
+
 rnntg_status rnntg_model_set_encoder(rnntg_model_t model,
                                      const rnntg_encoder_desc* desc);
 /* feats: [frame_splits[B]][F]; enc_out: [frame_splits[B]][D].  `mem` says

@@ -589,6 +589,28 @@ rnntg_status rnntg_model_create(const rnntg_model_desc* desc, int32_t device,
   return RNNTG_OK;
 }
 
+rnntg_status rnntg_host_alloc(size_t bytes, void** out) {
+  if (!out) return invalid("null argument");
+  *out = nullptr;
+  if (bytes == 0) return RNNTG_OK;
+  if (cudaHostAlloc(out, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    set_error("cudaHostAlloc failed");
+    return RNNTG_CUDA_ERROR;
+  }
+  return RNNTG_OK;
+}
+
+rnntg_status rnntg_host_free(void* ptr) {
+  if (ptr && cudaFreeHost(ptr) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("cudaFreeHost failed");
+    return RNNTG_CUDA_ERROR;
+  }
+  return RNNTG_OK;
+}
+
 rnntg_status rnntg_model_destroy(rnntg_model_t h) {
   if (!h) return RNNTG_OK;
   {
