@@ -227,6 +227,16 @@ template <typename Launch>
 rnntg_status run_sliced(rnntg_model_t h, const float* enc, const int32_t* fs, int32_t B, int32_t mem,
                         int64_t* launches, Launch&& launch) {
   const int32_t D = h->d.D, J = h->d.J, T = fs[1] - fs[0];
+  // RNNTG_MEM_HOST_FEATURES: the slices carry acoustic features; the two
+  // encoder layers of a slice run (row groups) in front of its K1
+  const bool feat = mem == RNNTG_MEM_HOST_FEATURES;
+  const int32_t F = h->d.F, Dp = round_up(D, 128);
+  const int64_t total = static_cast<int64_t>(B) * T;
+  if (feat) {
+    RNNTG_CUDA_TRY(h->feat.ensure(sizeof(float) * std::max<int64_t>(1, total) * F));
+    RNNTG_CUDA_TRY(h->hid.ensure(sizeof(float) * std::max<int64_t>(1, total) * D));
+    RNNTG_CUDA_TRY(h->fenc.ensure(sizeof(float) * std::max<int64_t>(1, total) * D));
+  }
   std::vector<int32_t> cut{0};
   for (int32_t len = h->slice_first; cut.back() < T; len = std::min(2 * len, std::max(h->slice_first, h->slice_max)))
     cut.push_back(std::min(T, cut.back() + len));
@@ -242,9 +252,17 @@ rnntg_status run_sliced(rnntg_model_t h, const float* enc, const int32_t* fs, in
   RNNTG_CUDA_TRY(cudaEventRecord(h->ev[0], h->stream));
   RNNTG_CUDA_TRY(cudaStreamWaitEvent(cs, h->ev[0], 0));  // the previous call is done with h->enc
   const size_t pitch = sizeof(float) * static_cast<size_t>(T) * D;
-  const float* d_enc = mem == RNNTG_MEM_HOST ? h->enc.as<float>() : enc;
+  const float* d_enc = feat ? h->fenc.as<float>() : mem == RNNTG_MEM_HOST ? h->enc.as<float>() : enc;
   for (int k = 0; k < nsl; ++k) {
     const int32_t f0 = cut[k], nf = cut[k + 1] - cut[k];
+    if (feat) {
+      const size_t fp = sizeof(float) * static_cast<size_t>(T) * F;
+      RNNTG_CUDA_TRY(cudaMemcpy2DAsync(h->feat.as<float>() + static_cast<int64_t>(f0) * F, fp,
+                                       enc + static_cast<int64_t>(f0) * F, fp, sizeof(float) * static_cast<size_t>(nf) * F,
+                                       B, cudaMemcpyHostToDevice, cs));
+      RNNTG_CUDA_TRY(cudaEventRecord(h->slice_ev[k], cs));
+      continue;
+    }
     if (mem != RNNTG_MEM_HOST) {  // frames already resident: the slice is ready now
       RNNTG_CUDA_TRY(cudaEventRecord(h->slice_ev[k], cs));
       continue;
@@ -274,6 +292,17 @@ rnntg_status run_sliced(rnntg_model_t h, const float* enc, const int32_t* fs, in
     // delaying decode k-1's start.
     if (ks != h->stream && h->slice_throttle > 0 && k >= 1 + h->slice_throttle)
       RNNTG_CUDA_TRY(cudaStreamWaitEvent(ks, h->k1_ev[nsl + k - 1 - h->slice_throttle], 0));
+    if (feat) {  // encoder_forward (model.hpp:224-238) of the slice: two affine + tanh layers
+      RNNTG_CUDA_TRY(rnntg::launch_gemm_exact_grouped(
+          h->feat.as<float>() + static_cast<int64_t>(f0) * F, F, h->d.enc_w1t, Dp, h->d.enc_b1,
+          h->hid.as<float>() + static_cast<int64_t>(f0) * D, D, static_cast<int64_t>(B) * nf, D, F, true, nullptr, 0, 0,
+          nf, T, ks));
+      RNNTG_CUDA_TRY(rnntg::launch_gemm_exact_grouped(
+          h->hid.as<float>() + static_cast<int64_t>(f0) * D, D, h->d.enc_w2t, Dp, h->d.enc_b2,
+          h->fenc.as<float>() + static_cast<int64_t>(f0) * D, D, static_cast<int64_t>(B) * nf, D, D, true, nullptr, 0, 0,
+          nf, T, ks));
+      *launches += 2;
+    }
     RNNTG_CUDA_TRY(rnntg::launch_gemm_exact_grouped(d_enc + static_cast<int64_t>(f0) * D, D, h->d.j_wet, h->d.Jp,
                                                     nullptr, h->pe.as<float>() + static_cast<int64_t>(f0) * J, J,
                                                     static_cast<int64_t>(B) * nf, J, D, false, nullptr, 0, 0, nf,
@@ -773,7 +802,21 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
   if (!out_splits) return invalid("out_splits is null");
   std::lock_guard<std::mutex> lk(h->mu);
   int32_t out_mem = mem;
-  if ((st = frames_from(h, enc, fs, B, mem, out_mem))) return st;
+  // Host features of a uniform batch that will be decoded in time slices:
+  // the encoder runs per slice inside run_sliced (copies, encoder, K1 and
+  // decode overlap) instead of all up front.
+  bool feat_sliced = false;
+  if (mem == RNNTG_MEM_HOST_FEATURES && B > 0 && p->max_symbols == 1 && h->joiner_mode == RNNTG_JOINER_EXACT &&
+      h->sliced > 0 && h->d.F > 0 && fs[1] - fs[0] > h->slice_first) {
+    bool uni = true;
+    for (int32_t i = 1; i < B; ++i) uni = uni && fs[i + 1] - fs[i] == fs[1] - fs[0];
+    feat_sliced = uni && !(h->beam_cluster && rnntg::beam_cluster_streams(h->d, B, p->beam_size, h->num_sms) > 0);
+  }
+  if (feat_sliced) {
+    out_mem = RNNTG_MEM_HOST;
+  } else if ((st = frames_from(h, enc, fs, B, mem, out_mem))) {
+    return st;
+  }
   RNNTG_CUDA_TRY(cudaSetDevice(h->device));
   // S > 1 (search.hpp:228-235): up to `cap` sub-steps per frame, cap = 10
   // for kNoSymbolLimit (frames stopped by it counted in the stats).
@@ -788,7 +831,7 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
     rnntg_model_t h;
     ~SlotReset() { h->slot_mult = 1; }
   } slot_reset{h};
-  if ((st = prepare(h, fs, B, mem))) return st;
+  if ((st = prepare(h, fs, B, feat_sliced ? RNNTG_MEM_DEVICE : mem))) return st;
   int64_t launches = 0;
   if (B > 0 && cap > 1) {
     RNNTG_CUDA_TRY(h->pool.ensure(sizeof(int32_t) * 2 * (static_cast<int64_t>(fs[B]) * cap + B) * rnntg::kMaxBeam));
@@ -864,8 +907,9 @@ rnntg_status rnntg_beam_search_batch(rnntg_model_t h, const float* enc,
       if (st) return st;
       return finish(h, fs, B, out_mem, out_splits, out_tokens, out_scores, launches);
     }
-    const bool sliced = exact && uniform && fs[1] - fs[0] > h->slice_first &&
-                        ((mem == RNNTG_MEM_HOST && h->sliced > 0) || (mem == RNNTG_MEM_DEVICE && h->sliced > 1));
+    const bool sliced = feat_sliced || (exact && uniform && fs[1] - fs[0] > h->slice_first &&
+                                        ((mem == RNNTG_MEM_HOST && h->sliced > 0) ||
+                                         (mem == RNNTG_MEM_DEVICE && h->sliced > 1)));
     if (sliced) {
       st = run_sliced(h, enc, fs, B, mem, &launches, [&](int32_t t0, int32_t t1, cudaStream_t cs) {
         rnntg::DecodeArgs a = args(0, B);
