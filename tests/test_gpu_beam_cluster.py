@@ -4,8 +4,8 @@ shared memory, rows reduced where their slices land, beam steps on CTA 0)
 against the persistent kernel (RNNTG_BEAM_CLUSTER=0) and the oracle:
 identical tokens, bit-equal scores, for ragged batches, every beam width,
 both merge ops, length normalisation and the symbol cap, and at the
-batch sizes where the cluster kernel takes over (up to 18 clusters x 64 /
-beam streams)."""
+batch sizes where the cluster kernel takes over (up to 15 resident clusters
+x min(14, 64 / beam) streams)."""
 import numpy as np
 import pytest
 
@@ -45,16 +45,17 @@ def test_cluster_matches_persistent_and_oracle(beam, merge, lnorm, cap):
     H.assert_scores_equal(gsc, osc)
 
 
-@pytest.mark.parametrize("B", [15, 150, 180])
-def test_cluster_batch_sizes(B):
-    """One stream per cluster; 10; 12 per cluster (up to 48 joiner rows a
-    frame: two h / GEMM passes)."""
+@pytest.mark.parametrize("B,beam", [(15, 4), (150, 4), (180, 4), (210, 4), (120, 8)])
+def test_cluster_batch_sizes(B, beam):
+    """One stream per cluster; 10; 12; 14 per cluster (up to 56 joiner rows
+    a frame: two h / GEMM passes); beam 8 at 8 per cluster (up to 64 rows:
+    two full passes)."""
     from paper_2211_00484_b200.api import BeamParams
 
     m = H.model(V=500, seed=4, blank_bias=0.2)
     rng = np.random.default_rng(B)
     Ts = rng.integers(1, 24, B).tolist()
     _, enc, splits = H.frames(m, Ts, seed0=7000 + B)
-    (got, gsc), (want, wsc) = _both(m, enc, splits, BeamParams(beam_size=4))
+    (got, gsc), (want, wsc) = _both(m, enc, splits, BeamParams(beam_size=beam))
     assert got == want
     H.assert_scores_equal(gsc, wsc)
