@@ -1596,14 +1596,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 1)
           S.R = Rn;
           S.stat[1] += R;
         }
-#ifdef RNNTG_BC_PD_PREFETCH
-        // the next frame's decoder-table rows into L2 (each CTA gathers a
-        // 256-byte segment of every row): a head start on the h build
-        for (int x = lane; x < Rn * (m.J / 32); x += 32) {
-          const int r = x / (m.J / 32), l = x - r * (m.J / 32);
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(m.pd + static_cast<int64_t>(S.row_ctx[r]) * m.J + l * 32));
-        }
-#endif
       }
     }
     const long long cf = clock64();
