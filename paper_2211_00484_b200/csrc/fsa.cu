@@ -184,15 +184,24 @@ struct LpRows {
   __device__ __forceinline__ double lp(int row, int label) const { return P[static_cast<int64_t>(row) * V + label]; }
 };
 
+// The active tuple whose candidate segment holds q: the last i < n_act with
+// act_off[i] <= q (act_off[0] = 0, strictly increasing), by binary lifting
+// over kMaxStates -- a fixed, unrolled sequence of predicated loads, so a
+// thread's kU lookups interleave instead of running data-dependent loops.
+__device__ __forceinline__ int seg_of(const FsaStream& S, int q) {
+  int lo = 0;
+#pragma unroll
+  for (int step = kMaxStates / 2; step > 0; step >>= 1) {
+    const int mid = lo + step;
+    if (mid < S.n_act && S.act_off[mid] <= q) lo = mid;
+  }
+  return lo;
+}
+
 template <class Src>
 __device__ __forceinline__ Raw raw_cand(const FsaStream& S, int q, const ArcRec* __restrict__ arcs, const Src& src,
                                         int V) {
-  int lo = 0, hi = S.n_act - 1;  // last i with act_off[i] <= q
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (S.act_off[mid] <= q) lo = mid;
-    else hi = mid - 1;
-  }
+  const int lo = seg_of(S, q);
   Raw r;
   r.i = lo;
   const int row = S.row_base + S.act_row[lo];
@@ -228,12 +237,7 @@ __device__ __forceinline__ void raw_batch(const FsaStream& S, int q0, int stride
   for (int u = 0; u < kU; ++u) {
     const int q = q0 + u * stride;
     ok[u] = q < nraw;
-    int lo = 0, hi = S.n_act - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (S.act_off[mid] <= q) lo = mid;
-      else hi = mid - 1;
-    }
+    const int lo = seg_of(S, q);
     ii[u] = lo;
     jj[u] = ok[u] ? q - S.act_off[lo] : 0;
   }
