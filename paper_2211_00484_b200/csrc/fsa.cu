@@ -498,12 +498,12 @@ __device__ __forceinline__ void fsa_frame(FsaStream& S, const Group& grp, const 
         const int p = grp.tid;
         int fo = p;
         if (p < npass) {
+          // first q < p with the same context: a fixed-trip scan (no early
+          // exit), so the shared-memory loads pipeline; the lowest match wins
           const int32_t c = static_cast<int32_t>(S.hkey[p] >> 32);
-          for (int q = 0; q < p; ++q)
-            if (static_cast<int32_t>(S.hkey[q] >> 32) == c) {
-              fo = q;
-              break;
-            }
+#pragma unroll 8
+          for (int q = npass - 1; q >= 0; --q)
+            if (q < p && static_cast<int32_t>(S.hkey[q] >> 32) == c) fo = q;
           if (fo == p) atomicOr(&S.m_first, 1ull << p);
         }
         grp.sync();
