@@ -1,8 +1,10 @@
 """Small-batch greedy on thread-block clusters (cluster.cu: out_w column
-slices resident in 8 CTAs' shared memory, DSMEM first-max combine) against
-the compiled reference and against the persistent single-CTA kernel, across
-the batch sizes where the cluster kernel is chosen (<= 144 streams) and
-just beyond it."""
+slices resident in 8 CTAs' shared memory, h slices and slice maxima
+exchanged by st.async on mbarriers, next-frame h rows built ahead and
+rebuilt after an emission) against the compiled reference and against the
+persistent single-CTA kernel, across the batch sizes where the cluster
+kernel is chosen (<= 144 streams) and just beyond it, at a low and a high
+emission rate (the rebuild path on most frames)."""
 import os
 
 import numpy as np
@@ -27,9 +29,10 @@ def _decoder(m, on):
             os.environ["RNNTG_GREEDY_CLUSTER"] = old
 
 
-@pytest.mark.parametrize("B", [1, 7, 8, 19, 144, 150])
-def test_greedy_cluster_matches_reference_and_plain_kernel(B):
-    m = H.model(V=500, seed=3, blank_bias=0.2)
+@pytest.mark.parametrize("B,bias", [(1, 0.2), (7, 0.2), (8, 0.2), (19, 0.2), (144, 0.2), (150, 0.2), (8, -3.0),
+                                    (40, -3.0)])
+def test_greedy_cluster_matches_reference_and_plain_kernel(B, bias):
+    m = H.model(V=500, seed=3, blank_bias=bias)
     Ts = [int(x) for x in np.random.default_rng(B).integers(0, 30, B)]
     feats, enc, splits = H.frames(m, Ts, seed0=7000 + B)
     want = m.greedy(feats, splits)
